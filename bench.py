@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""GCOOSpDM benchmark on B200 (driver contract: one JSON line from rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Workload (BASELINE.json configs[1], the metric's configuration): the
+reference's square_benchmark(seed=1) inputs (bench.hpp:168-174) at n=8000,
+sparsity 0.99 — A = generate_uniform_sparse(8000, 0.99, 1) (640,000 nnz), B =
+generate_uniform_sparse(8000, 0, derive_seed(1, 8000, 0xb)) dense fp32,
+ExecConfig{p=4, b=64}.  A step = one spdm_gcoo(A_gcoo, B) -> C.
+
+Multi-GPU (configs[4] decomposition): B and C are column-sharded with A
+replicated; every rank owns an 8000-column block of B/C (weak scaling: per-GPU
+work fixed, the global problem is A[8000x8000] x B[8000 x 8000N]).  There is no
+collective on the data path; NCCL is used for the barrier and the max-over-
+ranks timing only.
+
+value      kernel-only GFLOPS (2*nnz*N / t), operands resident in HBM, L2 flushed
+           (256 MiB write) before every timed launch, CUDA events on the
+           launching stream, max over ranks.
+e2e        the same metric through the public host API (paper_2005_14469_b200.
+           spdm_gcoo -> C ABI gcoo_spdm_f32): pinned host A/B in, pinned host C
+           out, copies inside the timed region.
+--impl reference  times the reference's own CPU spdm_gcoo (oracle/_ref, built
+           from the unmodified reference sources) with all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_DIM = 8000
+SPARSITY = 0.99
+SEED = 1
+P, BW = 4, 64
+METRIC = "GCOOSpDM GFLOPS (2·nnz·N) and HBM GB/s-% roofline at 1/2/4/8 B200 vs CPU ref"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def fp32_peak_tflops():
+    """FFMA peak from this repo's microbenchmark (tools/microbench, profiles/)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_microbench.json")) as f:
+            return float(json.load(f)["ffma_tflops"]), "measured (tools/microbench)"
+    except Exception:
+        return 148 * 128 * 2 * 1.965e9 / 1e12, "derived 148 SM x 128 x 2 x 1.965 GHz"
+
+
+def compulsory_bytes(nnz, m, k, n, p, k_nz):
+    # A triples + group arrays + B rows that are touched + C once
+    return 12 * nnz + 16 * (-(-m // p)) + 4 * k_nz * n + 4 * m * n
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
+                except ValueError:
+                    pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, fl in rows for i, v in enumerate(fl) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def make_inputs(G, n, s, seed, dev, n_cols):
+    """square_benchmark inputs; B/C column block of width n_cols (same B for
+    every rank's block: B is generated once at n x n and tiled)."""
+    import torch
+    a = G.generate_uniform_sparse(n, s, seed)
+    b = G.generate_uniform_sparse(n, 0.0, G.derive_seed(seed, n, 0xB))
+    if n_cols != n:
+        reps = -(-n_cols // n)
+        b = np.ascontiguousarray(np.tile(b, (1, reps))[:, :n_cols])
+    dA = torch.from_numpy(a).to(dev)
+    dg = G.dense_to_gcoo_dev(dA, P)
+    del dA
+    dB = torch.from_numpy(b).to(dev)
+    return a, b, dg, dB
+
+
+def time_kernel(G, dg, dB, dC, steps, warmup, stream, flush):
+    import torch
+    cfg = G.ExecConfig(p=P, b=BW)
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            flush.zero_()
+            G.spdm_gcoo_dev(dg, dB, dC, cfg, stream=stream)
+        torch.cuda.synchronize()
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        l0 = G.launch_count()
+        for i in range(steps):
+            flush.zero_()  # > L2 (126 MB): every timed launch starts cold
+            starts[i].record(stream)
+            G.spdm_gcoo_dev(dg, dB, dC, cfg, stream=stream)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        launches = G.launch_count() - l0
+    times = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    return sum(times) / len(times), min(times), launches
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2005_14469_b200 as G
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    G.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    n, s = args.n, args.sparsity
+    a_host, b_host, dg, dB = make_inputs(G, n, s, SEED, dev, n)
+    nnz = dg.nnz()
+    m = k = n
+    dC = torch.empty((m, n), dtype=torch.float32, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB
+    stream = torch.cuda.Stream(device=dev)
+
+    # ---- kernel-only, device-resident ----------------------------------
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        ms_mean, ms_min, launches = time_kernel(G, dg, dB, dC, args.steps, args.warmup, stream, flush)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([ms_mean, ms_min], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_mean, ms_min = float(t[0]), float(t[1])
+    flops_rank = 2.0 * nnz * n
+    value = world * flops_rank / (ms_mean * 1e-3) / 1e9
+
+    # ---- end to end through the public host API ----------------------
+    g_host = dg.to_host()
+    b_pin = torch.empty((k, n), dtype=torch.float32, pin_memory=True)
+    b_pin.numpy()[:] = b_host
+    c_pin = torch.empty((m, n), dtype=torch.float32, pin_memory=True)
+    def pin(x):
+        t_ = torch.empty(x.shape, dtype=getattr(torch, str(x.dtype)), pin_memory=True)
+        t_.numpy()[...] = x
+        return t_.numpy()
+
+    g_pin = G.GcooMatrix(g_host.rows_dim, g_host.cols_dim, g_host.p, pin(g_host.values), pin(g_host.row_idx),
+                         pin(g_host.col_idx), pin(g_host.g_idxes), pin(g_host.nnz_per_group))
+    cfg = G.ExecConfig(p=P, b=BW)
+    for _ in range(max(1, args.warmup)):
+        G.spdm_gcoo(g_pin, b_pin.numpy(), cfg, out=c_pin.numpy())
+    if world > 1:
+        dist.barrier()
+    e2e_steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        G.spdm_gcoo(g_pin, b_pin.numpy(), cfg, out=c_pin.numpy())
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_s = float(te[0])
+    e2e_value = world * flops_rank / e2e_s / 1e9
+    h2d = g_host.values.nbytes + g_host.row_idx.nbytes + g_host.col_idx.nbytes + g_host.g_idxes.nbytes + \
+        g_host.nnz_per_group.nbytes + b_host.nbytes
+    d2h = m * n * 4
+
+    # C sanity against the reference hash (computed on rank 0 only at n=8000)
+    parity = None
+    if rank == 0 and n == 8000:
+        try:
+            with open(os.path.join(ROOT, "tests", "golden", "hashes.json")) as f:
+                ent = json.load(f)[f"n8000_s{s}"]
+            parity = {"c0": float(dC[0, 0]), "clast": float(dC[-1, -1]),
+                      "c0_ref_fma": ent["C_fma"]["c0"], "clast_ref_fma": ent["C_fma"]["clast"],
+                      "checksum": float(dC.double().sum()), "checksum_ref_fma": ent["C_fma"]["checksum"]}
+            parity["match"] = (parity["c0"] == parity["c0_ref_fma"] and parity["clast"] == parity["clast_ref_fma"]
+                               and abs(parity["checksum"] - parity["checksum_ref_fma"]) < 1e-3)
+        except Exception as e:  # noqa: BLE001
+            parity = {"error": str(e)}
+
+    # ---- roofline --------------------------------------------------------
+    hbm_peak, hbm_src = peaks()
+    k_nz = int(np.count_nonzero(np.bincount(g_host.col_idx, minlength=k)))
+    cb = compulsory_bytes(nnz, m, k, n, P, k_nz)
+    achieved_gbs = cb / (ms_mean * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tr = json.load(f)
+            if tr.get("n") == n and tr.get("sparsity") == s:
+                traffic = tr.get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    fp_peak, fp_src = fp32_peak_tflops()
+    tflops = flops_rank / (ms_mean * 1e-3) / 1e12
+
+    extra = {}
+    if rank == 0 and world == 1 and not args.no_sweep:
+        for s2 in (0.9, 0.995):
+            _, _, dg2, _ = make_inputs(G, n, s2, SEED, dev, n)
+            ms2, _, _ = time_kernel(G, dg2, dB, dC, max(3, args.steps // 2), 2, stream, flush)
+            f2 = 2.0 * dg2.nnz() * n
+            cb2 = compulsory_bytes(dg2.nnz(), m, k, n, P, k)
+            extra[f"s{s2}"] = {"nnz": dg2.nnz(), "ms": round(ms2, 4), "gflops": round(f2 / ms2 / 1e6, 1),
+                               "hbm_frac": round(cb2 / (ms2 * 1e-3) / 1e9 / hbm_peak, 4),
+                               "fp32_frac": round(f2 / (ms2 * 1e-3) / 1e12 / fp_peak, 4)}
+            del dg2
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(g_host, b_host, n)
+
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "GFLOPS",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_mean, 4),
+        "ms_per_step_min": round(ms_min, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic: reference square_benchmark(seed=1) generator, bit-identical inputs",
+        "config": {"workload": f"GCOOSpDM n={n} s={s} uniform-random A x dense B, fp32 (BASELINE configs[1])",
+                   "m": m, "k": k, "n_per_gpu": n, "n_total": n * world, "nnz": nnz, "p": P, "b": BW,
+                   "parallelism": f"column-shard B/C x{world}, A replicated",
+                   "l2": "flushed (256 MiB write) before every timed launch; B+C = 512 MB > L2"},
+        "e2e": {"value": round(e2e_value, 2), "unit": "GFLOPS", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_s * 1e3, 3),
+                "path": "paper_2005_14469_b200.spdm_gcoo -> gcoo_spdm_f32 (pinned host buffers)"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                     "frac": round(achieved_gbs / hbm_peak, 4), "traffic": traffic,
+                     "peak_source": hbm_src, "algorithmic_bytes_per_launch": int(cb)},
+        "roofline_fp32": {"achieved": round(tflops, 3), "peak": round(fp_peak, 2), "unit": "TFLOP/s",
+                          "frac": round(tflops / fp_peak, 4), "peak_source": fp_src,
+                          "note": "the path is an FP32 FFMA gather: this, not HBM, is its binding roofline"},
+        "clocks": clk.summary(),
+        "parity": parity,
+        "sweep": extra,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(g_host, b_host, n):
+    """The reference's own CPU spdm_gcoo (oracle/_ref) on this host's cores."""
+    try:
+        from oracle import Gcoo, Reference, have_reference
+    except Exception as e:  # noqa: BLE001
+        return {"error": f"oracle unavailable: {e}"}
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    g = Gcoo(g_host.rows_dim, g_host.cols_dim, g_host.p, g_host.values, g_host.row_idx, g_host.col_idx,
+             g_host.g_idxes, g_host.nnz_per_group)
+    if have_reference():
+        R = Reference(False)
+        r = R.time_spdm(g, b_host, b=BW, workers=0, warmup=1, reps=3)
+        kc = r["kc_s"]
+        return {"value": round(2.0 * g.nnz * n / kc / 1e9, 3), "unit": "GFLOPS", "cores": int(r["workers"]),
+                "kind": "reference",
+                "sample": f"full workload (n={n}, nnz={g.nnz}): reference spdm_gcoo, median of 3 after 1 warmup, "
+                          f"OpenMP {r['workers']} threads, default-ISA build",
+                "kc_seconds": kc}
+    return {"error": "oracle/_ref not built"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU spdm_gcoo on the same workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import Reference, have_reference
+    if not have_reference():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (reference sources absent)"}))
+        return
+    cores = os.cpu_count() or 1
+    R = Reference(False)
+    n, s = args.n, args.sparsity
+    a = R.uniform_sparse(n, s, SEED)
+    b = R.uniform_sparse(n, 0.0, R.derive_seed(SEED, n, 0xB))
+    g = R.dense_to_gcoo(a, P)
+    r = R.time_spdm(g, b, b=BW, workers=0, warmup=max(0, min(args.warmup, 2)), reps=max(1, args.steps))
+    kc = r["kc_s"]
+    v = 2.0 * g.nnz * n / kc / 1e9
+    line = {
+        "metric": METRIC, "value": round(v, 3), "unit": "GFLOPS", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(kc * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic: reference square_benchmark(seed=1)",
+        "config": {"workload": f"GCOOSpDM n={n} s={s} uniform-random A x dense B, fp32 (BASELINE configs[1])",
+                   "m": n, "k": n, "n_per_gpu": n, "nnz": g.nnz, "p": P, "b": BW},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(v, 3), "unit": "GFLOPS", "cores": int(r["workers"]), "kind": "reference",
+                         "sample": f"full workload each step: reference spdm_gcoo (median of {max(1, args.steps)}),"
+                                   f" OpenMP {r['workers']} threads of {cores}"},
+        "e2e": {"value": round(v, 3), "unit": "GFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=N_DIM)
+    ap.add_argument("--sparsity", type=float, default=SPARSITY)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

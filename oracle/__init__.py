@@ -1,0 +1,289 @@
+"""ctypes front-end for the CPU checker (TEST INFRASTRUCTURE ONLY).
+
+Two back-ends, both built by ``oracle/Makefile``:
+
+* ``Oracle``    — ``oracle/_build/libgcoo_oracle.so``, the plain-C restatement
+  (``gcoo_oracle.c``; every function cites the reference file:line it follows).
+* ``Reference`` — ``oracle/_ref/libgcoo_ref{,_fma}.so``, the unmodified reference
+  library compiled from ``/root/reference/proj`` (``ref_shim.cpp``).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and the ``cpu_baseline`` /
+``--impl reference`` legs of ``bench.py`` may import this package; the CUDA
+product never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "_build", "libgcoo_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libgcoo_ref.so")
+REF_FMA_SO = os.path.join(HERE, "_ref", "libgcoo_ref_fma.so")
+
+_i64, _i32, _u64, _dbl, _vp = C.c_int64, C.c_int32, C.c_uint64, C.c_double, C.c_void_p
+
+
+def build(quiet: bool = True) -> None:
+    """make -C oracle (restatement always; the reference when its sources exist)."""
+    out = subprocess.run(["make", "-C", HERE, "-j4"], capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("oracle build failed:\n" + out.stdout + out.stderr)
+    if not quiet:
+        print(out.stdout)
+
+
+def _p(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(_vp)
+
+
+@dataclass
+class Gcoo:
+    """Host GCOO arrays with the reference's field names (matrix.hpp:176-245)."""
+    rows_dim: int
+    cols_dim: int
+    p: int
+    values: np.ndarray
+    row_idx: np.ndarray
+    col_idx: np.ndarray
+    g_idxes: np.ndarray
+    nnz_per_group: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.values.size)
+
+    @property
+    def groups(self) -> int:
+        return int(self.g_idxes.size)
+
+
+class Oracle:
+    def __init__(self, path: str = ORACLE_SO):
+        if not os.path.exists(path):
+            build()
+        L = self.lib = C.CDLL(path)
+        L.orc_derive_seed.restype = _u64
+        L.orc_derive_seed.argtypes = [_u64, _u64, _u64]
+        L.orc_uniform_sparse_f32.restype = _i64
+        L.orc_uniform_sparse_f32.argtypes = [_i64, _dbl, _u64, _vp]
+        L.orc_uniform_sparse_f64.restype = _i64
+        L.orc_uniform_sparse_f64.argtypes = [_i64, _dbl, _u64, _vp]
+        L.orc_uniform_sparse_coo_f32.restype = _i64
+        L.orc_uniform_sparse_coo_f32.argtypes = [_i64, _dbl, _u64, _vp, _vp, _vp, _i64]
+        L.orc_powerlaw_coo_f32.restype = _i64
+        L.orc_powerlaw_coo_f32.argtypes = [_i64, _dbl, _dbl, _u64, _vp, _vp, _vp, _i64]
+        L.orc_realized_nnz.restype = _i64
+        L.orc_realized_nnz.argtypes = [_i64, _dbl]
+        for t in ("f32", "f64"):
+            f = getattr(L, f"orc_dense_to_gcoo_{t}")
+            f.restype = _i64
+            f.argtypes = [_i64, _i64, _vp, _i32, _vp, _vp, _vp, _vp, _vp]
+            f = getattr(L, f"orc_spdm_gcoo_{t}")
+            f.restype = None
+            f.argtypes = [_i64, _i64, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int]
+        L.orc_coo_to_gcoo_f32.restype = C.c_int
+        L.orc_coo_to_gcoo_f32.argtypes = [_i64, _i64, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.orc_gcoo_validate.restype = C.c_int
+        L.orc_gcoo_validate.argtypes = [_i64, _i64, _i32, _i64, _vp, _vp, _i64, _vp, _vp]
+        L.orc_gcoo_stats.restype = None
+        L.orc_gcoo_stats.argtypes = [_i64, _i32, _i64, _vp, _vp, _vp, _vp]
+        L.orc_spdm_gcoo_rows_f32.restype = None
+        L.orc_spdm_gcoo_rows_f32.argtypes = [_i64, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, C.c_int]
+        L.orc_fnv1a32.restype = C.c_uint32
+        L.orc_fnv1a32.argtypes = [_vp, _i64]
+
+    # -- inputs -------------------------------------------------------------
+    def derive_seed(self, base: int, a: int, b: int = 0) -> int:
+        return int(self.lib.orc_derive_seed(base, a, b))
+
+    def uniform_sparse(self, n: int, s: float, seed: int, dtype=np.float32) -> np.ndarray:
+        out = np.empty((n, n), dtype=dtype)
+        f = self.lib.orc_uniform_sparse_f32 if dtype == np.float32 else self.lib.orc_uniform_sparse_f64
+        f(n, s, seed, _p(out))
+        return out
+
+    def uniform_sparse_coo(self, n: int, s: float, seed: int):
+        nnz = int(self.lib.orc_realized_nnz(n, s))
+        v = np.empty(nnz, np.float32); r = np.empty(nnz, np.int32); c = np.empty(nnz, np.int32)
+        got = self.lib.orc_uniform_sparse_coo_f32(n, s, seed, _p(v), _p(r), _p(c), nnz)
+        assert got == nnz
+        return v, r, c
+
+    def powerlaw_coo(self, n: int, s: float, alpha: float, seed: int):
+        nnz = int(self.lib.orc_realized_nnz(n, s))
+        v = np.empty(nnz, np.float32); r = np.empty(nnz, np.int32); c = np.empty(nnz, np.int32)
+        got = self.lib.orc_powerlaw_coo_f32(n, s, alpha, seed, _p(v), _p(r), _p(c), nnz)
+        assert got == nnz, got
+        return v, r, c
+
+    # -- construction -------------------------------------------------------
+    def dense_to_gcoo(self, a: np.ndarray, p: int) -> Gcoo:
+        m, k = a.shape
+        a = np.ascontiguousarray(a)
+        cap = int(np.count_nonzero(a))
+        g = -(-m // p) if p > 0 else 0
+        vals = np.empty(cap, a.dtype); rows = np.empty(cap, np.int32); cols = np.empty(cap, np.int32)
+        gi = np.empty(max(g, 1), np.int64); gn = np.empty(max(g, 1), np.int64)
+        f = self.lib.orc_dense_to_gcoo_f32 if a.dtype == np.float32 else self.lib.orc_dense_to_gcoo_f64
+        nnz = f(m, k, _p(a), p, _p(vals), _p(rows), _p(cols), _p(gi), _p(gn))
+        if nnz < 0:
+            raise ValueError("dense_to_gcoo: p must be a power of two")
+        return Gcoo(m, k, p, vals, rows, cols, gi[:g], gn[:g])
+
+    def coo_to_gcoo(self, m, k, vals, rows, cols, p) -> Gcoo:
+        nnz = vals.size
+        g = -(-m // p) if p > 0 else 1
+        ov = np.empty(nnz, np.float32); orr = np.empty(nnz, np.int32); oc = np.empty(nnz, np.int32)
+        gi = np.empty(max(g, 1), np.int64); gn = np.empty(max(g, 1), np.int64)
+        bad = C.c_int64(-1)
+        rc = self.lib.orc_coo_to_gcoo_f32(m, k, nnz, _p(vals), _p(rows), _p(cols), p, _p(ov), _p(orr), _p(oc),
+                                          _p(gi), _p(gn), C.byref(bad))
+        if rc == -1:
+            raise ValueError("coo_to_gcoo: p must be a power of two")
+        if rc == -2:
+            raise ValueError(f"CooMatrix: invalid entry {bad.value}")
+        return Gcoo(m, k, p, ov, orr, oc, gi[:g], gn[:g])
+
+    def validate(self, g: Gcoo) -> int:
+        return int(self.lib.orc_gcoo_validate(g.rows_dim, g.cols_dim, g.p, g.nnz, _p(g.row_idx), _p(g.col_idx),
+                                              g.groups, _p(g.g_idxes), _p(g.nnz_per_group)))
+
+    # -- multiply -----------------------------------------------------------
+    def spdm(self, g: Gcoo, B: np.ndarray, b: int = 64, fma: bool = True):
+        k, n = B.shape
+        Cm = np.empty((g.rows_dim, n), dtype=B.dtype)
+        st = (_u64 * 4)()
+        f = self.lib.orc_spdm_gcoo_f32 if B.dtype == np.float32 else self.lib.orc_spdm_gcoo_f64
+        f(g.rows_dim, k, n, g.p, b, _p(g.values), _p(g.row_idx), _p(g.col_idx), _p(g.g_idxes),
+          _p(g.nnz_per_group), _p(np.ascontiguousarray(B)), _p(Cm), st, int(fma))
+        return Cm, tuple(int(x) for x in st)
+
+    def spdm_rows(self, g: Gcoo, B: np.ndarray, r0: int, r1: int, b: int = 64, fma: bool = True) -> np.ndarray:
+        k, n = B.shape
+        Cm = np.zeros((g.rows_dim, n), dtype=np.float32)
+        self.lib.orc_spdm_gcoo_rows_f32(g.rows_dim, n, g.p, b, _p(g.values), _p(g.row_idx), _p(g.col_idx),
+                                        _p(g.g_idxes), _p(g.nnz_per_group), _p(np.ascontiguousarray(B)),
+                                        _p(Cm), r0, r1, int(fma))
+        return Cm
+
+    def stats(self, g: Gcoo, n: int, b: int):
+        st = (_u64 * 4)()
+        self.lib.orc_gcoo_stats(n, b, g.groups, _p(g.col_idx), _p(g.g_idxes), _p(g.nnz_per_group), st)
+        return tuple(int(x) for x in st)
+
+    def fnv(self, a: np.ndarray) -> str:
+        a = np.ascontiguousarray(a)
+        return "%08x" % self.lib.orc_fnv1a32(_p(a), a.nbytes)
+
+
+class Reference:
+    """The reference library itself (fma=False: as shipped; fma=True: -mfma)."""
+
+    def __init__(self, fma: bool = False):
+        path = REF_FMA_SO if fma else REF_SO
+        if not os.path.exists(path):
+            raise FileNotFoundError(path + " (build with make -C oracle while /root/reference exists)")
+        L = self.lib = C.CDLL(path)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_derive_seed.restype = _u64
+        L.ref_derive_seed.argtypes = [_u64, _u64, _u64]
+        L.ref_uniform_sparse_f32.restype = C.c_int
+        L.ref_uniform_sparse_f32.argtypes = [_i64, _dbl, _u64, _vp]
+        L.ref_uniform_sparse_f64.restype = C.c_int
+        L.ref_uniform_sparse_f64.argtypes = [_i64, _dbl, _u64, _vp]
+        for t in ("f32", "f64"):
+            f = getattr(L, f"ref_dense_to_gcoo_{t}")
+            f.restype = _i64
+            f.argtypes = [_i64, _i64, _vp, _i32, _vp, _vp, _vp, _vp, _vp]
+            f = getattr(L, f"ref_spdm_gcoo_{t}")
+            f.restype = C.c_int
+            f.argtypes = [_i64, _i64, _i64, _i32, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp,
+                          C.c_int, _vp, _i64]
+            f = getattr(L, f"ref_gemm_oracle_{t}")
+            f.restype = C.c_int
+            f.argtypes = [_i64, _i64, _i64, _vp, _vp, _vp]
+        L.ref_coo_to_gcoo_f32.restype = C.c_int
+        L.ref_coo_to_gcoo_f32.argtypes = [_i64, _i64, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp]
+        L.ref_run_benchmark_gcoo_f32.restype = C.c_int
+        L.ref_run_benchmark_gcoo_f32.argtypes = [_i64, _vp, _vp, _i32, _i32, C.c_int, C.c_int, C.c_int, _vp]
+        L.ref_time_spdm_gcoo_f32.restype = C.c_int
+        L.ref_time_spdm_gcoo_f32.argtypes = [_i64, _i64, _i64, _i32, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp,
+                                             _vp, C.c_int, C.c_int, C.c_int, _vp]
+
+    def _check(self, rc: int):
+        if rc == 1:
+            raise ValueError(self.lib.ref_last_error().decode())
+        if rc != 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+
+    def uniform_sparse(self, n, s, seed, dtype=np.float32):
+        out = np.empty((n, n), dtype=dtype)
+        f = self.lib.ref_uniform_sparse_f32 if dtype == np.float32 else self.lib.ref_uniform_sparse_f64
+        self._check(f(n, s, seed, _p(out)))
+        return out
+
+    def derive_seed(self, base, a, b=0):
+        return int(self.lib.ref_derive_seed(base, a, b))
+
+    def dense_to_gcoo(self, a: np.ndarray, p: int) -> Gcoo:
+        m, k = a.shape
+        a = np.ascontiguousarray(a)
+        f = self.lib.ref_dense_to_gcoo_f32 if a.dtype == np.float32 else self.lib.ref_dense_to_gcoo_f64
+        nnz = f(m, k, _p(a), p, None, None, None, None, None)
+        if nnz < 0:
+            raise ValueError(self.lib.ref_last_error().decode())
+        g = -(-m // p)
+        vals = np.empty(nnz, a.dtype); rows = np.empty(nnz, np.int32); cols = np.empty(nnz, np.int32)
+        gi = np.empty(g, np.int64); gn = np.empty(g, np.int64)
+        f(m, k, _p(a), p, _p(vals), _p(rows), _p(cols), _p(gi), _p(gn))
+        return Gcoo(m, k, p, vals, rows, cols, gi, gn)
+
+    def coo_to_gcoo(self, m, k, vals, rows, cols, p) -> Gcoo:
+        nnz = vals.size
+        g = -(-m // p) if p > 0 else 1
+        ov = np.empty(nnz, np.float32); orr = np.empty(nnz, np.int32); oc = np.empty(nnz, np.int32)
+        gi = np.empty(max(g, 1), np.int64); gn = np.empty(max(g, 1), np.int64)
+        self._check(self.lib.ref_coo_to_gcoo_f32(m, k, nnz, _p(vals), _p(rows), _p(cols), p, _p(ov), _p(orr),
+                                                 _p(oc), _p(gi), _p(gn)))
+        return Gcoo(m, k, p, ov, orr, oc, gi[:g], gn[:g])
+
+    def spdm(self, g: Gcoo, B: np.ndarray, b: int = 64, workers: int = 0, tile_order=None):
+        k, n = B.shape
+        Cm = np.empty((g.rows_dim, n), dtype=B.dtype)
+        st = (_u64 * 4)()
+        f = self.lib.ref_spdm_gcoo_f32 if B.dtype == np.float32 else self.lib.ref_spdm_gcoo_f64
+        to = None if tile_order is None else np.ascontiguousarray(tile_order, dtype=np.int64)
+        self._check(f(g.rows_dim, k, n, g.p, b, g.nnz, _p(g.values), _p(g.row_idx), _p(g.col_idx), g.groups,
+                      _p(g.g_idxes), _p(g.nnz_per_group), _p(np.ascontiguousarray(B)), _p(Cm), st, workers,
+                      _p(to), 0 if to is None else to.size))
+        return Cm, tuple(int(x) for x in st)
+
+    def gemm_oracle(self, A: np.ndarray, B: np.ndarray) -> np.ndarray:
+        m, k = A.shape
+        n = B.shape[1]
+        Cm = np.empty((m, n), dtype=A.dtype)
+        f = self.lib.ref_gemm_oracle_f32 if A.dtype == np.float32 else self.lib.ref_gemm_oracle_f64
+        self._check(f(m, k, n, _p(np.ascontiguousarray(A)), _p(np.ascontiguousarray(B)), _p(Cm)))
+        return Cm
+
+    def run_benchmark_gcoo(self, A: np.ndarray, B: np.ndarray, p=4, b=64, workers=0, warmup=1, reps=5):
+        out = (_dbl * 5)()
+        self._check(self.lib.ref_run_benchmark_gcoo_f32(A.shape[0], _p(A), _p(B), p, b, workers, warmup, reps, out))
+        return dict(eo_s=out[0], kc_s=out[1], gflops=out[2], workers=int(out[3]), nnz=int(out[4]))
+
+    def time_spdm(self, g: Gcoo, B: np.ndarray, b=64, workers=0, warmup=1, reps=5):
+        out = (_dbl * 2)()
+        k, n = B.shape
+        self._check(self.lib.ref_time_spdm_gcoo_f32(g.rows_dim, k, n, g.p, b, g.nnz, _p(g.values), _p(g.row_idx),
+                                                    _p(g.col_idx), g.groups, _p(g.g_idxes), _p(g.nnz_per_group),
+                                                    _p(np.ascontiguousarray(B)), workers, warmup, reps, out))
+        return dict(kc_s=out[0], workers=int(out[1]))
+
+
+def have_reference() -> bool:
+    return os.path.exists(REF_SO) and os.path.exists(REF_FMA_SO)

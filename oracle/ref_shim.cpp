@@ -1,0 +1,243 @@
+// ref_shim.cpp — C entry points over the UNMODIFIED reference library.
+//
+// TEST INFRASTRUCTURE ONLY.  Compiled by oracle/Makefile directly against the
+// reference headers and sources under /root/reference/proj (never copied into
+// this repository) into oracle/_ref/libgcoo_ref{,_fma}.so.  It lets the tests
+// pin oracle/gcoo_oracle.c against the real reference and lets bench.py time
+// the reference's own CPU implementation (`--impl reference`,
+// cpu_baseline.kind = "reference").
+//
+// Two numeric flavours are built from the same file:
+//   libgcoo_ref.so      default x86-64 ISA (as shipped): mul+add chain
+//   libgcoo_ref_fma.so  -mfma: GCC contracts kernels.hpp:305 into FMA
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gcoo/bench.hpp"
+#include "gcoo/io.hpp"
+#include "gcoo/kernels.hpp"
+#include "gcoo/matrix.hpp"
+
+using namespace gcoo;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+template <typename T>
+GcooMatrix<T> make_gcoo(int64_t m, int64_t k, int32_t p, int64_t nnz, const T* vals,
+                        const int32_t* rows, const int32_t* cols, int64_t groups,
+                        const int64_t* gidx, const int64_t* gnnz) {
+  return GcooMatrix<T>(m, k, p, std::vector<T>(vals, vals + nnz),
+                       std::vector<index_t>(rows, rows + nnz),
+                       std::vector<index_t>(cols, cols + nnz),
+                       std::vector<int64_t>(gidx, gidx + groups),
+                       std::vector<int64_t>(gnnz, gnnz + groups));
+}
+
+template <typename T>
+DenseMatrix<T> make_dense(int64_t r, int64_t c, const T* data) {
+  DenseMatrix<T> d(r, c);
+  std::memcpy(d.data.data(), data, sizeof(T) * static_cast<size_t>(r * c));
+  return d;
+}
+
+template <typename T>
+void copy_gcoo(const GcooMatrix<T>& g, T* vals, int32_t* rows, int32_t* cols, int64_t* gidx,
+               int64_t* gnnz) {
+  std::memcpy(vals, g.values.data(), sizeof(T) * g.values.size());
+  std::memcpy(rows, g.row_idx.data(), sizeof(int32_t) * g.row_idx.size());
+  std::memcpy(cols, g.col_idx.data(), sizeof(int32_t) * g.col_idx.size());
+  std::memcpy(gidx, g.g_idxes.data(), sizeof(int64_t) * g.g_idxes.size());
+  std::memcpy(gnnz, g.nnz_per_group.data(), sizeof(int64_t) * g.nnz_per_group.size());
+}
+
+template <typename T>
+int spdm(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, int64_t nnz, const T* vals,
+         const int32_t* rows, const int32_t* cols, int64_t groups, const int64_t* gidx,
+         const int64_t* gnnz, const T* B, T* C, uint64_t* stats, int workers,
+         const int64_t* tile_order, int64_t tile_count) {
+  return guarded([&] {
+    const auto a = make_gcoo<T>(m, k, p, nnz, vals, rows, cols, groups, gidx, gnnz);
+    const auto bm = make_dense<T>(k, n, B);
+    ExecConfig cfg;
+    cfg.p = p;
+    cfg.b = b;
+    cfg.workers = workers;
+    KernelStats st;
+    DenseMatrix<T> c = tile_order
+        ? spdm_gcoo(a, bm, cfg, std::span<const int64_t>(tile_order, tile_count), &st)
+        : spdm_gcoo(a, bm, cfg, &st);
+    std::memcpy(C, c.data.data(), sizeof(T) * c.data.size());
+    if (stats) {
+      stats[0] = st.flops;
+      stats[1] = st.b_loads_total;
+      stats[2] = st.b_loads_reused;
+      stats[3] = st.staging_fills;
+    }
+  });
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+uint64_t ref_derive_seed(uint64_t base, uint64_t a, uint64_t b) { return derive_seed(base, a, b); }
+
+// generate_uniform_sparse<T>(n, s, seed) -> dense n*n
+int ref_uniform_sparse_f32(int64_t n, double s, uint64_t seed, float* out) {
+  return guarded([&] {
+    const auto d = generate_uniform_sparse<float>(n, s, seed);
+    std::memcpy(out, d.data.data(), sizeof(float) * d.data.size());
+  });
+}
+int ref_uniform_sparse_f64(int64_t n, double s, uint64_t seed, double* out) {
+  return guarded([&] {
+    const auto d = generate_uniform_sparse<double>(n, s, seed);
+    std::memcpy(out, d.data.data(), sizeof(double) * d.data.size());
+  });
+}
+
+// dense_to_gcoo: two calls — size query (vals == nullptr) then fill.
+int64_t ref_dense_to_gcoo_f32(int64_t m, int64_t k, const float* a, int32_t p, float* vals,
+                              int32_t* rows, int32_t* cols, int64_t* gidx, int64_t* gnnz) {
+  int64_t nnz = -1;
+  const int rc = guarded([&] {
+    const auto g = dense_to_gcoo(make_dense<float>(m, k, a), p);
+    nnz = g.nnz();
+    if (vals) copy_gcoo(g, vals, rows, cols, gidx, gnnz);
+  });
+  return rc ? -1 : nnz;
+}
+int64_t ref_dense_to_gcoo_f64(int64_t m, int64_t k, const double* a, int32_t p, double* vals,
+                              int32_t* rows, int32_t* cols, int64_t* gidx, int64_t* gnnz) {
+  int64_t nnz = -1;
+  const int rc = guarded([&] {
+    const auto g = dense_to_gcoo(make_dense<double>(m, k, a), p);
+    nnz = g.nnz();
+    if (vals) copy_gcoo(g, vals, rows, cols, gidx, gnnz);
+  });
+  return rc ? -1 : nnz;
+}
+
+int ref_coo_to_gcoo_f32(int64_t m, int64_t k, int64_t nnz, const float* vals, const int32_t* rows,
+                        const int32_t* cols, int32_t p, float* ovals, int32_t* orows,
+                        int32_t* ocols, int64_t* gidx, int64_t* gnnz) {
+  return guarded([&] {
+    CooMatrix<float> coo;
+    coo.rows_dim = m;
+    coo.cols_dim = k;
+    coo.values.assign(vals, vals + nnz);
+    coo.row_idx.assign(rows, rows + nnz);
+    coo.col_idx.assign(cols, cols + nnz);
+    const auto g = coo_to_gcoo(coo, p);
+    copy_gcoo(g, ovals, orows, ocols, gidx, gnnz);
+  });
+}
+
+int ref_spdm_gcoo_f32(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, int64_t nnz,
+                      const float* vals, const int32_t* rows, const int32_t* cols, int64_t groups,
+                      const int64_t* gidx, const int64_t* gnnz, const float* B, float* C,
+                      uint64_t* stats, int workers, const int64_t* tile_order,
+                      int64_t tile_count) {
+  return spdm<float>(m, k, n, p, b, nnz, vals, rows, cols, groups, gidx, gnnz, B, C, stats,
+                     workers, tile_order, tile_count);
+}
+int ref_spdm_gcoo_f64(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, int64_t nnz,
+                      const double* vals, const int32_t* rows, const int32_t* cols,
+                      int64_t groups, const int64_t* gidx, const int64_t* gnnz, const double* B,
+                      double* C, uint64_t* stats, int workers, const int64_t* tile_order,
+                      int64_t tile_count) {
+  return spdm<double>(m, k, n, p, b, nnz, vals, rows, cols, groups, gidx, gnnz, B, C, stats,
+                      workers, tile_order, tile_count);
+}
+
+// gemm_oracle (kernels.hpp:80-98): double accumulation, used by the
+// reference's own ≤1e-5 / ≤1e-12 gates.
+int ref_gemm_oracle_f32(int64_t m, int64_t k, int64_t n, const float* A, const float* B,
+                        float* C) {
+  return guarded([&] {
+    const auto c = gemm_oracle(make_dense<float>(m, k, A), make_dense<float>(k, n, B));
+    std::memcpy(C, c.data.data(), sizeof(float) * c.data.size());
+  });
+}
+int ref_gemm_oracle_f64(int64_t m, int64_t k, int64_t n, const double* A, const double* B,
+                        double* C) {
+  return guarded([&] {
+    const auto c = gemm_oracle(make_dense<double>(m, k, A), make_dense<double>(k, n, B));
+    std::memcpy(C, c.data.data(), sizeof(double) * c.data.size());
+  });
+}
+
+// The reference's own benchmark entry (bench.hpp:92-163, gcoo branch):
+// EO = dense_to_gcoo once, KC = median of `reps` timed spdm_gcoo calls
+// (C allocation included, as in the reference).  out = {eo_s, kc_s, gflops,
+// workers, nnz}.
+int ref_run_benchmark_gcoo_f32(int64_t n, const float* A, const float* B, int32_t p, int32_t b,
+                               int workers, int warmup, int reps, double* out) {
+  return guarded([&] {
+    const auto a = make_dense<float>(n, n, A);
+    const auto bm = make_dense<float>(n, n, B);
+    BenchOptions opt;
+    opt.exec.p = p;
+    opt.exec.b = b;
+    opt.exec.workers = workers;
+    opt.warmup = warmup;
+    opt.repetitions = reps;
+    const BenchResult r = run_benchmark(KernelKind::gcoo, a, bm, opt);
+    out[0] = r.eo_seconds;
+    out[1] = r.kc_seconds;
+    out[2] = r.gflops;
+    out[3] = r.workers;
+    out[4] = static_cast<double>(r.nnz);
+  });
+}
+
+// Timed spdm_gcoo on caller-provided GCOO (for samples whose dense A would be
+// too big to materialise): median of `reps` calls after `warmup`.
+int ref_time_spdm_gcoo_f32(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, int64_t nnz,
+                           const float* vals, const int32_t* rows, const int32_t* cols,
+                           int64_t groups, const int64_t* gidx, const int64_t* gnnz,
+                           const float* B, int workers, int warmup, int reps, double* out) {
+  return guarded([&] {
+    const auto a = make_gcoo<float>(m, k, p, nnz, vals, rows, cols, groups, gidx, gnnz);
+    const auto bm = make_dense<float>(k, n, B);
+    ExecConfig cfg;
+    cfg.p = p;
+    cfg.b = b;
+    cfg.workers = workers;
+    float sink = 0;
+    for (int w = 0; w < warmup; ++w) sink += spdm_gcoo(a, bm, cfg).data.back();
+    std::vector<double> ts;
+    for (int r = 0; r < reps; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      const auto c = spdm_gcoo(a, bm, cfg);
+      ts.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+      sink += c.data.back();
+    }
+    volatile float keep = sink;
+    (void)keep;
+    out[0] = median(ts);
+    out[1] = resolve_workers(workers);
+  });
+}
+
+}  // extern "C"

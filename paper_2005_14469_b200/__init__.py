@@ -1,0 +1,516 @@
+"""B200-native GCOOSpDM (arXiv 2005.14469): Python host mirror of the reference API.
+
+The product is ``lib/libgcoo_cuda.so`` (hand-written sm_100a CUDA behind the C
+ABI in ``include/gcoo_capi.h``).  This module binds that ABI with ctypes and
+mirrors the reference's C++ names and semantics (``proj/include/gcoo``):
+
+==========================  =========================================
+reference (C++)             here
+==========================  =========================================
+``GcooMatrix<T>``           :class:`GcooMatrix` (same fields)
+``ExecConfig``              :class:`ExecConfig` (p, b, workers)
+``KernelStats``             :class:`KernelStats`
+``TimingBreakdown``         :class:`TimingBreakdown`
+``dense_to_gcoo``           :func:`dense_to_gcoo`
+``coo_to_gcoo``             :func:`coo_to_gcoo`
+(new) CSR entry             :func:`csr_to_gcoo`
+``spdm_gcoo`` (2 overloads) :func:`spdm_gcoo`
+``spdm_gcoo_auto``          :func:`spdm_gcoo_auto`
+``generate_uniform_sparse`` :func:`generate_uniform_sparse`
+``derive_seed``             :func:`derive_seed`
+==========================  =========================================
+
+``std::invalid_argument`` surfaces as :class:`ValueError`, CUDA failures as
+:class:`RuntimeError`, allocation failures as :class:`MemoryError` — raised at
+the same points the reference throws.  There is no CPU fallback: without the
+built library or a GPU every compute call raises.
+
+Device-resident variants (``*_dev``) take torch CUDA tensors and a stream and
+are what bench.py times.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import time
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "lib", "libgcoo_cuda.so")
+
+_i64, _i32, _u64, _dbl, _vp, _int = C.c_int64, C.c_int32, C.c_uint64, C.c_double, C.c_void_p, C.c_int
+
+GCOO_OK, GCOO_EINVAL, GCOO_ECUDA, GCOO_ENOMEM = 0, 1, 2, 3
+FLAVOR_FMA, FLAVOR_MUL_ADD = 0, 1
+
+
+class _Stats(C.Structure):
+    _fields_ = [("flops", _u64), ("b_loads_total", _u64), ("b_loads_reused", _u64), ("staging_fills", _u64)]
+
+
+_lib = None
+
+
+def _sig(L, name, res, args):
+    f = getattr(L, name)
+    f.restype = res
+    f.argtypes = args
+
+
+def lib():
+    """Load libgcoo_cuda.so (raises if it was not built: no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2005_14469_b200.build`")
+    L = C.CDLL(LIB_PATH)
+    _sig(L, "gcoo_abi_version", _int, [])
+    _sig(L, "gcoo_last_error", C.c_char_p, [])
+    _sig(L, "gcoo_device_count", _int, [C.POINTER(_int)])
+    _sig(L, "gcoo_set_device", _int, [_int])
+    _sig(L, "gcoo_launch_count", _u64, [])
+    _sig(L, "gcoo_stream_sync", _int, [_vp])
+    spdm_args = [_i64, _i64, _i64, _i32, _i32, _i32, _i64, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp,
+                 C.POINTER(_Stats), _vp, _i64]
+    _sig(L, "gcoo_spdm_f32", _int, spdm_args)
+    _sig(L, "gcoo_spdm_f64", _int, spdm_args)
+    dev_args = [_i64, _i64, _i64, _i32, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _i64,
+                C.POINTER(_Stats), _int, _vp]
+    _sig(L, "gcoo_spdm_f32_dev", _int, dev_args)
+    _sig(L, "gcoo_spdm_f64_dev", _int, dev_args)
+    _sig(L, "gcoo_stats_dev", _int, [_i64, _i64, _i32, _i32, _i64, _vp, _vp, _i64, _vp, C.POINTER(_Stats), _vp])
+    coo_args = [_i64, _i64, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+    _sig(L, "gcoo_coo_to_gcoo_f32", _int, coo_args)
+    _sig(L, "gcoo_coo_to_gcoo_f64", _int, coo_args)
+    _sig(L, "gcoo_coo_to_gcoo_f32_dev", _int, coo_args + [_vp])
+    _sig(L, "gcoo_csr_to_gcoo_f32", _int, coo_args)
+    _sig(L, "gcoo_csr_to_gcoo_f64", _int, coo_args)
+    dense_args = [_i64, _i64, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, C.POINTER(_i64)]
+    _sig(L, "gcoo_dense_to_gcoo_f32", _int, dense_args)
+    _sig(L, "gcoo_dense_to_gcoo_f64", _int, dense_args)
+    _sig(L, "gcoo_dense_to_gcoo_f32_dev", _int, dense_args + [_vp])
+    _sig(L, "gcoo_generate_uniform_sparse_f32", _int, [_i64, _dbl, _u64, _vp])
+    _sig(L, "gcoo_generate_uniform_sparse_coo_f32", _int, [_i64, _dbl, _u64, _i64, _vp, _vp, _vp, C.POINTER(_i64)])
+    _sig(L, "gcoo_generate_powerlaw_coo_f32", _int, [_i64, _dbl, _dbl, _u64, _i64, _vp, _vp, _vp, C.POINTER(_i64)])
+    _sig(L, "gcoo_derive_seed", _u64, [_u64, _u64, _u64])
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc == GCOO_OK:
+        return
+    msg = (lib().gcoo_last_error() or b"").decode()
+    if rc == GCOO_EINVAL:
+        raise ValueError(msg)
+    if rc == GCOO_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+def _p(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(_vp)
+    return C.c_void_p(a.data_ptr())  # torch tensor
+
+
+def device_count() -> int:
+    c = _int(0)
+    lib().gcoo_device_count(C.byref(c))
+    return int(c.value)
+
+
+def set_device(device: int) -> None:
+    _check(lib().gcoo_set_device(device))
+
+
+def launch_count() -> int:
+    """Kernels this process launched through the library (bench: gpu_launches)."""
+    return int(lib().gcoo_launch_count())
+
+
+# ---------------------------------------------------------------- types ----
+@dataclass
+class ExecConfig:
+    """kernels.hpp:27-37.  workers is accepted and ignored on the GPU."""
+    p: int = 4
+    b: int = 64
+    workers: int = 0
+
+    def validate(self) -> None:
+        if not (_pow2(self.p) and _pow2(self.b)):
+            raise ValueError("ExecConfig: p and b must be powers of two")
+        if self.workers < 0:
+            raise ValueError("ExecConfig: workers must be >= 0")
+
+
+@dataclass
+class KernelStats:
+    """kernels.hpp:52-65."""
+    flops: int = 0
+    b_loads_total: int = 0
+    b_loads_reused: int = 0
+    staging_fills: int = 0
+
+    @classmethod
+    def _from(cls, s: _Stats) -> "KernelStats":
+        return cls(int(s.flops), int(s.b_loads_total), int(s.b_loads_reused), int(s.staging_fills))
+
+    def __iadd__(self, o: "KernelStats"):
+        self.flops += o.flops
+        self.b_loads_total += o.b_loads_total
+        self.b_loads_reused += o.b_loads_reused
+        self.staging_fills += o.staging_fills
+        return self
+
+
+@dataclass
+class TimingBreakdown:
+    """kernels.hpp:69-72."""
+    eo_seconds: float = 0.0
+    kc_seconds: float = 0.0
+
+
+def _pow2(v: int) -> bool:
+    return v > 0 and (v & (v - 1)) == 0
+
+
+@dataclass
+class GcooMatrix:
+    """GcooMatrix<T> (matrix.hpp:176-245): p-row bands, per-band COO slices in
+    (col,row) order, int32 coordinates, int64 group offsets and counts."""
+    rows_dim: int
+    cols_dim: int
+    p: int
+    values: np.ndarray
+    row_idx: np.ndarray
+    col_idx: np.ndarray
+    g_idxes: np.ndarray
+    nnz_per_group: np.ndarray
+
+    def nnz(self) -> int:
+        return int(self.values.size)
+
+    def groups(self) -> int:
+        return int(self.g_idxes.size)
+
+    @property
+    def dtype(self):
+        return self.values.dtype
+
+    def validate(self) -> None:
+        """GcooMatrix::validate (matrix.hpp:206-244), vectorised on the host."""
+        m, k, p = self.rows_dim, self.cols_dim, self.p
+        if m < 1 or k < 1:
+            raise ValueError("GcooMatrix: dimensions must be >= 1")
+        if not _pow2(p):
+            raise ValueError("GcooMatrix: p must be a power of two")
+        g = -(-m // p)
+        if self.groups() != g or self.nnz_per_group.size != g:
+            raise ValueError(f"GcooMatrix: expected {g} groups")
+        n = self.nnz()
+        if self.row_idx.size != n or self.col_idx.size != n:
+            raise ValueError("GcooMatrix: array lengths differ")
+        gn = self.nnz_per_group.astype(np.int64)
+        if np.any(gn < 0):
+            raise ValueError("GcooMatrix: negative group size")
+        off = np.concatenate([[0], np.cumsum(gn)[:-1]]) if g else np.zeros(0, np.int64)
+        if not np.array_equal(off, self.g_idxes):
+            raise ValueError("GcooMatrix: g_idxes inconsistent with group sizes")
+        if gn.sum() != n:
+            raise ValueError("GcooMatrix: group sizes do not cover all entries")
+        grp = np.repeat(np.arange(g, dtype=np.int64), gn)
+        r = self.row_idx.astype(np.int64)
+        c = self.col_idx.astype(np.int64)
+        if np.any(r // p != grp) or np.any(r >= m) or np.any(r < 0):
+            raise ValueError("GcooMatrix: row outside its group band")
+        if np.any(c < 0) or np.any(c >= k):
+            raise ValueError("GcooMatrix: column out of range")
+        if n > 1:
+            same = grp[1:] == grp[:-1]
+            ok = (c[:-1] < c[1:]) | ((c[:-1] == c[1:]) & (r[:-1] < r[1:]))
+            if np.any(same & ~ok):
+                raise ValueError("GcooMatrix: group entries not in (col,row) order (or duplicate)")
+
+
+def _dense_check(a: np.ndarray) -> np.ndarray:
+    if a.ndim != 2 or a.shape[0] < 1 or a.shape[1] < 1:
+        raise ValueError("DenseMatrix: dimensions must be >= 1")
+    if a.dtype not in (np.float32, np.float64):
+        raise TypeError("DenseMatrix: float32 or float64 required")
+    return np.ascontiguousarray(a)
+
+
+# ---------------------------------------------------------- construction ---
+def dense_to_gcoo(a: np.ndarray, p: int) -> GcooMatrix:
+    """dense_to_gcoo (matrix.hpp:306-353) on the GPU."""
+    a = _dense_check(a)
+    m, k = a.shape
+    L = lib()
+    f = L.gcoo_dense_to_gcoo_f32 if a.dtype == np.float32 else L.gcoo_dense_to_gcoo_f64
+    nnz = _i64(0)
+    _check(f(m, k, p, _p(a), 0, None, None, None, None, None, C.byref(nnz)))
+    n = int(nnz.value)
+    g = -(-m // p)
+    vals = np.empty(n, a.dtype)
+    rows = np.empty(n, np.int32)
+    cols = np.empty(n, np.int32)
+    gi = np.empty(g, np.int64)
+    gn = np.empty(g, np.int64)
+    _check(f(m, k, p, _p(a), n, _p(vals), _p(rows), _p(cols), _p(gi), _p(gn), C.byref(nnz)))
+    return GcooMatrix(m, k, p, vals, rows, cols, gi, gn)
+
+
+def coo_to_gcoo(rows_dim: int, cols_dim: int, values: np.ndarray, row_idx: np.ndarray, col_idx: np.ndarray,
+                p: int) -> GcooMatrix:
+    """coo_to_gcoo (matrix.hpp:366-405) on the GPU; validates the COO like
+    CooMatrix::validate (:95-115)."""
+    values = np.ascontiguousarray(values)
+    row_idx = np.ascontiguousarray(row_idx, dtype=np.int32)
+    col_idx = np.ascontiguousarray(col_idx, dtype=np.int32)
+    if rows_dim < 1 or cols_dim < 1:
+        raise ValueError("CooMatrix: dimensions must be >= 1")
+    if not (values.size == row_idx.size == col_idx.size):
+        raise ValueError("CooMatrix: array lengths differ")
+    n = values.size
+    g = -(-rows_dim // p) if _pow2(p) else 0
+    ov = np.empty(n, values.dtype)
+    orr = np.empty(n, np.int32)
+    oc = np.empty(n, np.int32)
+    gi = np.empty(max(g, 1), np.int64)
+    gn = np.empty(max(g, 1), np.int64)
+    L = lib()
+    f = L.gcoo_coo_to_gcoo_f32 if values.dtype == np.float32 else L.gcoo_coo_to_gcoo_f64
+    _check(f(rows_dim, cols_dim, p, n, _p(values), _p(row_idx), _p(col_idx), _p(ov), _p(orr), _p(oc), _p(gi),
+             _p(gn)))
+    return GcooMatrix(rows_dim, cols_dim, p, ov, orr, oc, gi[:g], gn[:g])
+
+
+def csr_to_gcoo(rows_dim: int, cols_dim: int, values: np.ndarray, col_idx: np.ndarray, row_ptr: np.ndarray,
+                p: int) -> GcooMatrix:
+    """CSR -> GCOO (new entry point; CSR validated like CsrMatrix::validate)."""
+    values = np.ascontiguousarray(values)
+    col_idx = np.ascontiguousarray(col_idx, dtype=np.int32)
+    row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    if rows_dim < 1 or cols_dim < 1:
+        raise ValueError("CsrMatrix: dimensions must be >= 1")
+    if values.size != col_idx.size:
+        raise ValueError("CsrMatrix: array lengths differ")
+    if row_ptr.size != rows_dim + 1:
+        raise ValueError("CsrMatrix: row_ptr must have rows_dim+1 entries")
+    n = values.size
+    g = -(-rows_dim // p) if _pow2(p) else 0
+    ov = np.empty(n, values.dtype)
+    orr = np.empty(n, np.int32)
+    oc = np.empty(n, np.int32)
+    gi = np.empty(max(g, 1), np.int64)
+    gn = np.empty(max(g, 1), np.int64)
+    L = lib()
+    f = L.gcoo_csr_to_gcoo_f32 if values.dtype == np.float32 else L.gcoo_csr_to_gcoo_f64
+    _check(f(rows_dim, cols_dim, p, n, _p(values), _p(col_idx), _p(row_ptr), _p(ov), _p(orr), _p(oc), _p(gi),
+             _p(gn)))
+    return GcooMatrix(rows_dim, cols_dim, p, ov, orr, oc, gi[:g], gn[:g])
+
+
+# -------------------------------------------------------------- multiply ---
+def spdm_gcoo(a: GcooMatrix, b: np.ndarray, cfg: Optional[ExecConfig] = None,
+              tile_order: Optional[Sequence[int]] = None, stats: Optional[KernelStats] = None,
+              out: Optional[np.ndarray] = None) -> np.ndarray:
+    """spdm_gcoo (kernels.hpp:334-348): C = A_gcoo * B on the GPU.
+
+    ``tile_order`` is the second overload's span (must have
+    groups*ceil(n/b) entries).  When ``stats`` is given it is filled with the
+    KernelStats for ``cfg.b``.  ``out`` (optional, e.g. pinned host memory)
+    receives C instead of a fresh array."""
+    cfg = cfg or ExecConfig()
+    if b.ndim != 2:
+        raise ValueError("DenseMatrix: 2-D operand required")
+    b = np.ascontiguousarray(b, dtype=a.values.dtype)
+    k_b, n = b.shape
+    if out is not None:
+        if out.shape != (a.rows_dim, n) or out.dtype != a.values.dtype or not out.flags.c_contiguous:
+            raise ValueError("spdm_gcoo: out has the wrong shape/dtype/layout")
+        c = out
+    else:
+        c = np.empty((a.rows_dim, n), dtype=a.values.dtype)
+    to = None if tile_order is None else np.ascontiguousarray(np.asarray(tile_order, dtype=np.int64))
+    st = _Stats()
+    L = lib()
+    f = L.gcoo_spdm_f32 if a.values.dtype == np.float32 else L.gcoo_spdm_f64
+    _check(f(a.rows_dim, a.cols_dim, n, a.p, cfg.p, cfg.b, k_b, a.nnz(), _p(a.values), _p(a.row_idx),
+             _p(a.col_idx), a.groups(), _p(a.g_idxes), _p(a.nnz_per_group), _p(b), _p(c),
+             C.byref(st) if stats is not None else None, _p(to), 0 if to is None else to.size))
+    if stats is not None:
+        s = KernelStats._from(st)
+        stats.flops, stats.b_loads_total, stats.b_loads_reused, stats.staging_fills = (
+            s.flops, s.b_loads_total, s.b_loads_reused, s.staging_fills)
+    return c
+
+
+def spdm_gcoo_auto(a: np.ndarray, b: np.ndarray, cfg: Optional[ExecConfig] = None,
+                   timing: Optional[TimingBreakdown] = None, stats: Optional[KernelStats] = None) -> np.ndarray:
+    """spdm_gcoo_auto (kernels.hpp:353-367): EO = dense_to_gcoo, KC = spdm_gcoo."""
+    cfg = cfg or ExecConfig()
+    cfg.validate()
+    t0 = time.perf_counter()
+    g = dense_to_gcoo(a, cfg.p)
+    t1 = time.perf_counter()
+    c = spdm_gcoo(g, b, cfg, stats=stats)
+    t2 = time.perf_counter()
+    if timing is not None:
+        timing.eo_seconds, timing.kc_seconds = t1 - t0, t2 - t1
+    return c
+
+
+# ------------------------------------------------------ device-resident ----
+@dataclass
+class DeviceGcoo:
+    """GCOO arrays resident in HBM (torch tensors on one CUDA device)."""
+    rows_dim: int
+    cols_dim: int
+    p: int
+    values: "object"
+    row_idx: "object"
+    col_idx: "object"
+    g_idxes: "object"
+    nnz_per_group: "object"
+
+    @classmethod
+    def from_host(cls, g: GcooMatrix, device="cuda") -> "DeviceGcoo":
+        import torch
+        t = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(device)
+        return cls(g.rows_dim, g.cols_dim, g.p, t(g.values), t(g.row_idx), t(g.col_idx), t(g.g_idxes),
+                   t(g.nnz_per_group))
+
+    def nnz(self) -> int:
+        return int(self.values.numel())
+
+    def groups(self) -> int:
+        return int(self.g_idxes.numel())
+
+    def to_host(self) -> GcooMatrix:
+        h = lambda x: x.cpu().numpy()
+        return GcooMatrix(self.rows_dim, self.cols_dim, self.p, h(self.values), h(self.row_idx),
+                          h(self.col_idx), h(self.g_idxes), h(self.nnz_per_group))
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+def spdm_gcoo_dev(a: DeviceGcoo, b, c, cfg: Optional[ExecConfig] = None, flavor: int = FLAVOR_FMA,
+                  stream=None, stats: Optional[KernelStats] = None) -> None:
+    """Stream-ordered C = A * B on device tensors (b: k x n, c: m x n; a
+    column shard may be a strided view with unit column stride)."""
+    import torch
+    cfg = cfg or ExecConfig(p=a.p)
+    n = b.shape[1]
+    if b.stride(1) != 1 or c.stride(1) != 1:
+        raise ValueError("spdm_gcoo_dev: B and C need unit column stride")
+    if b.shape[0] != a.cols_dim:
+        raise ValueError("spdm_gcoo: inner dimensions differ")
+    if cfg.p != a.p:
+        raise ValueError("spdm_gcoo: matrix grouped with a different p")
+    if c.shape[0] != a.rows_dim or c.shape[1] != n:
+        raise ValueError("spdm_gcoo_dev: C has the wrong shape")
+    st = _Stats()
+    L = lib()
+    f = L.gcoo_spdm_f32_dev if b.dtype == torch.float32 else L.gcoo_spdm_f64_dev
+    _check(f(a.rows_dim, a.cols_dim, n, a.p, cfg.b, a.nnz(), _p(a.values), _p(a.row_idx), _p(a.col_idx),
+             a.groups(), _p(a.g_idxes), _p(a.nnz_per_group), _p(b), b.stride(0), _p(c), c.stride(0),
+             C.byref(st) if stats is not None else None, flavor, _stream_ptr(stream)))
+    if stats is not None:
+        s = KernelStats._from(st)
+        stats.flops, stats.b_loads_total, stats.b_loads_reused, stats.staging_fills = (
+            s.flops, s.b_loads_total, s.b_loads_reused, s.staging_fills)
+
+
+def coo_to_gcoo_dev(rows_dim: int, cols_dim: int, values, row_idx, col_idx, p: int, stream=None) -> DeviceGcoo:
+    import torch
+    n = values.numel()
+    g = -(-rows_dim // p) if _pow2(p) else 1
+    dev = values.device
+    ov = torch.empty(n, dtype=values.dtype, device=dev)
+    orr = torch.empty(n, dtype=torch.int32, device=dev)
+    oc = torch.empty(n, dtype=torch.int32, device=dev)
+    gi = torch.empty(g, dtype=torch.int64, device=dev)
+    gn = torch.empty(g, dtype=torch.int64, device=dev)
+    _check(lib().gcoo_coo_to_gcoo_f32_dev(rows_dim, cols_dim, p, n, _p(values), _p(row_idx), _p(col_idx), _p(ov),
+                                          _p(orr), _p(oc), _p(gi), _p(gn), _stream_ptr(stream)))
+    return DeviceGcoo(rows_dim, cols_dim, p, ov, orr, oc, gi, gn)
+
+
+def dense_to_gcoo_dev(a, p: int, stream=None) -> DeviceGcoo:
+    import torch
+    m, k = a.shape
+    dev = a.device
+    if not _pow2(p):
+        raise ValueError("dense_to_gcoo: p must be a power of two")
+    g = -(-m // p)
+    gi = torch.empty(g, dtype=torch.int64, device=dev)
+    gn = torch.empty(g, dtype=torch.int64, device=dev)
+    nnz = _i64(0)
+    L = lib()
+    sp = _stream_ptr(stream)
+    _check(L.gcoo_dense_to_gcoo_f32_dev(m, k, p, _p(a), 0, None, None, None, _p(gi), _p(gn), C.byref(nnz), sp))
+    n = int(nnz.value)
+    ov = torch.empty(n, dtype=a.dtype, device=dev)
+    orr = torch.empty(n, dtype=torch.int32, device=dev)
+    oc = torch.empty(n, dtype=torch.int32, device=dev)
+    _check(L.gcoo_dense_to_gcoo_f32_dev(m, k, p, _p(a), n, _p(ov), _p(orr), _p(oc), _p(gi), _p(gn),
+                                        C.byref(nnz), sp))
+    return DeviceGcoo(m, k, p, ov, orr, oc, gi, gn)
+
+
+# ------------------------------------------------------- synthetic inputs ---
+def derive_seed(base: int, salt_a: int, salt_b: int = 0) -> int:
+    return int(lib().gcoo_derive_seed(base, salt_a, salt_b))
+
+
+def generate_uniform_sparse(n: int, s: float, seed: int) -> np.ndarray:
+    """generate_uniform_sparse<float> (io.hpp:129-145), bit-identical."""
+    out = np.empty((n, n), np.float32)
+    _check(lib().gcoo_generate_uniform_sparse_f32(n, s, seed, _p(out)))
+    return out
+
+
+def generate_uniform_sparse_coo(n: int, s: float, seed: int):
+    """Same sample as generate_uniform_sparse, as row-major COO arrays."""
+    nnz = _i64(0)
+    L = lib()
+    _check(L.gcoo_generate_uniform_sparse_coo_f32(n, s, seed, 0, None, None, None, C.byref(nnz)))
+    k = int(nnz.value)
+    v = np.empty(k, np.float32)
+    r = np.empty(k, np.int32)
+    c = np.empty(k, np.int32)
+    _check(L.gcoo_generate_uniform_sparse_coo_f32(n, s, seed, k, _p(v), _p(r), _p(c), C.byref(nnz)))
+    return v, r, c
+
+
+def generate_powerlaw_coo(n: int, s: float, alpha: float, seed: int):
+    nnz = _i64(0)
+    L = lib()
+    _check(L.gcoo_generate_powerlaw_coo_f32(n, s, alpha, seed, 0, None, None, None, C.byref(nnz)))
+    k = int(nnz.value)
+    v = np.empty(k, np.float32)
+    r = np.empty(k, np.int32)
+    c = np.empty(k, np.int32)
+    _check(L.gcoo_generate_powerlaw_coo_f32(n, s, alpha, seed, k, _p(v), _p(r), _p(c), C.byref(nnz)))
+    return v, r, c
+
+
+__all__ = [
+    "ExecConfig", "KernelStats", "TimingBreakdown", "GcooMatrix", "DeviceGcoo", "dense_to_gcoo", "coo_to_gcoo",
+    "csr_to_gcoo", "spdm_gcoo", "spdm_gcoo_auto", "spdm_gcoo_dev", "coo_to_gcoo_dev", "dense_to_gcoo_dev",
+    "derive_seed", "generate_uniform_sparse", "generate_uniform_sparse_coo", "generate_powerlaw_coo",
+    "device_count", "set_device", "launch_count", "lib", "FLAVOR_FMA", "FLAVOR_MUL_ADD",
+]

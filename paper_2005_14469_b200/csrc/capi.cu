@@ -1,0 +1,658 @@
+// capi.cu — the C ABI of libgcoo_cuda.so (declared in include/gcoo_capi.h).
+//
+// Host-side orchestration only: argument validation in the reference's order
+// (so the same inputs raise the same exception class), device buffers from the
+// stream-ordered pool, copies, and kernel launches.  All arithmetic on matrix
+// data happens in the CUDA kernels (spdm_rowtile.cuh, spdm_panel.cuh,
+// construct.cuh); there is no host compute path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "construct.cuh"
+#include "spdm_panel.cuh"
+#include "spdm_rowtile.cuh"
+
+namespace gcoo_b200 {
+
+std::atomic<uint64_t> g_launches{0};
+
+namespace {
+
+thread_local std::string t_error;
+thread_local int t_device = -1;
+
+int current_device() {
+  if (t_device < 0) {
+    int d = 0;
+    GCOO_CUDA(cudaGetDevice(&d));
+    t_device = d;
+  }
+  return t_device;
+}
+
+std::mutex g_pool_mu;
+bool g_pool_set[64] = {};
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return GCOO_OK;
+  } catch (const Error& e) {
+    t_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    t_error = "host out of memory";
+    return GCOO_ENOMEM;
+  } catch (const std::exception& e) {
+    t_error = e.what();
+    return GCOO_ECUDA;
+  }
+}
+
+void einval(const std::string& msg) { fail(GCOO_EINVAL, msg); }
+
+template <typename T>
+void h2d(T* dst, const T* src, size_t count, cudaStream_t s) {
+  if (count) GCOO_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+template <typename T>
+void d2h(T* dst, const T* src, size_t count, cudaStream_t s) {
+  if (count) GCOO_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+}
+
+int grid_for(int64_t work, int threads, int per_sm = 8) {
+  const int64_t want = ceil_div(std::max<int64_t>(work, 1), threads);
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  return (int)std::max<int64_t>(1, std::min(want, cap));
+}
+
+}  // namespace
+
+cudaStream_t thread_stream() {
+  thread_local cudaStream_t streams[64] = {};
+  const int d = current_device();
+  if (!streams[d]) {
+    GCOO_CUDA(cudaSetDevice(d));
+    ensure_pool_retains();
+    GCOO_CUDA(cudaStreamCreateWithFlags(&streams[d], cudaStreamNonBlocking));
+  }
+  return streams[d];
+}
+
+int sm_count() {
+  thread_local int cached[64] = {};
+  const int d = current_device();
+  if (!cached[d]) GCOO_CUDA(cudaDeviceGetAttribute(&cached[d], cudaDevAttrMultiProcessorCount, d));
+  return cached[d];
+}
+
+void ensure_pool_retains() {
+  const int d = current_device();
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (g_pool_set[d]) return;
+  cudaMemPool_t pool;
+  GCOO_CUDA(cudaDeviceGetDefaultMemPool(&pool, d));
+  uint64_t threshold = UINT64_MAX;  // keep freed blocks for the next call
+  GCOO_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+  g_pool_set[d] = true;
+}
+
+// ------------------------------------------------------------ scan --------
+void exclusive_scan(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s) {
+  if (n == 0) {
+    GCOO_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), s));
+    return;
+  }
+  const int64_t tiles = ceil_div(n, kScanTile);
+  DevBuf<int64_t> sums(tiles, s), sums_scan(tiles + 1, s);
+  GCOO_LAUNCH(scan_tiles_kernel, (unsigned)tiles, kScanThreads, 0, s, in, out, n, sums.get());
+  if (tiles > 1) {
+    exclusive_scan(sums.get(), sums_scan.get(), tiles, s);
+    GCOO_LAUNCH(add_tile_offsets_kernel, (unsigned)ceil_div(n, 256), 256, 0, s, out, n, sums_scan.get());
+  }
+  GCOO_LAUNCH(write_total_kernel, 1, 1, 0, s, in, out, n);
+}
+
+// ------------------------------------------------------------ spdm --------
+template <typename T>
+struct DevGcoo {
+  int64_t m, k, nnz, groups;
+  int32_t p;
+  const T* vals;
+  const int32_t* rows;
+  const int32_t* cols;
+  const int64_t* gidx;
+  const int64_t* gnnz;
+};
+
+template <typename T, int PMAX, bool VEC, bool FMA>
+void launch_rowtile(const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C, int64_t ldc,
+                    cudaStream_t s) {
+  constexpr int V = VecOf<T>::V;
+  const int64_t row_tiles = ceil_div(a.m, PMAX);
+  const int64_t row_blocks = ceil_div(row_tiles, kRowTileWarps);
+  const int64_t col_tiles = ceil_div(n, 32 * V);
+  const int64_t grid = row_blocks * col_tiles;
+  if (grid > INT32_MAX) fail(GCOO_EINVAL, "spdm_gcoo: problem too large for one launch");
+  GCOO_LAUNCH((spdm_rowtile_kernel<T, PMAX, VEC, FMA>), (unsigned)grid, kRowTileWarps * 32, 0, s, a.m,
+              a.k, n, a.p, a.groups, a.vals, a.rows, a.cols, a.gidx, a.gnnz, B, ldb, C, ldc, row_tiles,
+              row_blocks);
+}
+
+template <typename T, bool FMA>
+void launch_rowtile_p(const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C, int64_t ldc,
+                      cudaStream_t s) {
+  constexpr int V = VecOf<T>::V;
+  const bool vec = n % V == 0 && ldb % V == 0 && ldc % V == 0 &&
+                   (reinterpret_cast<uintptr_t>(B) % 16) == 0 && (reinterpret_cast<uintptr_t>(C) % 16) == 0;
+  if (a.p <= 8) {
+    if (vec) launch_rowtile<T, 8, true, FMA>(a, n, B, ldb, C, ldc, s);
+    else launch_rowtile<T, 8, false, FMA>(a, n, B, ldb, C, ldc, s);
+  } else {
+    if (vec) launch_rowtile<T, 16, true, FMA>(a, n, B, ldb, C, ldc, s);
+    else launch_rowtile<T, 16, false, FMA>(a, n, B, ldb, C, ldc, s);
+  }
+}
+
+template <typename T>
+void launch_spdm(const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C, int64_t ldc, int flavor,
+                 cudaStream_t s) {
+  if (a.m == 0 || n == 0) return;
+  const bool fma = flavor != GCOO_FLAVOR_MUL_ADD;
+  if constexpr (std::is_same<T, float>::value) {
+    if (fma && panel_applicable(a.m, a.k, n, ldb, ldc, B, C)) {
+      launch_panel(a.m, a.k, n, a.p, a.groups, a.vals, a.rows, a.cols, a.gidx, a.gnnz, B, ldb, C, ldc, s);
+      return;
+    }
+  }
+  if (fma) launch_rowtile_p<T, true>(a, n, B, ldb, C, ldc, s);
+  else launch_rowtile_p<T, false>(a, n, B, ldb, C, ldc, s);
+}
+
+// KernelStats for the caller's b (flops, staging and run counts; see
+// construct.cuh K4).  Synchronises to return host values.
+void device_stats(int64_t nnz, int64_t n, int32_t p, int32_t b, int64_t groups, const int32_t* rows,
+                  const int32_t* cols, const int64_t* gidx, gcoo_stats* st, cudaStream_t s) {
+  DevBuf<unsigned long long> runs(1, s);
+  GCOO_CUDA(cudaMemsetAsync(runs.get(), 0, sizeof(unsigned long long), s));
+  if (nnz > 0)
+    GCOO_LAUNCH(run_count_kernel, grid_for(nnz, 256), 256, 0, s, nnz, p, b, groups, rows, cols, gidx,
+                runs.get());
+  unsigned long long h_runs = 0;
+  d2h(&h_runs, runs.get(), 1, s);
+  GCOO_CUDA(cudaStreamSynchronize(s));
+  const uint64_t col_tiles = (uint64_t)ceil_div(n, b);
+  st->flops = 2ull * (uint64_t)nnz * (uint64_t)n;
+  st->staging_fills = (uint64_t)nnz * col_tiles;
+  st->b_loads_total = (uint64_t)h_runs * (uint64_t)n;
+  st->b_loads_reused = ((uint64_t)nnz - (uint64_t)h_runs) * (uint64_t)n;
+}
+
+// Explicit tile order that is not a permutation: the reference computes the
+// listed tiles (duplicates twice, with identical results) and never writes
+// unlisted ones, so they stay zero; its counters sum over the list.
+template <typename T>
+void apply_tile_list(const DevGcoo<T>& a, int64_t n, int32_t b, const int64_t* h_order, int64_t count,
+                     T* C, int64_t ldc, gcoo_stats* st, cudaStream_t s) {
+  const int64_t col_tiles = ceil_div(n, b);
+  const int64_t tiles = a.groups * col_tiles;
+  DevBuf<int64_t> order(count, s);
+  DevBuf<unsigned int> cover(tiles, s);
+  DevBuf<unsigned long long> gruns(a.groups, s), dst(4, s);
+  h2d(order.get(), h_order, count, s);
+  GCOO_CUDA(cudaMemsetAsync(cover.get(), 0, cover.bytes(), s));
+  GCOO_CUDA(cudaMemsetAsync(gruns.get(), 0, gruns.bytes(), s));
+  GCOO_CUDA(cudaMemsetAsync(dst.get(), 0, dst.bytes(), s));
+  if (a.nnz > 0)
+    GCOO_LAUNCH(group_runs_kernel, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, b, a.groups, a.rows, a.cols,
+                a.gidx, gruns.get());
+  GCOO_LAUNCH(tile_list_kernel, grid_for(count, 256), 256, 0, s, count, order.get(), col_tiles, n, b,
+              a.gnnz, gruns.get(), cover.get(), dst.get());
+  GCOO_LAUNCH(zero_uncovered_kernel<T>, grid_for(a.m * n, 256), 256, 0, s, a.m, n, a.p, b, col_tiles,
+              cover.get(), C, ldc);
+  if (st) {
+    unsigned long long h[4];
+    d2h(h, dst.get(), 4, s);
+    GCOO_CUDA(cudaStreamSynchronize(s));
+    st->flops = h[0];
+    st->b_loads_total = h[1];
+    st->b_loads_reused = h[2];
+    st->staging_fills = h[3];
+  }
+}
+
+// detail::spdm_gcoo_impl's checks, in its order (kernels.hpp:244-254).
+void validate_spdm(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int32_t cfg_b, int64_t b_rows,
+                   int64_t nnz, int64_t groups, const int64_t* tile_order, int64_t tile_count) {
+  if (!is_pow2(cfg_p) || !is_pow2(cfg_b)) einval("ExecConfig: p and b must be powers of two");
+  if (k != b_rows) einval("spdm_gcoo: inner dimensions differ");
+  if (a_p != cfg_p) einval("spdm_gcoo: matrix grouped with a different p");
+  if (m < 1 || k < 1 || n < 1) einval("spdm_gcoo: dimensions must be >= 1");
+  if (groups != ceil_div(m, a_p)) einval("spdm_gcoo: GCOO group arrays do not match ceil(m/p)");
+  if (nnz < 0) einval("spdm_gcoo: negative nnz");
+  const int64_t tiles = groups * ceil_div(n, cfg_b);
+  if (tile_order && tile_count != tiles) einval("spdm_gcoo: tile order must cover every tile once");
+}
+
+// Returns true when the order is a permutation (then it cannot change C);
+// rejects out-of-range ids, which the reference would dereference blindly.
+bool tile_order_is_permutation(const int64_t* order, int64_t count) {
+  std::vector<uint8_t> seen((size_t)count, 0);
+  bool perm = true;
+  for (int64_t i = 0; i < count; ++i) {
+    const int64_t t = order[i];
+    if (t < 0 || t >= count) einval("spdm_gcoo: tile id out of range in tile order");
+    if (seen[(size_t)t]) perm = false;
+    seen[(size_t)t] = 1;
+  }
+  return perm;
+}
+
+template <typename T>
+void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int32_t cfg_b, int64_t b_rows,
+               int64_t nnz, const T* values, const int32_t* row_idx, const int32_t* col_idx, int64_t groups,
+               const int64_t* g_idxes, const int64_t* gnnz, const T* B, T* C, gcoo_stats* stats,
+               const int64_t* tile_order, int64_t tile_count, int flavor) {
+  validate_spdm(m, k, n, a_p, cfg_p, cfg_b, b_rows, nnz, groups, tile_order, tile_count);
+  const bool perm = tile_order ? tile_order_is_permutation(tile_order, tile_count) : true;
+  cudaStream_t s = thread_stream();
+  DevBuf<T> d_vals(nnz, s), d_B(k * n, s), d_C(m * n, s);
+  DevBuf<int32_t> d_rows(nnz, s), d_cols(nnz, s);
+  DevBuf<int64_t> d_gidx(groups, s), d_gnnz(groups, s);
+  h2d(d_vals.get(), values, nnz, s);
+  h2d(d_rows.get(), row_idx, nnz, s);
+  h2d(d_cols.get(), col_idx, nnz, s);
+  h2d(d_gidx.get(), g_idxes, groups, s);
+  h2d(d_gnnz.get(), gnnz, groups, s);
+  h2d(d_B.get(), B, k * n, s);
+  DevGcoo<T> a{m, k, nnz, groups, a_p, d_vals.get(), d_rows.get(), d_cols.get(), d_gidx.get(), d_gnnz.get()};
+  launch_spdm<T>(a, n, d_B.get(), n, d_C.get(), n, flavor, s);
+  if (!perm) {
+    apply_tile_list<T>(a, n, cfg_b, tile_order, tile_count, d_C.get(), n, stats, s);
+  } else if (stats) {
+    device_stats(nnz, n, a_p, cfg_b, groups, d_rows.get(), d_cols.get(), d_gidx.get(), stats, s);
+  }
+  d2h(C, d_C.get(), m * n, s);
+  GCOO_CUDA(cudaStreamSynchronize(s));
+}
+
+template <typename T>
+void spdm_dev(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, int64_t nnz, const T* values,
+              const int32_t* row_idx, const int32_t* col_idx, int64_t groups, const int64_t* g_idxes,
+              const int64_t* gnnz, const T* B, int64_t ldb, T* C, int64_t ldc, gcoo_stats* stats, int flavor,
+              cudaStream_t s) {
+  validate_spdm(m, k, n, p, p, b, k, nnz, groups, nullptr, 0);
+  if (ldb < n || ldc < n) einval("spdm_gcoo: leading dimension smaller than n");
+  DevGcoo<T> a{m, k, nnz, groups, p, values, row_idx, col_idx, g_idxes, gnnz};
+  launch_spdm<T>(a, n, B, ldb, C, ldc, flavor, s);
+  if (stats) device_stats(nnz, n, p, b, groups, row_idx, col_idx, g_idxes, stats, s);
+}
+
+// ------------------------------------------------------- construction -----
+// coo_to_gcoo on device arrays: validate, offsets, log2(p) merge rounds.
+template <typename T>
+void coo_to_gcoo_device(int64_t m, int64_t k, int32_t p, int64_t nnz, const T* vals, const int32_t* rows,
+                        const int32_t* cols, T* ovals, int32_t* orows, int32_t* ocols, int64_t* gidx,
+                        int64_t* gnnz, bool validate, cudaStream_t s) {
+  if (m < 1 || k < 1) einval("CooMatrix: dimensions must be >= 1");
+  if (validate && nnz > 0) {
+    DevBuf<unsigned long long> bad(1, s);
+    GCOO_CUDA(cudaMemsetAsync(bad.get(), 0xff, sizeof(unsigned long long), s));
+    GCOO_LAUNCH(validate_coo_kernel, grid_for(nnz, 256), 256, 0, s, nnz, m, k, rows, cols, bad.get());
+    unsigned long long h = 0;
+    d2h(&h, bad.get(), 1, s);
+    GCOO_CUDA(cudaStreamSynchronize(s));
+    if (h != ~0ull) {
+      const unsigned long long i = h >> 1;
+      if ((h & 1ull) == 0) einval("CooMatrix: coordinate out of range at entry " + std::to_string(i));
+      einval("CooMatrix: entries not in row-major order (or duplicate) at entry " + std::to_string(i));
+    }
+  }
+  if (!is_pow2(p)) einval("coo_to_gcoo: p must be a power of two");
+  const int64_t groups = ceil_div(m, p);
+  DevBuf<int64_t> rp(m + 1, s);
+  GCOO_LAUNCH(row_ptr_kernel, (unsigned)ceil_div(m + 1, 256), 256, 0, s, m, nnz, rows, rp.get());
+  GCOO_LAUNCH(group_offsets_kernel, (unsigned)ceil_div(groups, 256), 256, 0, s, groups, m, p, rp.get(), gidx,
+              gnnz);
+  const int rounds = ilog2(p);
+  if (nnz == 0) return;
+  if (rounds == 0) {
+    GCOO_CUDA(cudaMemcpyAsync(ovals, vals, nnz * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    GCOO_CUDA(cudaMemcpyAsync(orows, rows, nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    GCOO_CUDA(cudaMemcpyAsync(ocols, cols, nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  // ping-pong so that the final round lands in the caller's arrays
+  DevBuf<T> tv(nnz, s);
+  DevBuf<int32_t> tr(nnz, s), tc(nnz, s);
+  const T* iv = vals;
+  const int32_t* ir = rows;
+  const int32_t* ic = cols;
+  for (int t = 0; t < rounds; ++t) {
+    const bool to_out = ((rounds - 1 - t) % 2) == 0;
+    T* ov = to_out ? ovals : tv.get();
+    int32_t* orr = to_out ? orows : tr.get();
+    int32_t* oc = to_out ? ocols : tc.get();
+    GCOO_LAUNCH(merge_round_kernel<T>, grid_for(nnz, 256), 256, 0, s, nnz, m, t, rp.get(), iv, ir, ic, ov, orr,
+                oc);
+    iv = ov;
+    ir = orr;
+    ic = oc;
+  }
+}
+
+template <typename T>
+void coo_to_gcoo_host(int64_t m, int64_t k, int32_t p, int64_t nnz, const T* vals, const int32_t* rows,
+                      const int32_t* cols, T* ovals, int32_t* orows, int32_t* ocols, int64_t* gidx,
+                      int64_t* gnnz) {
+  if (m < 1 || k < 1) einval("CooMatrix: dimensions must be >= 1");
+  if (nnz < 0) einval("CooMatrix: array lengths differ");
+  cudaStream_t s = thread_stream();
+  const int64_t groups = is_pow2(p) ? ceil_div(m, p) : 0;
+  DevBuf<T> dv(nnz, s), dov(nnz, s);
+  DevBuf<int32_t> dr(nnz, s), dc(nnz, s), dor(nnz, s), doc(nnz, s);
+  DevBuf<int64_t> dgi(groups, s), dgn(groups, s);
+  h2d(dv.get(), vals, nnz, s);
+  h2d(dr.get(), rows, nnz, s);
+  h2d(dc.get(), cols, nnz, s);
+  coo_to_gcoo_device<T>(m, k, p, nnz, dv.get(), dr.get(), dc.get(), dov.get(), dor.get(), doc.get(), dgi.get(),
+                        dgn.get(), true, s);
+  d2h(ovals, dov.get(), nnz, s);
+  d2h(orows, dor.get(), nnz, s);
+  d2h(ocols, doc.get(), nnz, s);
+  d2h(gidx, dgi.get(), groups, s);
+  d2h(gnnz, dgn.get(), groups, s);
+  GCOO_CUDA(cudaStreamSynchronize(s));
+}
+
+template <typename T>
+void csr_to_gcoo_host(int64_t m, int64_t k, int32_t p, int64_t nnz, const T* vals, const int32_t* cols,
+                      const int64_t* row_ptr, T* ovals, int32_t* orows, int32_t* ocols, int64_t* gidx,
+                      int64_t* gnnz) {
+  // CsrMatrix::validate, host-checkable parts first (matrix.hpp:126-133)
+  if (m < 1 || k < 1) einval("CsrMatrix: dimensions must be >= 1");
+  if (nnz < 0) einval("CsrMatrix: array lengths differ");
+  if (row_ptr[0] != 0 || row_ptr[m] != nnz) einval("CsrMatrix: row_ptr endpoints wrong");
+  cudaStream_t s = thread_stream();
+  DevBuf<int64_t> drp(m + 1, s);
+  DevBuf<T> dv(nnz, s), dov(nnz, s);
+  DevBuf<int32_t> dr(nnz, s), dc(nnz, s), dor(nnz, s), doc(nnz, s);
+  h2d(drp.get(), row_ptr, m + 1, s);
+  h2d(dv.get(), vals, nnz, s);
+  h2d(dc.get(), cols, nnz, s);
+  {
+    DevBuf<unsigned long long> bad(1, s);
+    GCOO_CUDA(cudaMemsetAsync(bad.get(), 0xff, sizeof(unsigned long long), s));
+    GCOO_LAUNCH(validate_csr_kernel, grid_for(m, 256), 256, 0, s, m, k, drp.get(), dc.get(), bad.get());
+    unsigned long long h = 0;
+    d2h(&h, bad.get(), 1, s);
+    GCOO_CUDA(cudaStreamSynchronize(s));
+    if (h != ~0ull) {
+      if ((h & 1ull) == 0) einval("CsrMatrix: row_ptr not monotone");
+      einval("CsrMatrix: columns not strictly increasing (or out of range) in row " + std::to_string(h >> 1));
+    }
+  }
+  if (!is_pow2(p)) einval("csr_to_gcoo: p must be a power of two");
+  const int64_t groups = ceil_div(m, p);
+  DevBuf<int64_t> dgi(groups, s), dgn(groups, s);
+  if (nnz > 0) GCOO_LAUNCH(expand_rows_kernel, grid_for(nnz, 256), 256, 0, s, nnz, m, drp.get(), dr.get());
+  coo_to_gcoo_device<T>(m, k, p, nnz, dv.get(), dr.get(), dc.get(), dov.get(), dor.get(), doc.get(), dgi.get(),
+                        dgn.get(), false, s);
+  d2h(ovals, dov.get(), nnz, s);
+  d2h(orows, dor.get(), nnz, s);
+  d2h(ocols, doc.get(), nnz, s);
+  d2h(gidx, dgi.get(), groups, s);
+  d2h(gnnz, dgn.get(), groups, s);
+  GCOO_CUDA(cudaStreamSynchronize(s));
+}
+
+// dense_to_gcoo on a device A: returns nnz; fills when capacity allows.
+template <typename T>
+int64_t dense_to_gcoo_device(int64_t m, int64_t k, int32_t p, const T* A, int64_t capacity, T* ovals,
+                             int32_t* orows, int32_t* ocols, int64_t* gidx, int64_t* gnnz, cudaStream_t s) {
+  if (!is_pow2(p)) einval("dense_to_gcoo: p must be a power of two");
+  if (m < 1 || k < 1) einval("DenseMatrix: dimensions must be >= 1");
+  const int64_t groups = ceil_div(m, p);
+  const int64_t n_ct = ceil_div(k, kDenseTileCols);
+  const int64_t tiles = groups * n_ct;
+  DevBuf<int64_t> counts(tiles, s), off(tiles + 1, s);
+  const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * 16);
+  GCOO_LAUNCH(dense_count_kernel<T>, grid, kDenseTileCols, 0, s, m, k, p, A, n_ct, tiles, counts.get());
+  exclusive_scan(counts.get(), off.get(), tiles, s);
+  GCOO_LAUNCH(dense_groups_kernel, (unsigned)ceil_div(groups, 256), 256, 0, s, groups, n_ct, off.get(), gidx,
+              gnnz);
+  int64_t nnz = 0;
+  d2h(&nnz, off.get() + tiles, 1, s);
+  GCOO_CUDA(cudaStreamSynchronize(s));
+  if (nnz > 0 && capacity >= nnz && ovals)
+    GCOO_LAUNCH(dense_fill_kernel<T>, grid, kDenseTileCols, 0, s, m, k, p, A, n_ct, tiles, off.get(), ovals,
+                orows, ocols);
+  return nnz;
+}
+
+// Per-thread slot for the two-call host protocol of dense_to_gcoo.
+struct DenseStash {
+  const void* key = nullptr;
+  int64_t m = 0, k = 0;
+  int32_t p = 0;
+  int dtype = 0;
+  int64_t nnz = -1;
+  std::vector<uint8_t> vals;
+  std::vector<int32_t> rows, cols;
+  std::vector<int64_t> gidx, gnnz;
+};
+thread_local DenseStash t_stash;
+
+template <typename T>
+void dense_to_gcoo_host(int64_t m, int64_t k, int32_t p, const T* A, int64_t capacity, T* ovals,
+                        int32_t* orows, int32_t* ocols, int64_t* gidx, int64_t* gnnz, int64_t* nnz_out) {
+  const int dtype = sizeof(T);
+  DenseStash& st = t_stash;
+  const bool hit = st.key == A && st.m == m && st.k == k && st.p == p && st.dtype == dtype && st.nnz >= 0;
+  if (!(hit && ovals)) {
+    if (!is_pow2(p)) einval("dense_to_gcoo: p must be a power of two");
+    if (m < 1 || k < 1) einval("DenseMatrix: dimensions must be >= 1");
+    cudaStream_t s = thread_stream();
+    const int64_t groups = ceil_div(m, p);
+    DevBuf<T> dA(m * k, s);
+    h2d(dA.get(), A, m * k, s);
+    DevBuf<int64_t> dgi(groups, s), dgn(groups, s);
+    // count first, then allocate exactly nnz entries and fill
+    const int64_t nnz = dense_to_gcoo_device<T>(m, k, p, dA.get(), 0, nullptr, nullptr, nullptr, dgi.get(),
+                                                dgn.get(), s);
+    DevBuf<T> dv(nnz, s);
+    DevBuf<int32_t> dr(nnz, s), dc(nnz, s);
+    dense_to_gcoo_device<T>(m, k, p, dA.get(), nnz, dv.get(), dr.get(), dc.get(), dgi.get(), dgn.get(), s);
+    st.key = A; st.m = m; st.k = k; st.p = p; st.dtype = dtype; st.nnz = nnz;
+    st.vals.resize(nnz * sizeof(T));
+    st.rows.resize(nnz);
+    st.cols.resize(nnz);
+    st.gidx.resize(groups);
+    st.gnnz.resize(groups);
+    d2h(reinterpret_cast<T*>(st.vals.data()), dv.get(), nnz, s);
+    d2h(st.rows.data(), dr.get(), nnz, s);
+    d2h(st.cols.data(), dc.get(), nnz, s);
+    d2h(st.gidx.data(), dgi.get(), groups, s);
+    d2h(st.gnnz.data(), dgn.get(), groups, s);
+    GCOO_CUDA(cudaStreamSynchronize(s));
+  }
+  *nnz_out = st.nnz;
+  if (!ovals) return;  // size query; result kept for the fill call
+  if (capacity < st.nnz) einval("dense_to_gcoo: output capacity smaller than nnz");
+  std::memcpy(ovals, st.vals.data(), st.vals.size());
+  std::memcpy(orows, st.rows.data(), st.rows.size() * sizeof(int32_t));
+  std::memcpy(ocols, st.cols.data(), st.cols.size() * sizeof(int32_t));
+  std::memcpy(gidx, st.gidx.data(), st.gidx.size() * sizeof(int64_t));
+  std::memcpy(gnnz, st.gnnz.data(), st.gnnz.size() * sizeof(int64_t));
+  st = DenseStash{};
+}
+
+}  // namespace gcoo_b200
+
+// =================================================================== C ABI =
+using namespace gcoo_b200;
+
+extern "C" {
+
+int gcoo_abi_version(void) { return GCOO_ABI_VERSION; }
+const char* gcoo_last_error(void) { return t_error.c_str(); }
+
+int gcoo_device_count(int* count) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    c = 0;
+  }
+  *count = c;
+  return GCOO_OK;
+}
+
+int gcoo_set_device(int device) {
+  return guarded([&] {
+    int c = 0;
+    GCOO_CUDA(cudaGetDeviceCount(&c));
+    if (device < 0 || device >= c) einval("gcoo_set_device: no such device");
+    GCOO_CUDA(cudaSetDevice(device));
+    t_device = device;
+  });
+}
+
+uint64_t gcoo_launch_count(void) { return g_launches.load(); }
+
+int gcoo_stream_sync(void* stream) {
+  return guarded([&] { GCOO_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream))); });
+}
+
+int gcoo_spdm_f32(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int32_t cfg_b, int64_t b_rows,
+                  int64_t nnz, const float* values, const int32_t* row_idx, const int32_t* col_idx, int64_t groups,
+                  const int64_t* g_idxes, const int64_t* nnz_per_group, const float* B, float* C,
+                  gcoo_stats* stats, const int64_t* tile_order, int64_t tile_count) {
+  return guarded([&] {
+    spdm_host<float>(m, k, n, a_p, cfg_p, cfg_b, b_rows, nnz, values, row_idx, col_idx, groups, g_idxes,
+                     nnz_per_group, B, C, stats, tile_order, tile_count, GCOO_FLAVOR_FMA);
+  });
+}
+
+int gcoo_spdm_f64(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int32_t cfg_b, int64_t b_rows,
+                  int64_t nnz, const double* values, const int32_t* row_idx, const int32_t* col_idx,
+                  int64_t groups, const int64_t* g_idxes, const int64_t* nnz_per_group, const double* B,
+                  double* C, gcoo_stats* stats, const int64_t* tile_order, int64_t tile_count) {
+  return guarded([&] {
+    spdm_host<double>(m, k, n, a_p, cfg_p, cfg_b, b_rows, nnz, values, row_idx, col_idx, groups, g_idxes,
+                      nnz_per_group, B, C, stats, tile_order, tile_count, GCOO_FLAVOR_FMA);
+  });
+}
+
+int gcoo_spdm_f32_dev(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, int64_t nnz, const float* values,
+                      const int32_t* row_idx, const int32_t* col_idx, int64_t groups, const int64_t* g_idxes,
+                      const int64_t* nnz_per_group, const float* B, int64_t ldb, float* C, int64_t ldc,
+                      gcoo_stats* stats, int flavor, void* stream) {
+  return guarded([&] {
+    spdm_dev<float>(m, k, n, p, b, nnz, values, row_idx, col_idx, groups, g_idxes, nnz_per_group, B, ldb, C,
+                    ldc, stats, flavor, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int gcoo_spdm_f64_dev(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, int64_t nnz, const double* values,
+                      const int32_t* row_idx, const int32_t* col_idx, int64_t groups, const int64_t* g_idxes,
+                      const int64_t* nnz_per_group, const double* B, int64_t ldb, double* C, int64_t ldc,
+                      gcoo_stats* stats, int flavor, void* stream) {
+  return guarded([&] {
+    spdm_dev<double>(m, k, n, p, b, nnz, values, row_idx, col_idx, groups, g_idxes, nnz_per_group, B, ldb, C,
+                     ldc, stats, flavor, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int gcoo_stats_dev(int64_t m, int64_t n, int32_t p, int32_t b, int64_t nnz, const int32_t* row_idx,
+                   const int32_t* col_idx, int64_t groups, const int64_t* g_idxes, gcoo_stats* stats,
+                   void* stream) {
+  return guarded([&] {
+    if (!is_pow2(p) || !is_pow2(b)) einval("ExecConfig: p and b must be powers of two");
+    if (groups != ceil_div(m, p)) einval("gcoo_stats: group arrays do not match ceil(m/p)");
+    device_stats(nnz, n, p, b, groups, row_idx, col_idx, g_idxes, stats, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int gcoo_coo_to_gcoo_f32(int64_t m, int64_t k, int32_t p, int64_t nnz, const float* values, const int32_t* row_idx,
+                         const int32_t* col_idx, float* out_values, int32_t* out_row_idx, int32_t* out_col_idx,
+                         int64_t* g_idxes, int64_t* nnz_per_group) {
+  return guarded([&] {
+    coo_to_gcoo_host<float>(m, k, p, nnz, values, row_idx, col_idx, out_values, out_row_idx, out_col_idx,
+                            g_idxes, nnz_per_group);
+  });
+}
+
+int gcoo_coo_to_gcoo_f64(int64_t m, int64_t k, int32_t p, int64_t nnz, const double* values,
+                         const int32_t* row_idx, const int32_t* col_idx, double* out_values, int32_t* out_row_idx,
+                         int32_t* out_col_idx, int64_t* g_idxes, int64_t* nnz_per_group) {
+  return guarded([&] {
+    coo_to_gcoo_host<double>(m, k, p, nnz, values, row_idx, col_idx, out_values, out_row_idx, out_col_idx,
+                             g_idxes, nnz_per_group);
+  });
+}
+
+int gcoo_coo_to_gcoo_f32_dev(int64_t m, int64_t k, int32_t p, int64_t nnz, const float* values,
+                             const int32_t* row_idx, const int32_t* col_idx, float* out_values,
+                             int32_t* out_row_idx, int32_t* out_col_idx, int64_t* g_idxes,
+                             int64_t* nnz_per_group, void* stream) {
+  return guarded([&] {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    coo_to_gcoo_device<float>(m, k, p, nnz, values, row_idx, col_idx, out_values, out_row_idx, out_col_idx,
+                              g_idxes, nnz_per_group, true, s);
+  });
+}
+
+int gcoo_csr_to_gcoo_f32(int64_t m, int64_t k, int32_t p, int64_t nnz, const float* values, const int32_t* col_idx,
+                         const int64_t* row_ptr, float* out_values, int32_t* out_row_idx, int32_t* out_col_idx,
+                         int64_t* g_idxes, int64_t* nnz_per_group) {
+  return guarded([&] {
+    csr_to_gcoo_host<float>(m, k, p, nnz, values, col_idx, row_ptr, out_values, out_row_idx, out_col_idx,
+                            g_idxes, nnz_per_group);
+  });
+}
+
+int gcoo_csr_to_gcoo_f64(int64_t m, int64_t k, int32_t p, int64_t nnz, const double* values,
+                         const int32_t* col_idx, const int64_t* row_ptr, double* out_values, int32_t* out_row_idx,
+                         int32_t* out_col_idx, int64_t* g_idxes, int64_t* nnz_per_group) {
+  return guarded([&] {
+    csr_to_gcoo_host<double>(m, k, p, nnz, values, col_idx, row_ptr, out_values, out_row_idx, out_col_idx,
+                             g_idxes, nnz_per_group);
+  });
+}
+
+int gcoo_dense_to_gcoo_f32(int64_t m, int64_t k, int32_t p, const float* A, int64_t capacity, float* out_values,
+                           int32_t* out_row_idx, int32_t* out_col_idx, int64_t* g_idxes, int64_t* nnz_per_group,
+                           int64_t* nnz) {
+  return guarded([&] {
+    dense_to_gcoo_host<float>(m, k, p, A, capacity, out_values, out_row_idx, out_col_idx, g_idxes, nnz_per_group,
+                              nnz);
+  });
+}
+
+int gcoo_dense_to_gcoo_f64(int64_t m, int64_t k, int32_t p, const double* A, int64_t capacity,
+                           double* out_values, int32_t* out_row_idx, int32_t* out_col_idx, int64_t* g_idxes,
+                           int64_t* nnz_per_group, int64_t* nnz) {
+  return guarded([&] {
+    dense_to_gcoo_host<double>(m, k, p, A, capacity, out_values, out_row_idx, out_col_idx, g_idxes,
+                               nnz_per_group, nnz);
+  });
+}
+
+int gcoo_dense_to_gcoo_f32_dev(int64_t m, int64_t k, int32_t p, const float* A, int64_t capacity,
+                               float* out_values, int32_t* out_row_idx, int32_t* out_col_idx, int64_t* g_idxes,
+                               int64_t* nnz_per_group, int64_t* nnz, void* stream) {
+  return guarded([&] {
+    *nnz = dense_to_gcoo_device<float>(m, k, p, A, capacity, out_values, out_row_idx, out_col_idx, g_idxes,
+                                       nnz_per_group, static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"

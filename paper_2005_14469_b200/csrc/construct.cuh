@@ -1,0 +1,328 @@
+// construct.cuh — GCOO construction and counter kernels (K2-K5).
+//
+//  K2 coo_to_gcoo   (matrix.hpp:366-405): validate -> row offsets -> group
+//     offsets -> log2(p) rounds of pairwise merges of (col,row)-sorted runs.
+//     A row-major COO is a sequence of single-row runs, each sorted by col;
+//     round t merges runs of 2^t rows pairwise, every entry computing its
+//     destination with one binary search in the partner run.  After log2(p)
+//     rounds each p-row band is one (col,row)-sorted slice: the GCOO.  Keys
+//     (col,row) are unique inside a band, so the result is the unique sorted
+//     order — bit-exact with the reference's std::sort, no tie-breaking.
+//  K3 dense_to_gcoo (matrix.hpp:306-353): per (band, 256-column tile) count ->
+//     device exclusive scan -> per-tile fill in column-major-within-band order.
+//  K4 run counter   (kernels.hpp:283-310): KernelStats for the caller's b.
+//  K5 csr_to_gcoo   (new): validate CSR -> expand row_ptr to row indices -> K2.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace gcoo_b200 {
+
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+// ---------------------------------------------------------------- scan ----
+// Block-wide exclusive scan of per-thread int64 values; returns the block total.
+template <int NT>
+__device__ __forceinline__ int64_t block_exclusive_scan(int64_t x, int64_t& total) {
+  __shared__ int64_t warp_sums[NT / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t incl = x;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  if (lane == 31) warp_sums[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = lane < NT / 32 ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= d) w += y;
+    }
+    if (lane < NT / 32) warp_sums[lane] = w;  // inclusive warp prefix
+  }
+  __syncthreads();
+  const int64_t warp_off = warp ? warp_sums[warp - 1] : 0;
+  total = warp_sums[NT / 32 - 1];
+  __syncthreads();
+  return warp_off + incl - x;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+scan_tiles_kernel(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t n,
+                  int64_t* __restrict__ tile_sums) {
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int64_t v[kScanItems], s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = base + i < n ? in[base + i] : 0;
+    s += v[i];
+  }
+  int64_t total;
+  int64_t run = block_exclusive_scan<kScanThreads>(s, total);
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < n) out[base + i] = run;
+    run += v[i];
+  }
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+
+__global__ void add_tile_offsets_kernel(int64_t* __restrict__ out, int64_t n,
+                                        const int64_t* __restrict__ tile_off) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] += tile_off[i / kScanTile];
+}
+
+__global__ void write_total_kernel(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t n) {
+  out[n] = n > 0 ? out[n - 1] + in[n - 1] : 0;
+}
+
+// --------------------------------------------------------------- K2 -------
+// First invalid entry, encoded 2*i + kind (kind 0: coordinate out of range,
+// 1: not strictly row-major / duplicate), in CooMatrix::validate's order.
+__global__ void validate_coo_kernel(int64_t nnz, int64_t m, int64_t k, const int32_t* __restrict__ rows,
+                                    const int32_t* __restrict__ cols, unsigned long long* first_bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = rows[i], c = cols[i];
+    unsigned long long code = ~0ull;
+    if (r < 0 || r >= m || c < 0 || c >= k) {
+      code = 2ull * (unsigned long long)i;
+    } else if (i > 0) {
+      const int32_t pr = rows[i - 1], pc = cols[i - 1];
+      if (!(pr < r || (pr == r && pc < c))) code = 2ull * (unsigned long long)i + 1ull;
+    }
+    if (code != ~0ull) atomicMin(first_bad, code);
+  }
+}
+
+// row_ptr[r] = #entries with row < r, r in [0, m] (binary search; rows sorted)
+__global__ void row_ptr_kernel(int64_t m, int64_t nnz, const int32_t* __restrict__ rows,
+                               int64_t* __restrict__ rp) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > m) return;
+  int64_t lo = 0, hi = nnz;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (rows[mid] < r) lo = mid + 1; else hi = mid;
+  }
+  rp[r] = lo;
+}
+
+__global__ void group_offsets_kernel(int64_t groups, int64_t m, int32_t p, const int64_t* __restrict__ rp,
+                                     int64_t* __restrict__ gidx, int64_t* __restrict__ gnnz) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= groups) return;
+  const int64_t lo = g * p;
+  const int64_t hi = lo + p < m ? lo + p : m;
+  gidx[g] = rp[lo];
+  gnnz[g] = rp[hi] - rp[lo];
+}
+
+// One merge round: runs of 2^t rows -> runs of 2^(t+1) rows.
+template <typename T>
+__global__ void merge_round_kernel(int64_t nnz, int64_t m, int t, const int64_t* __restrict__ rp,
+                                   const T* __restrict__ vin, const int32_t* __restrict__ rin,
+                                   const int32_t* __restrict__ cin, T* __restrict__ vout,
+                                   int32_t* __restrict__ rout, int32_t* __restrict__ cout) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = rin[i], c = cin[i];
+    const int64_t q = (int64_t)r >> t;           // own run
+    const int64_t pq = q ^ 1;                    // partner run
+    const int64_t own_lo = rp[q << t];
+    const int64_t pair_lo = rp[(q >> 1) << (t + 1)];
+    int64_t plo_row = pq << t, phi_row = (pq + 1) << t;
+    if (plo_row > m) plo_row = m;
+    if (phi_row > m) phi_row = m;
+    int64_t lo = rp[plo_row], hi = rp[phi_row];
+    // count partner entries with (col,row) < (c,r)
+    const int64_t start = lo;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      const int32_t mc = cin[mid], mr = rin[mid];
+      if (mc < c || (mc == c && mr < r)) lo = mid + 1; else hi = mid;
+    }
+    const int64_t dst = pair_lo + (i - own_lo) + (lo - start);
+    vout[dst] = vin[i];
+    rout[dst] = r;
+    cout[dst] = c;
+  }
+}
+
+// --------------------------------------------------------------- K5 -------
+// CsrMatrix::validate (matrix.hpp:122-165) after the host-side size checks:
+// first bad row (2*r: row_ptr not monotone, 2*r+1: column out of range or not
+// strictly increasing).
+__global__ void validate_csr_kernel(int64_t m, int64_t k, const int64_t* __restrict__ rp,
+                                    const int32_t* __restrict__ cols, unsigned long long* first_bad) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = rp[r], b = rp[r + 1];
+    unsigned long long code = ~0ull;
+    if (a > b) {
+      code = 2ull * (unsigned long long)r;
+    } else {
+      for (int64_t e = a; e < b; ++e) {
+        const int32_t c = cols[e];
+        if (c < 0 || c >= k || (e > a && cols[e - 1] >= c)) { code = 2ull * (unsigned long long)r + 1ull; break; }
+      }
+    }
+    if (code != ~0ull) atomicMin(first_bad, code);
+  }
+}
+
+__global__ void expand_rows_kernel(int64_t nnz, int64_t m, const int64_t* __restrict__ rp,
+                                   int32_t* __restrict__ rows) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = m + 1;  // first index with rp[idx] > i
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (rp[mid] <= i) lo = mid + 1; else hi = mid;
+    }
+    rows[i] = (int32_t)(lo - 1);
+  }
+}
+
+// --------------------------------------------------------------- K3 -------
+constexpr int kDenseTileCols = 256;
+
+// counts[g * n_ct + ct] = nonzeros of band g in columns [ct*256, ct*256+256)
+template <typename T>
+__global__ void __launch_bounds__(kDenseTileCols)
+dense_count_kernel(int64_t m, int64_t k, int32_t p, const T* __restrict__ A, int64_t n_ct,
+                   int64_t tiles, int64_t* __restrict__ counts) {
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t g = tile / n_ct, ct = tile % n_ct;
+    const int64_t c = ct * kDenseTileCols + threadIdx.x;
+    const int64_t lo = g * p;
+    const int64_t hi = lo + p < m ? lo + p : m;
+    int64_t cnt = 0;
+    if (c < k)
+      for (int64_t r = lo; r < hi; ++r) cnt += A[r * k + c] != T(0);
+    // block reduction
+#pragma unroll
+    for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+    __shared__ int64_t ws[kDenseTileCols / 32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t s = 0;
+      for (int w = 0; w < kDenseTileCols / 32; ++w) s += ws[w];
+      counts[tile] = s;
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kDenseTileCols)
+dense_fill_kernel(int64_t m, int64_t k, int32_t p, const T* __restrict__ A, int64_t n_ct, int64_t tiles,
+                  const int64_t* __restrict__ tile_off, T* __restrict__ vals, int32_t* __restrict__ rows,
+                  int32_t* __restrict__ cols) {
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t g = tile / n_ct, ct = tile % n_ct;
+    const int64_t c = ct * kDenseTileCols + threadIdx.x;
+    const int64_t lo = g * p;
+    const int64_t hi = lo + p < m ? lo + p : m;
+    int64_t cnt = 0;
+    if (c < k)
+      for (int64_t r = lo; r < hi; ++r) cnt += A[r * k + c] != T(0);
+    int64_t total;
+    int64_t w = tile_off[tile] + block_exclusive_scan<kDenseTileCols>(cnt, total);
+    if (c < k)
+      for (int64_t r = lo; r < hi; ++r) {
+        const T a = A[r * k + c];
+        if (a != T(0)) {
+          vals[w] = a;
+          rows[w] = (int32_t)r;
+          cols[w] = (int32_t)c;
+          ++w;
+        }
+      }
+  }
+}
+
+__global__ void dense_groups_kernel(int64_t groups, int64_t n_ct, const int64_t* __restrict__ tile_off,
+                                    int64_t* __restrict__ gidx, int64_t* __restrict__ gnnz) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= groups) return;
+  gidx[g] = tile_off[g * n_ct];
+  gnnz[g] = tile_off[(g + 1) * n_ct] - tile_off[g * n_ct];
+}
+
+// --------------------------------------------------------------- K4 -------
+// Number of staged runs summed over groups: a position e (0-based inside its
+// group's slice) starts a run iff e % b == 0 (a staging refill,
+// kernels.hpp:283) or its column differs from the previous entry's (:294-296).
+__global__ void run_count_kernel(int64_t nnz, int32_t p, int32_t b, int64_t groups,
+                                 const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
+                                 const int64_t* __restrict__ gidx, unsigned long long* runs) {
+  unsigned long long local = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = (int64_t)rows[i] / p;
+    if (g < 0 || g >= groups) continue;
+    const int64_t e = i - gidx[g];
+    if ((e & (b - 1)) == 0 || cols[i] != cols[i - 1]) ++local;
+  }
+#pragma unroll
+  for (int d = 16; d; d >>= 1) local += __shfl_xor_sync(0xffffffffu, local, d);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(runs, local);
+}
+
+// Per-group run counts (for an explicit, non-permutation tile order).
+__global__ void group_runs_kernel(int64_t nnz, int32_t p, int32_t b, int64_t groups,
+                                  const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
+                                  const int64_t* __restrict__ gidx, unsigned long long* runs) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = (int64_t)rows[i] / p;
+    if (g < 0 || g >= groups) continue;
+    const int64_t e = i - gidx[g];
+    if ((e & (b - 1)) == 0 || cols[i] != cols[i - 1]) atomicAdd(&runs[g], 1ull);
+  }
+}
+
+// Stats over an explicit tile list (duplicates count twice, as in the
+// reference's loop over tile_order) and coverage counts per tile.
+__global__ void tile_list_kernel(int64_t count, const int64_t* __restrict__ order, int64_t col_tiles,
+                                 int64_t n, int32_t b, const int64_t* __restrict__ gnnz,
+                                 const unsigned long long* __restrict__ gruns, unsigned int* cover,
+                                 unsigned long long* st) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tile = order[t];
+    const int64_t g = tile / col_tiles, sj = tile % col_tiles;
+    const int64_t j0 = sj * b;
+    const unsigned long long w = (unsigned long long)(b < n - j0 ? b : n - j0);
+    const unsigned long long cnt = (unsigned long long)gnnz[g], runs = gruns[g];
+    atomicAdd(&cover[tile], 1u);
+    atomicAdd(&st[0], 2ull * cnt * w);
+    atomicAdd(&st[1], runs * w);
+    atomicAdd(&st[2], (cnt - runs) * w);
+    atomicAdd(&st[3], cnt);
+  }
+}
+
+// Tiles absent from the list are never written by the reference: C stays 0.
+template <typename T>
+__global__ void zero_uncovered_kernel(int64_t m, int64_t n, int32_t p, int32_t b, int64_t col_tiles,
+                                      const unsigned int* __restrict__ cover, T* __restrict__ C,
+                                      int64_t ldc) {
+  const int64_t total = m * n;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = x / n, j = x % n;
+    if (!cover[(i / p) * col_tiles + j / b]) C[i * ldc + j] = T(0);
+  }
+}
+
+}  // namespace gcoo_b200
