@@ -41,6 +41,11 @@ def _p(a: np.ndarray | None):
     return None if a is None else a.ctypes.data_as(_vp)
 
 
+def _n(x) -> int:
+    """nnz/groups as attribute (oracle Gcoo) or method (product GcooMatrix)."""
+    return int(x() if callable(x) else x)
+
+
 @dataclass
 class Gcoo:
     """Host GCOO arrays with the reference's field names (matrix.hpp:176-245)."""
@@ -258,7 +263,7 @@ class Reference:
         st = (_u64 * 4)()
         f = self.lib.ref_spdm_gcoo_f32 if B.dtype == np.float32 else self.lib.ref_spdm_gcoo_f64
         to = None if tile_order is None else np.ascontiguousarray(tile_order, dtype=np.int64)
-        self._check(f(g.rows_dim, k, n, g.p, b, g.nnz, _p(g.values), _p(g.row_idx), _p(g.col_idx), g.groups,
+        self._check(f(g.rows_dim, k, n, g.p, b, _n(g.nnz), _p(g.values), _p(g.row_idx), _p(g.col_idx), _n(g.groups),
                       _p(g.g_idxes), _p(g.nnz_per_group), _p(np.ascontiguousarray(B)), _p(Cm), st, workers,
                       _p(to), 0 if to is None else to.size))
         return Cm, tuple(int(x) for x in st)

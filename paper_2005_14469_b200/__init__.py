@@ -97,6 +97,7 @@ def lib():
     _sig(L, "gcoo_generate_uniform_sparse_coo_f32", _int, [_i64, _dbl, _u64, _i64, _vp, _vp, _vp, C.POINTER(_i64)])
     _sig(L, "gcoo_generate_powerlaw_coo_f32", _int, [_i64, _dbl, _dbl, _u64, _i64, _vp, _vp, _vp, C.POINTER(_i64)])
     _sig(L, "gcoo_derive_seed", _u64, [_u64, _u64, _u64])
+    _sig(L, "gcoo_debug_force_kernel", _int, [_int])
     _lib = L
     return L
 
@@ -128,6 +129,14 @@ def device_count() -> int:
 
 def set_device(device: int) -> None:
     _check(lib().gcoo_set_device(device))
+
+
+KERNELS = {"auto": -1, "rowtile": 0, "panel_wide": 1, "panel_tall": 2}
+
+
+def force_kernel(which: str = "auto") -> None:
+    """Test/benchmark hook: pin the fp32 multiply kernel (auto = heuristic)."""
+    lib().gcoo_debug_force_kernel(KERNELS[which])
 
 
 def launch_count() -> int:

@@ -5,6 +5,7 @@
 // stream-ordered pool, copies, and kernel launches.  All arithmetic on matrix
 // data happens in the CUDA kernels (spdm_rowtile.cuh, spdm_panel.cuh,
 // construct.cuh); there is no host compute path.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -162,15 +163,96 @@ void launch_rowtile_p(const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T
   }
 }
 
+// ------------------------------------------------------- panel path -----
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    GCOO_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) fail(GCOO_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// B (k x n, leading dimension ldb) as a 2-D fp32 tensor; box = W columns x KC rows.
+CUtensorMap make_b_map(const float* B, int64_t k, int64_t n, int64_t ldb, int box_w, int box_k) {
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)k};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldb * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)box_k};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(B), dims, strides,
+                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(GCOO_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return map;
+}
+
+template <class Cfg>
+bool panel_fits(const DevGcoo<float>& a, int64_t n, int64_t ldb, int64_t ldc, const float* B, const float* C) {
+  return a.p <= Cfg::RW && a.k < (int64_t(1) << kColBits) && ldb % 4 == 0 && ldc % Cfg::V == 0 &&
+         n % Cfg::V == 0 && (reinterpret_cast<uintptr_t>(B) % 16) == 0 &&
+         (reinterpret_cast<uintptr_t>(C) % (4 * Cfg::V)) == 0 && a.k <= INT32_MAX && n <= INT32_MAX;
+}
+
+template <class Cfg>
+void launch_panel(const DevGcoo<float>& a, int64_t n, const float* B, int64_t ldb, float* C, int64_t ldc,
+                  cudaStream_t s) {
+  static bool attr_set[64] = {};
+  int d = 0;
+  GCOO_CUDA(cudaGetDevice(&d));
+  if (!attr_set[d]) {
+    GCOO_CUDA(cudaFuncSetAttribute(spdm_panel_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)Cfg::SMEM));
+    attr_set[d] = true;
+  }
+  const int64_t tiles = ceil_div(a.m, Cfg::RW);
+  DevBuf<uint2> ent(a.nnz, s);
+  if (a.nnz > 0)
+    GCOO_LAUNCH(regroup_pack_kernel<Cfg::RW>, (unsigned)std::min<int64_t>(tiles, (int64_t)sm_count() * 16),
+                kRegroupThreads, 0, s, a.m, a.p, a.groups, a.nnz, a.vals, a.rows, a.cols, a.gidx, ent.get(),
+                tiles);
+  const CUtensorMap map = make_b_map(B, a.k, n, ldb, Cfg::W, Cfg::KC);
+  const int64_t row_blocks = ceil_div(a.m, Cfg::RB);
+  const int64_t col_tiles = ceil_div(n, Cfg::W);
+  const int64_t grid = row_blocks * col_tiles;
+  const int nchunks = (int)ceil_div(a.k, Cfg::KC);
+  if (grid > INT32_MAX) fail(GCOO_EINVAL, "spdm_gcoo: problem too large for one launch");
+  GCOO_LAUNCH(spdm_panel_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n, a.p, a.groups,
+              a.nnz, ent.get(), a.gidx, C, ldc, row_blocks, nchunks);
+}
+
+// Which fp32 kernel runs: the panel kernel whenever layout allows (wide
+// strips when the row block holds enough nonzeros per B row, tall otherwise),
+// the row-tile kernel for everything else.
+int g_force_kernel = -1;  // test hook: -1 auto, 0 row-tile, 1 wide, 2 tall
+
 template <typename T>
 void launch_spdm(const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C, int64_t ldc, int flavor,
                  cudaStream_t s) {
   if (a.m == 0 || n == 0) return;
   const bool fma = flavor != GCOO_FLAVOR_MUL_ADD;
   if constexpr (std::is_same<T, float>::value) {
-    if (fma && panel_applicable(a.m, a.k, n, ldb, ldc, B, C)) {
-      launch_panel(a.m, a.k, n, a.p, a.groups, a.vals, a.rows, a.cols, a.gidx, a.gnnz, B, ldb, C, ldc, s);
-      return;
+    if (fma && g_force_kernel != 0) {
+      const double density = (double)a.nnz / ((double)a.m * (double)a.k);
+      const bool wide_ok = panel_fits<PanelWide>(a, n, ldb, ldc, B, C);
+      const bool tall_ok = panel_fits<PanelTall>(a, n, ldb, ldc, B, C);
+      bool use_wide = wide_ok && (density * PanelWide::RB >= 12.0 || !tall_ok);
+      if (g_force_kernel == 1) use_wide = wide_ok;
+      if (g_force_kernel == 2) use_wide = false;
+      if (use_wide) {
+        launch_panel<PanelWide>(a, n, B, ldb, C, ldc, s);
+        return;
+      }
+      if (tall_ok && g_force_kernel != 1) {
+        launch_panel<PanelTall>(a, n, B, ldb, C, ldc, s);
+        return;
+      }
     }
   }
   if (fma) launch_rowtile_p<T, true>(a, n, B, ldb, C, ldc, s);
@@ -526,6 +608,12 @@ int gcoo_set_device(int device) {
 }
 
 uint64_t gcoo_launch_count(void) { return g_launches.load(); }
+
+// Test/benchmark hook (not in the public header): pin the fp32 kernel choice.
+int gcoo_debug_force_kernel(int which) {
+  g_force_kernel = which;
+  return GCOO_OK;
+}
 
 int gcoo_stream_sync(void* stream) {
   return guarded([&] { GCOO_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream))); });

@@ -98,6 +98,27 @@ def test_random_shapes_bit_exact(gcoo, cuda, oracle, seed):
         assert max_rel(c, c_mad) <= 1e-5
 
 
+@pytest.mark.parametrize("kernel", ["rowtile", "panel_wide", "panel_tall", "auto"])
+def test_each_fp32_kernel_bit_exact(gcoo, cuda, oracle, kernel):
+    """Every fp32 kernel variant, on shapes that hit its edges (m not a multiple
+    of the row block, k not a multiple of the chunk, n not a multiple of the
+    strip, empty rows/tiles, every p the variant supports)."""
+    rng = np.random.default_rng(hash(kernel) % 1000)
+    gcoo.force_kernel(kernel)
+    try:
+        for m, k, n, p, dens in [(1, 1, 4, 1, 1.0), (300, 200, 132, 4, 0.02), (777, 1000, 256, 1, 0.01),
+                                 (513, 129, 68, 16, 0.2), (1030, 333, 200, 8, 0.05), (64, 4000, 512, 2, 0.003),
+                                 (2000, 700, 196, 32, 0.01), (100, 100, 1024, 4, 0.0)]:
+            a = rand_dense(rng, m, k, dens)
+            bm = rand_dense(rng, k, n, 1.0)
+            go = oracle.dense_to_gcoo(a, p)
+            c_ref, _ = oracle.spdm(go, bm, 64, fma=True)
+            c = gcoo.spdm_gcoo(to_prod(gcoo, go), bm, gcoo.ExecConfig(p=p))
+            assert np.array_equal(c, c_ref), (kernel, m, k, n, p)
+    finally:
+        gcoo.force_kernel("auto")
+
+
 def test_f64(gcoo, cuda, oracle):
     rng = np.random.default_rng(77)
     for _ in range(6):
