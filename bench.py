@@ -129,6 +129,7 @@ def make_inputs(G, n, s, seed, dev, n_cols):
     dg = G.dense_to_gcoo_dev(dA, P)
     del dA
     dB = torch.from_numpy(b).to(dev)
+    torch.cuda.synchronize()  # inputs complete before other streams use them
     return a, b, dg, dB
 
 

@@ -39,7 +39,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libgcoo_cuda.so")
+LIB_PATH = os.environ.get("GCOO_LIB") or os.path.join(PKG, "lib", "libgcoo_cuda.so")
 
 _i64, _i32, _u64, _dbl, _vp, _int = C.c_int64, C.c_int32, C.c_uint64, C.c_double, C.c_void_p, C.c_int
 
@@ -98,6 +98,7 @@ def lib():
     _sig(L, "gcoo_generate_powerlaw_coo_f32", _int, [_i64, _dbl, _dbl, _u64, _i64, _vp, _vp, _vp, C.POINTER(_i64)])
     _sig(L, "gcoo_derive_seed", _u64, [_u64, _u64, _u64])
     _sig(L, "gcoo_debug_force_kernel", _int, [_int])
+    _sig(L, "gcoo_debug_raster_rows", _int, [_int])
     _lib = L
     return L
 
@@ -131,12 +132,17 @@ def set_device(device: int) -> None:
     _check(lib().gcoo_set_device(device))
 
 
-KERNELS = {"auto": -1, "rowtile": 0, "panel_wide": 1, "panel_tall": 2}
+KERNELS = {"auto": -1, "rowtile": 0, "panel_wide": 1, "panel_tall": 2, "panel_k128": 3, "panel_k96": 4}
 
 
 def force_kernel(which: str = "auto") -> None:
     """Test/benchmark hook: pin the fp32 multiply kernel (auto = heuristic)."""
     lib().gcoo_debug_force_kernel(KERNELS[which])
+
+
+def raster_rows(rows: int = 0) -> None:
+    """Tuning hook: row blocks per rasterisation band of the panel kernel (0 = all)."""
+    lib().gcoo_debug_raster_rows(rows)
 
 
 def launch_count() -> int:
@@ -453,8 +459,11 @@ def coo_to_gcoo_dev(rows_dim: int, cols_dim: int, values, row_idx, col_idx, p: i
     oc = torch.empty(n, dtype=torch.int32, device=dev)
     gi = torch.empty(g, dtype=torch.int64, device=dev)
     gn = torch.empty(g, dtype=torch.int64, device=dev)
+    sp = _stream_ptr(stream)
     _check(lib().gcoo_coo_to_gcoo_f32_dev(rows_dim, cols_dim, p, n, _p(values), _p(row_idx), _p(col_idx), _p(ov),
-                                          _p(orr), _p(oc), _p(gi), _p(gn), _stream_ptr(stream)))
+                                          _p(orr), _p(oc), _p(gi), _p(gn), sp))
+    # setup routine: finish before the arrays are handed to other streams
+    _check(lib().gcoo_stream_sync(sp))
     return DeviceGcoo(rows_dim, cols_dim, p, ov, orr, oc, gi, gn)
 
 
@@ -477,6 +486,8 @@ def dense_to_gcoo_dev(a, p: int, stream=None) -> DeviceGcoo:
     oc = torch.empty(n, dtype=torch.int32, device=dev)
     _check(L.gcoo_dense_to_gcoo_f32_dev(m, k, p, _p(a), n, _p(ov), _p(orr), _p(oc), _p(gi), _p(gn),
                                         C.byref(nnz), sp))
+    # setup routine: finish before the arrays are handed to other streams
+    _check(L.gcoo_stream_sync(sp))
     return DeviceGcoo(m, k, p, ov, orr, oc, gi, gn)
 
 

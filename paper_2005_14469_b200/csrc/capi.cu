@@ -195,10 +195,12 @@ CUtensorMap make_b_map(const float* B, int64_t k, int64_t n, int64_t ldb, int bo
 
 template <class Cfg>
 bool panel_fits(const DevGcoo<float>& a, int64_t n, int64_t ldb, int64_t ldc, const float* B, const float* C) {
-  return a.p <= Cfg::RW && a.k < (int64_t(1) << kColBits) && ldb % 4 == 0 && ldc % Cfg::V == 0 &&
-         n % Cfg::V == 0 && (reinterpret_cast<uintptr_t>(B) % 16) == 0 &&
-         (reinterpret_cast<uintptr_t>(C) % (4 * Cfg::V)) == 0 && a.k <= INT32_MAX && n <= INT32_MAX;
+  return a.p <= Cfg::RW && ldb % 4 == 0 && ldc % Cfg::V == 0 && n % Cfg::V == 0 &&
+         (reinterpret_cast<uintptr_t>(B) % 16) == 0 && (reinterpret_cast<uintptr_t>(C) % (4 * Cfg::V)) == 0 &&
+         a.k <= (int64_t)INT32_MAX - Cfg::KC && n <= INT32_MAX;
 }
+
+int g_raster_rows = 0;  // tuning hook: row blocks per rasterisation band (0 = all)
 
 template <class Cfg>
 void launch_panel(const DevGcoo<float>& a, int64_t n, const float* B, int64_t ldb, float* C, int64_t ldc,
@@ -212,25 +214,32 @@ void launch_panel(const DevGcoo<float>& a, int64_t n, const float* B, int64_t ld
     attr_set[d] = true;
   }
   const int64_t tiles = ceil_div(a.m, Cfg::RW);
-  DevBuf<uint2> ent(a.nnz, s);
-  if (a.nnz > 0)
-    GCOO_LAUNCH(regroup_pack_kernel<Cfg::RW>, (unsigned)std::min<int64_t>(tiles, (int64_t)sm_count() * 16),
-                kRegroupThreads, 0, s, a.m, a.p, a.groups, a.nnz, a.vals, a.rows, a.cols, a.gidx, ent.get(),
-                tiles);
+  const int nchunks = (int)ceil_div(a.k, Cfg::KC);
+  const int64_t nseg = tiles * (int64_t)nchunks;
+  // planner: segment lengths -> offsets -> entries + headers
+  DevBuf<int64_t> seg_len(nseg, s), seg_off(nseg + 1, s);
+  GCOO_LAUNCH(plan_count_kernel<Cfg>, grid_for(nseg, 256), 256, 0, s, a.p, a.groups, a.nnz, a.cols, a.gidx, tiles,
+              nchunks, seg_len.get());
+  exclusive_scan(seg_len.get(), seg_off.get(), nseg, s);
+  int64_t stream_len = 0;
+  d2h(&stream_len, seg_off.get() + nseg, 1, s);
+  GCOO_CUDA(cudaStreamSynchronize(s));
+  DevBuf<uint2> ent(stream_len + Cfg::CAP, s);
+  GCOO_LAUNCH(plan_fill_kernel<Cfg>, (unsigned)std::min<int64_t>(tiles, (int64_t)sm_count() * 8), kPlanThreads, 0,
+              s, a.p, a.groups, a.nnz, a.vals, a.rows, a.cols, a.gidx, seg_off.get(), ent.get(), tiles, nchunks);
   const CUtensorMap map = make_b_map(B, a.k, n, ldb, Cfg::W, Cfg::KC);
   const int64_t row_blocks = ceil_div(a.m, Cfg::RB);
   const int64_t col_tiles = ceil_div(n, Cfg::W);
   const int64_t grid = row_blocks * col_tiles;
-  const int nchunks = (int)ceil_div(a.k, Cfg::KC);
   if (grid > INT32_MAX) fail(GCOO_EINVAL, "spdm_gcoo: problem too large for one launch");
-  GCOO_LAUNCH(spdm_panel_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n, a.p, a.groups,
-              a.nnz, ent.get(), a.gidx, C, ldc, row_blocks, nchunks);
+  const int64_t group_rows = g_raster_rows > 0 ? std::min<int64_t>(g_raster_rows, row_blocks) : row_blocks;
+  GCOO_LAUNCH(spdm_panel_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n, ent.get(),
+              seg_off.get(), C, ldc, row_blocks, col_tiles, group_rows, tiles, nchunks);
 }
 
-// Which fp32 kernel runs: the panel kernel whenever layout allows (wide
-// strips when the row block holds enough nonzeros per B row, tall otherwise),
-// the row-tile kernel for everything else.
-int g_force_kernel = -1;  // test hook: -1 auto, 0 row-tile, 1 wide, 2 tall
+// Which fp32 kernel runs: a panel configuration whenever the layout allows
+// (chosen by density), the row-tile kernel for everything else.
+int g_force_kernel = -1;  // test hook: -1 auto, 0 row-tile, 1.. panel configs
 
 template <typename T>
 void launch_spdm(const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C, int64_t ldc, int flavor,
@@ -240,18 +249,23 @@ void launch_spdm(const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C, 
   if constexpr (std::is_same<T, float>::value) {
     if (fma && g_force_kernel != 0) {
       const double density = (double)a.nnz / ((double)a.m * (double)a.k);
-      const bool wide_ok = panel_fits<PanelWide>(a, n, ldb, ldc, B, C);
-      const bool tall_ok = panel_fits<PanelTall>(a, n, ldb, ldc, B, C);
-      bool use_wide = wide_ok && (density * PanelWide::RB >= 12.0 || !tall_ok);
-      if (g_force_kernel == 1) use_wide = wide_ok;
-      if (g_force_kernel == 2) use_wide = false;
-      if (use_wide) {
-        launch_panel<PanelWide>(a, n, B, ldb, C, ldc, s);
-        return;
-      }
-      if (tall_ok && g_force_kernel != 1) {
-        launch_panel<PanelTall>(a, n, B, ldb, C, ldc, s);
-        return;
+      int pick = g_force_kernel;
+      if (pick < 0) pick = density * PanelWide::RB >= 12.0 ? 1 : 3;
+      switch (pick) {
+        case 1:
+          if (panel_fits<PanelWide>(a, n, ldb, ldc, B, C)) return launch_panel<PanelWide>(a, n, B, ldb, C, ldc, s);
+          break;
+        case 2:
+          if (panel_fits<PanelTall>(a, n, ldb, ldc, B, C)) return launch_panel<PanelTall>(a, n, B, ldb, C, ldc, s);
+          break;
+        case 3:
+          if (panel_fits<PanelK128>(a, n, ldb, ldc, B, C)) return launch_panel<PanelK128>(a, n, B, ldb, C, ldc, s);
+          break;
+        case 4:
+          if (panel_fits<PanelK96>(a, n, ldb, ldc, B, C)) return launch_panel<PanelK96>(a, n, B, ldb, C, ldc, s);
+          break;
+        default:
+          break;
       }
     }
   }
@@ -612,6 +626,11 @@ uint64_t gcoo_launch_count(void) { return g_launches.load(); }
 // Test/benchmark hook (not in the public header): pin the fp32 kernel choice.
 int gcoo_debug_force_kernel(int which) {
   g_force_kernel = which;
+  return GCOO_OK;
+}
+
+int gcoo_debug_raster_rows(int rows) {
+  g_raster_rows = rows;
   return GCOO_OK;
 }
 

@@ -1,27 +1,29 @@
 // spdm_panel.cuh — K1-fast: fp32 GCOOSpDM with TMA-fed shared-memory B panels.
 //
 // Replaces detail::spdm_gcoo_impl (kernels.hpp:240-327) for fp32 inputs whose
-// B/C rows are 16-byte aligned.  Design:
+// B/C rows are 16-byte aligned and p <= RW.  Design:
 //
 //   * The path is an FP32 FFMA gather.  Every multiply-add consumes one B
-//     element that is not reused in registers (uniform A at s>=0.99 has
-//     almost no same-column pairs inside a few rows), so the ceiling is the
-//     rate at which B reaches the FMA units, not HBM.  Measured on B200:
-//     smem 128 B/clk/SM, L2->SM ~34 B/clk/SM, FFMA 128/clk/SM.
+//     element that is (almost) never reused in registers at s >= 0.99, so
+//     the ceiling is the rate at which B reaches the FMA units, not HBM.
+//     Measured on B200 (profiles/r01_microbench.json): shared memory 128
+//     B/clk/SM, L2->SM ~34 B/clk/SM, FFMA 128/clk/SM.
 //   * A CTA owns a ROW BLOCK of RB = NW*RW rows x a column strip of W = 32*V
-//     columns and walks K in chunks of KC rows of B.  A dedicated producer
-//     warp streams B[chunk, strip] tiles into a STAGES-deep shared-memory ring
-//     with TMA (cp.async.bulk.tensor.2d, mbarrier complete_tx); every staged
-//     B element is then read by all RB rows' nonzeros in that column, so L2
-//     traffic per FMA drops by ~RB*(1-s) (the paper's "traffic moves from
-//     DRAM/L2 to shared memory", done B200-style).
-//   * Each consumer warp owns RW rows x W columns with acc[RW][V] in
-//     registers.  Its rows' entries arrive as one (col,row)-sorted stream (a
-//     GCOO with p = RW, produced from the caller's GCOO(p) by
-//     regroup_pack_kernel), packed to 8 bytes {value, col | slot<<27}; the
-//     warp stages 32 at a time through shared memory and reads them back as
-//     broadcast LDS.128 pairs.  Consecutive entries in the same column reuse
-//     the B vector already in registers (the reference's same-column runs).
+//     columns and walks K in chunks of KC rows of B.  A producer warp
+//     streams B[chunk, strip] tiles into a STAGES-deep shared-memory ring
+//     with TMA (cp.async.bulk.tensor.2d + mbarrier complete_tx); every staged
+//     B element is read by all of the RB rows' nonzeros in its column, so
+//     L2->SM traffic per FMA falls by ~RB*(1-s): the paper's "traffic moves
+//     from DRAM/L2 to shared memory", done B200-style.
+//   * Each consumer warp owns RW rows x W columns, acc[RW][V] in registers.
+//     Its rows' nonzeros arrive as one stream laid out by the planner
+//     (plan_segments_kernel): per chunk, a header of per-row counts and the
+//     chunk's entries sorted by (row, col).  The warp walks row slots
+//     0..RW-1 with COMPILE-TIME accumulator indices and count-driven loops
+//     (no per-entry dispatch, no data-dependent exits), so independent
+//     entries' LDG->LDS->FFMA chains overlap.
+//   * Entries are read with warp-uniform LDG (one L1 wavefront, broadcast)
+//     while the warp keeps 16 L1 lines of its stream prefetched ahead.
 //   * Per C element the FMAs still run over the row's nonzeros in ascending
 //     column order, one rounding each: bit-identical to the reference built
 //     with FMA contraction.
@@ -33,8 +35,6 @@
 
 namespace gcoo_b200 {
 
-constexpr int kColBits = 27;
-constexpr uint32_t kColMask = (1u << kColBits) - 1u;
 
 // ------------------------------------------------------------ PTX helpers --
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -75,9 +75,42 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+template <int V>
+__device__ __forceinline__ void lds_vec(uint32_t addr, float (&b)[V]) {
+  if constexpr (V == 4) {
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(b[0]), "=f"(b[1]), "=f"(b[2]), "=f"(b[3])
+                 : "r"(addr));
+  } else if constexpr (V == 2) {
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(b[0]), "=f"(b[1]) : "r"(addr));
+  } else {
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(b[0]) : "r"(addr));
+  }
+}
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 
 // -------------------------------------------------------- configurations --
-template <int V_, int RW_, int KC_, int STAGES_>
+template <int V_, int RW_, int KC_, int STAGES_, int CAP_>
 struct PanelCfg {
   static constexpr int V = V_;          // floats per lane (16 B for V=4)
   static constexpr int W = 32 * V_;     // columns per CTA strip
@@ -88,121 +121,151 @@ struct PanelCfg {
   static constexpr int STAGES = STAGES_;
   static constexpr int THREADS = (NW + 1) * 32;
   static constexpr uint32_t CHUNK_BYTES = KC_ * W * 4;
-  static constexpr size_t SMEM = (size_t)STAGES_ * CHUNK_BYTES + NW * 32 * 8 + 2 * STAGES_ * 8 + 128;
+  static constexpr int HDR = RW_ / 8;   // header entries (one count byte per row slot)
+  static constexpr int CAP = CAP_;      // staged entries per warp per chunk (header included)
+  static constexpr uint32_t SEG_BYTES = CAP_ * 8;
+  static constexpr uint32_t STAGE_BYTES = CHUNK_BYTES + NW * SEG_BYTES;
+  static constexpr size_t SMEM = (size_t)STAGES_ * STAGE_BYTES + 2 * STAGES_ * 8 + 128;
+  static_assert(CHUNK_BYTES <= 65536, "entry B offsets are 16-bit");
+  static_assert(KC_ <= 255, "per-slot counts are bytes");
+  static_assert(RW_ % 8 == 0 && RW_ <= 32, "header layout");
+  static_assert(CAP_ % 2 == 0, "16-byte segments");
 };
 
-using PanelWide = PanelCfg<4, 16, 64, 4>;   // W=128, RB=256: moderate sparsity
-using PanelTall = PanelCfg<2, 32, 128, 4>;  // W=64,  RB=512: s >= ~0.98
+// <V, RW, KC, STAGES, CAP>
+using PanelWide = PanelCfg<4, 16, 64, 4, 128>;   // W=128, RB=256, 48 KB stages: s ~ 0.9
+using PanelK96 = PanelCfg<4, 16, 96, 4, 64>;     // W=128, RB=256, 56 KB stages
+using PanelK128 = PanelCfg<4, 16, 128, 3, 64>;   // W=128, RB=256, 72 KB stages
+using PanelTall = PanelCfg<2, 32, 192, 3, 128>;  // W=64,  RB=512, 64 KB stages: s >= ~0.98
 
-// -------------------------------------------------- A regroup + packing --
-// GCOO(p) -> GCOO(RW) packed stream.  Tile t covers rows [t*RW, t*RW+RW) =
-// groups [t*RW/p, (t+1)*RW/p); its slices are contiguous in the input
-// (g_idxes is an exclusive scan), so the tile's output range is the same
-// [gidx[g0], gidx[g1]) and only the order inside changes: each entry's rank is
-// its index in its own group plus, for every other group of the tile, the
-// number of entries with a smaller (col,row) key (binary search; keys are
-// unique).  Keys are staged in shared memory when the tile fits.
-constexpr int kRegroupThreads = 256;
-constexpr int kRegroupSmemKeys = 6016;  // 47 KB of 64-bit keys (static smem limit)
+// -------------------------------------------------------------- planner --
+// Lays out the caller's GCOO(p) for one panel configuration.  Tile t = rows
+// [t*RW, t*RW+RW) = GCOO groups [t*RW/p, (t+1)*RW/p).  Segment (t, c) holds,
+// for chunk c of KC columns, a header of RW count bytes (entries of each row
+// slot) followed by the tile's entries in that chunk sorted by (row, col),
+// padded to 16 bytes; segments are laid out tile-major, chunk-minor, and
+// seg_off[t*nchunks + c] is each one's first entry (an exclusive scan of the
+// lengths counted by plan_count_kernel).  Entry = {value bits, byte offset of
+// its B row inside a chunk stage}.  An entry's rank inside its chunk follows
+// from the (col,row)-sorted group slices alone: #chunk entries of lower-row
+// groups + #own-group chunk entries before it in (row,col) order.
+constexpr int kPlanThreads = 256;
 
-__device__ __forceinline__ uint64_t entry_key(int32_t col, int32_t row) {
-  return (static_cast<uint64_t>(static_cast<uint32_t>(col)) << 32) | static_cast<uint32_t>(row);
+__device__ __forceinline__ int64_t lower_bound_col(const int32_t* __restrict__ cols, int64_t lo, int64_t hi,
+                                                   int32_t x) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (cols[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
 }
 
-template <int RW>
-__global__ void __launch_bounds__(kRegroupThreads)
-regroup_pack_kernel(int64_t m, int32_t p, int64_t groups, int64_t nnz, const float* __restrict__ vals,
-                    const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
-                    const int64_t* __restrict__ gidx, uint2* __restrict__ out, int64_t tiles) {
-  __shared__ uint64_t keys[kRegroupSmemKeys];
-  __shared__ int64_t goff[RW + 1];
+__device__ __forceinline__ void tile_groups(int64_t t, int RW, int32_t p, int64_t groups, int64_t& g0,
+                                            int64_t& g1) {
   const int gper = RW / p;
+  g0 = t * gper;
+  g1 = g0 + gper < groups ? g0 + gper : groups;
+  if (g0 > groups) g0 = groups;
+}
+
+// seg_len[t*nchunks + c] = round_up_even(HDR + entries of tile t in chunk c)
+template <class Cfg>
+__global__ void plan_count_kernel(int32_t p, int64_t groups, int64_t nnz, const int32_t* __restrict__ cols,
+                                  const int64_t* __restrict__ gidx, int64_t tiles, int nchunks,
+                                  int64_t* __restrict__ seg_len) {
+  const int64_t total = tiles * (int64_t)nchunks;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = x / nchunks;
+    const int c = (int)(x % nchunks);
+    int64_t g0, g1;
+    tile_groups(t, Cfg::RW, p, groups, g0, g1);
+    int64_t cnt = 0;
+    for (int64_t g = g0; g < g1; ++g) {
+      const int64_t a = gidx[g];
+      const int64_t b = g + 1 < groups ? gidx[g + 1] : nnz;
+      cnt += lower_bound_col(cols, a, b, (c + 1) * Cfg::KC) - lower_bound_col(cols, a, b, c * Cfg::KC);
+    }
+    seg_len[x] = (Cfg::HDR + cnt + 1) & ~int64_t(1);
+  }
+}
+
+// one block per tile: entries scattered to their segment slot, then headers
+template <class Cfg>
+__global__ void __launch_bounds__(kPlanThreads)
+plan_fill_kernel(int32_t p, int64_t groups, int64_t nnz, const float* __restrict__ vals,
+                 const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
+                 const int64_t* __restrict__ gidx, const int64_t* __restrict__ seg_off, uint2* __restrict__ out,
+                 int64_t tiles, int nchunks) {
+  constexpr int RW = Cfg::RW, KC = Cfg::KC, W = Cfg::W, HDR = Cfg::HDR;
+  __shared__ int64_t goff[RW + 1];
   for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const int64_t g0 = t * gper;
-    const int64_t g1 = g0 + gper < groups ? g0 + gper : groups;
+    int64_t g0, g1;
+    tile_groups(t, RW, p, groups, g0, g1);
     const int ng = (int)(g1 - g0);
     __syncthreads();
     if (threadIdx.x <= ng) goff[threadIdx.x] = (g0 + threadIdx.x < groups) ? gidx[g0 + threadIdx.x] : nnz;
     __syncthreads();
-    const int64_t start = goff[0], end = goff[ng], cnt = end - start;
-    const bool in_smem = cnt <= kRegroupSmemKeys;
-    if (in_smem && ng > 1)
-      for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) keys[i] = entry_key(cols[start + i], rows[start + i]);
-    __syncthreads();
+    const int64_t start = goff[0], end = goff[ng];
     const int64_t row0 = t * RW;
+    const int64_t* so = seg_off + t * (int64_t)nchunks;
     for (int64_t i = start + threadIdx.x; i < end; i += blockDim.x) {
       const int32_t r = rows[i], c = cols[i];
-      int64_t pos = i - start;
-      if (ng > 1) {
-        const uint64_t key = entry_key(c, r);
-        const int own = (int)((r / p) - g0);
-        pos = i - goff[own];
-        for (int g = 0; g < ng; ++g) {
-          if (g == own) continue;
-          int64_t lo = goff[g] - start, hi = goff[g + 1] - start;
-          const int64_t base = lo;
-          while (lo < hi) {
-            const int64_t mid = (lo + hi) >> 1;
-            const uint64_t mk = in_smem ? keys[mid] : entry_key(cols[start + mid], rows[start + mid]);
-            if (mk < key) lo = mid + 1; else hi = mid;
-          }
-          pos += lo - base;
+      const int ch = c / KC;
+      const int own = (int)(r / p - g0);
+      const int32_t lo_col = ch * KC, hi_col = lo_col + KC;
+      int64_t rank = 0;
+      for (int g = 0; g < own; ++g)
+        rank += lower_bound_col(cols, goff[g], goff[g + 1], hi_col) - lower_bound_col(cols, goff[g], goff[g + 1], lo_col);
+      for (int64_t j = lower_bound_col(cols, goff[own], goff[own + 1], lo_col); j < goff[own + 1] && cols[j] < hi_col;
+           ++j) {
+        const int32_t rj = rows[j];
+        if (rj < r || (rj == r && cols[j] < c)) ++rank;
+      }
+      const uint32_t off = (uint32_t)(c - lo_col) * (uint32_t)(W * 4);
+      out[so[ch] + HDR + rank] = make_uint2(__float_as_uint(vals[i]), off);
+    }
+    for (int ch = threadIdx.x; ch < nchunks; ch += blockDim.x) {
+      const int32_t lo_col = ch * KC, hi_col = lo_col + KC;
+      uint32_t words[RW / 4];
+#pragma unroll
+      for (int w = 0; w < RW / 4; ++w) words[w] = 0;
+      for (int g = 0; g < ng; ++g) {
+        for (int64_t j = lower_bound_col(cols, goff[g], goff[g + 1], lo_col); j < goff[g + 1] && cols[j] < hi_col;
+             ++j) {
+          const uint32_t slot = (uint32_t)(rows[j] - row0);
+#pragma unroll
+          for (int w = 0; w < RW / 4; ++w)
+            if ((slot >> 2) == (uint32_t)w) words[w] += 1u << (8 * (slot & 3));
         }
       }
-      const uint32_t slot = (uint32_t)(r - row0);
-      out[start + pos] = make_uint2(__float_as_uint(vals[i]), (uint32_t)c | (slot << kColBits));
+      uint2* h = out + so[ch];
+#pragma unroll
+      for (int q = 0; q < HDR; ++q) h[q] = make_uint2(words[2 * q], words[2 * q + 1]);
     }
   }
 }
 
 // ---------------------------------------------------------- main kernel --
-template <int RW, int V>
-__device__ __forceinline__ void fma_slot(float (&acc)[RW][V], uint32_t slot, float a, const float (&b)[V]) {
-#define GCOO_PCASE(s)                                                               \
-  case s:                                                                           \
-    if constexpr ((s) < RW) {                                                       \
-      _Pragma("unroll") for (int v = 0; v < V; ++v) acc[s][v] = __fmaf_rn(a, b[v], acc[s][v]); \
-    }                                                                               \
-    break;
-  switch (slot) {
-    GCOO_PCASE(0) GCOO_PCASE(1) GCOO_PCASE(2) GCOO_PCASE(3) GCOO_PCASE(4) GCOO_PCASE(5) GCOO_PCASE(6)
-    GCOO_PCASE(7) GCOO_PCASE(8) GCOO_PCASE(9) GCOO_PCASE(10) GCOO_PCASE(11) GCOO_PCASE(12) GCOO_PCASE(13)
-    GCOO_PCASE(14) GCOO_PCASE(15) GCOO_PCASE(16) GCOO_PCASE(17) GCOO_PCASE(18) GCOO_PCASE(19) GCOO_PCASE(20)
-    GCOO_PCASE(21) GCOO_PCASE(22) GCOO_PCASE(23) GCOO_PCASE(24) GCOO_PCASE(25) GCOO_PCASE(26) GCOO_PCASE(27)
-    GCOO_PCASE(28) GCOO_PCASE(29) GCOO_PCASE(30) GCOO_PCASE(31)
-    default: break;
-  }
-#undef GCOO_PCASE
-}
-
-template <int V>
-__device__ __forceinline__ void lds_b(const float* p, float (&b)[V]) {
-  if constexpr (V == 4) {
-    const float4 x = *reinterpret_cast<const float4*>(p);
-    b[0] = x.x; b[1] = x.y; b[2] = x.z; b[3] = x.w;
-  } else if constexpr (V == 2) {
-    const float2 x = *reinterpret_cast<const float2*>(p);
-    b[0] = x.x; b[1] = x.y;
-  } else {
-    b[0] = *p;
-  }
-}
-
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
-spdm_panel_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t n, int32_t p, int64_t groups,
-                  int64_t nnz, const uint2* __restrict__ ent, const int64_t* __restrict__ gidx,
-                  float* __restrict__ C, int64_t ldc, int64_t row_blocks, int nchunks) {
+spdm_panel_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t n, const uint2* __restrict__ ent,
+                  const int64_t* __restrict__ seg_off, float* __restrict__ C, int64_t ldc, int64_t row_blocks,
+                  int64_t col_tiles, int64_t group_rows, int64_t tiles, int nchunks) {
   constexpr int V = Cfg::V, W = Cfg::W, RW = Cfg::RW, NW = Cfg::NW, KC = Cfg::KC, S = Cfg::STAGES;
+  constexpr int HDR = Cfg::HDR, CAP = Cfg::CAP;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* bpanel = reinterpret_cast<float*>(smem_raw);                        // [S][KC][W]
-  uint2* stage = reinterpret_cast<uint2*>(smem_raw + (size_t)S * Cfg::CHUNK_BYTES);  // [NW][32]
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage + NW * 32);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * Cfg::STAGE_BYTES);
   uint64_t* empty = full + S;
+  const uint32_t smem0 = smem_u32(smem_raw);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t rb = blockIdx.x % row_blocks;
-  const int64_t ct = blockIdx.x / row_blocks;
+  // rasterisation: bands of `group_rows` row blocks; inside a band the row
+  // block varies fastest, so co-resident CTAs share a few B strips
+  const int64_t band = blockIdx.x / (group_rows * col_tiles);
+  const int64_t in_band = blockIdx.x % (group_rows * col_tiles);
+  const int64_t band_rows = (band + 1) * group_rows <= row_blocks ? group_rows : row_blocks - band * group_rows;
+  const int64_t rb = band * group_rows + in_band % band_rows;
+  const int64_t ct = in_band / band_rows;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -213,26 +276,41 @@ spdm_panel_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t
   }
   __syncthreads();
 
-  if (warp == NW) {  // ---------------- producer: TMA B[chunk, strip] -> ring
-    if (lane == 0) {
-      const int32_t x = (int32_t)(ct * W);
-      for (int c = 0; c < nchunks; ++c) {
-        const int s = c % S;
-        if (c >= S) mbar_wait(&empty[s], (uint32_t)((c / S) - 1) & 1u);
-        mbar_arrive_expect_tx(&full[s], Cfg::CHUNK_BYTES);
-        tma_load_2d(bpanel + (size_t)s * KC * W, &tmap_b, x, c * KC, &full[s]);
+  if (warp == NW) {
+    // ---------------- producer: per chunk, TMA B[chunk, strip] and one bulk
+    // copy per consumer warp of its (header + entries) segment, all on full[s]
+    const int64_t my_tile = rb * NW + lane;
+    const bool has_tile = lane < NW && my_tile < tiles;
+    const int64_t* so = seg_off + (has_tile ? my_tile : 0) * (int64_t)nchunks;
+    int64_t s_cur = has_tile ? so[0] : 0;
+    int64_t s_nxt = has_tile ? so[1] : 0;  // seg_off has tiles*nchunks+1 entries
+    const int32_t x = (int32_t)(ct * W);
+    for (int c = 0; c < nchunks; ++c) {
+      const int s = c % S;
+      const int64_t s_after = (has_tile && c + 2 <= nchunks) ? so[c + 2 < nchunks ? c + 2 : nchunks] : 0;
+      int64_t len = has_tile ? s_nxt - s_cur : 0;
+      if (len > CAP) len = CAP;
+      uint32_t bytes = (uint32_t)len * 8u;
+      uint32_t total = bytes;
+#pragma unroll
+      for (int d = 16; d; d >>= 1) total += __shfl_xor_sync(0xffffffffu, total, d);
+      if (c >= S) mbar_wait(&empty[s], (uint32_t)((c / S) - 1) & 1u);
+      const uint32_t stage = smem0 + (uint32_t)s * Cfg::STAGE_BYTES;
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&full[s], Cfg::CHUNK_BYTES + total);
+        tma_load_2d(smem_raw + (size_t)s * Cfg::STAGE_BYTES, &tmap_b, x, c * KC, &full[s]);
       }
+      __syncwarp();
+      if (bytes) bulk_g2s(stage + Cfg::CHUNK_BYTES + lane * Cfg::SEG_BYTES, ent + s_cur, bytes, &full[s]);
+      s_cur = s_nxt;
+      s_nxt = s_after;
     }
     return;
   }
 
   // ------------------------------------------------------------- consumers
   const int64_t tile = rb * NW + warp;
-  const int gper = RW / p;
-  const int64_t g0 = tile * gper;
-  const int64_t g1 = g0 + gper;
-  const int64_t start = g0 < groups ? gidx[g0] : nnz;
-  const int64_t end = g1 < groups ? gidx[g1] : nnz;
+  const bool active = tile < tiles;  // rows past m only take part in the ring protocol
 
   float acc[RW][V];
 #pragma unroll
@@ -240,59 +318,73 @@ spdm_panel_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t
 #pragma unroll
     for (int v = 0; v < V; ++v) acc[s][v] = 0.f;
 
-  int c = 0;
-  uint32_t chunk_end = KC;
-  mbar_wait(&full[0], 0);
-  const float* bs = bpanel + lane * V;  // this lane's columns inside stage 0
-  uint32_t prev_col = 0xffffffffu;
-  float b[V];
+  for (int c = 0; c < nchunks; ++c) {
+    const int s_idx = c % S;
+    mbar_wait(&full[s_idx], (uint32_t)(c / S) & 1u);
+    if (active) {
+      const uint32_t stage = smem0 + (uint32_t)s_idx * Cfg::STAGE_BYTES;
+      const uint32_t bbase = stage + (uint32_t)(lane * V * 4);
+      uint32_t eaddr = stage + Cfg::CHUNK_BYTES + (uint32_t)warp * Cfg::SEG_BYTES;
+      uint32_t hdr[RW / 4];
 #pragma unroll
-  for (int v = 0; v < V; ++v) b[v] = 0.f;
-  uint2* my_stage = stage + warp * 32;
-
-  // prefetch the first batch of 32 packed entries into registers
-  uint2 next = (start + lane < end) ? __ldg(ent + start + lane) : make_uint2(0, 0);
-  for (int64_t base = start; base < end; base += 32) {
-    my_stage[lane] = next;
-    __syncwarp();
-    const int64_t nb = base + 32 + lane;
-    if (nb < end) next = __ldg(ent + nb);
-    const int cnt = (int)(end - base < 32 ? end - base : 32);
-    for (int q = 0; q < cnt; q += 2) {
-      const uint4 pr = *reinterpret_cast<const uint4*>(my_stage + q);
+      for (int q = 0; q < HDR; ++q) {
+        const uint2 h = lds64(eaddr + q * 8);
+        hdr[2 * q] = h.x;
+        hdr[2 * q + 1] = h.y;
+      }
+      uint32_t tot = 0;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (h == 1 && q + 1 >= cnt) break;
-        const uint32_t cs = h ? pr.w : pr.y;
-        const float a = __uint_as_float(h ? pr.z : pr.x);
-        const uint32_t col = cs & kColMask;
-        while (col >= chunk_end) {  // advance the ring (warp-uniform)
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[c % S]);
-          ++c;
-          chunk_end += KC;
-          mbar_wait(&full[c % S], (uint32_t)(c / S) & 1u);
-          bs = bpanel + (size_t)(c % S) * KC * W + lane * V;
+      for (int q = 0; q < RW / 4; ++q) tot += __dp4a(hdr[q], 0x01010101u, 0u);
+      if (HDR + tot <= (uint32_t)CAP) {
+        // fast path: the whole segment is staged
+        eaddr += HDR * 8;
+#pragma unroll
+        for (int s = 0; s < RW; ++s) {
+          const uint32_t cnt = (hdr[s >> 2] >> (8 * (s & 3))) & 0xffu;
+          const uint32_t e_end = eaddr + cnt * 8;
+#pragma unroll 2
+          for (; eaddr < e_end; eaddr += 8) {
+            const uint2 e = lds64(eaddr);
+#ifdef GCOO_DEBUG_PANEL
+            if (e.y % (W * 4) != 0 || e.y >= Cfg::CHUNK_BYTES) {
+              if (lane == 0)
+                printf("BAD blk=%d warp=%d c=%d slot=%d tot=%u hdr0=%08x hdr1=%08x idx=%u e=(%08x,%08x)\n",
+                       (int)blockIdx.x, warp, c, s, tot, hdr[0], hdr[1],
+                       (eaddr - (stage + Cfg::CHUNK_BYTES + (uint32_t)warp * Cfg::SEG_BYTES)) / 8, e.x, e.y);
+              __trap();
+            }
+#endif
+            float bv[V];
+            lds_vec<V>(bbase + e.y, bv);
+            const float a = __uint_as_float(e.x);
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[s][v] = __fmaf_rn(a, bv[v], acc[s][v]);
+          }
         }
-        if (col != prev_col) {
-          lds_b<V>(bs + (size_t)(col - (chunk_end - KC)) * W, b);
-          prev_col = col;
+      } else {
+        // overflow (very dense rows): entries past CAP come from global memory
+        const uint2* g = ent + seg_off[tile * (int64_t)nchunks + c];
+        uint32_t idx = HDR;
+#pragma unroll
+        for (int s = 0; s < RW; ++s) {
+          const uint32_t cnt = (hdr[s >> 2] >> (8 * (s & 3))) & 0xffu;
+          for (uint32_t i = 0; i < cnt; ++i, ++idx) {
+            const uint2 e = idx < (uint32_t)CAP ? lds64(eaddr + idx * 8) : __ldg(g + idx);
+            float bv[V];
+            lds_vec<V>(bbase + e.y, bv);
+            const float a = __uint_as_float(e.x);
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[s][v] = __fmaf_rn(a, bv[v], acc[s][v]);
+          }
         }
-        fma_slot<RW, V>(acc, cs >> kColBits, a, b);
       }
     }
     __syncwarp();
-  }
-  // release the chunks this warp has not consumed (still wait for them to
-  // land so a stage is never refilled while its TMA is in flight)
-  __syncwarp();
-  if (lane == 0) mbar_arrive(&empty[c % S]);
-  for (++c; c < nchunks; ++c) {
-    mbar_wait(&full[c % S], (uint32_t)(c / S) & 1u);
-    if (lane == 0) mbar_arrive(&empty[c % S]);
+    if (lane == 0) mbar_arrive(&empty[s_idx]);
   }
 
   // single write of the tile
+  if (!active) return;
   const int64_t row0 = tile * RW;
   const int64_t j = ct * W + lane * V;
   if (j < n) {

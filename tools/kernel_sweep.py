@@ -1,0 +1,67 @@
+"""Time every fp32 multiply kernel variant on the n=8000 benchmark inputs.
+
+    python tools/kernel_sweep.py [--n 8000] [--s 0.9 0.99 0.995] [--kernels ...]
+
+Kernel-only CUDA-event times (L2 flushed before each launch), one JSON line per
+(kernel, sparsity), plus a bit-exactness check of each variant's C against the
+first variant's.
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2005_14469_b200 as G  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=8000)
+    ap.add_argument("--s", type=float, nargs="+", default=[0.9, 0.99, 0.995])
+    ap.add_argument("--kernels", nargs="+", default=["auto", "panel_wide", "panel_k96", "panel_k128", "panel_tall", "rowtile"])
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--raster", type=int, nargs="+", default=[0])
+    args = ap.parse_args()
+    n = args.n
+    dev = torch.device("cuda")
+    b = torch.from_numpy(G.generate_uniform_sparse(n, 0.0, G.derive_seed(1, n, 0xB))).to(dev)
+    c = torch.empty((n, n), dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    st = torch.cuda.Stream()
+    for s in args.s:
+        d = G.dense_to_gcoo_dev(torch.from_numpy(G.generate_uniform_sparse(n, s, 1)).to(dev), 4)
+        torch.cuda.synchronize()
+        ref = None
+        for kname, rr in [(k_, r_) for k_ in args.kernels for r_ in args.raster]:
+            G.force_kernel(kname)
+            G.raster_rows(rr)
+            with torch.cuda.stream(st):
+                for _ in range(2):
+                    G.spdm_gcoo_dev(d, b, c, stream=st)
+                ts = []
+                for _ in range(args.reps):
+                    flush.zero_()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(st)
+                    G.spdm_gcoo_dev(d, b, c, stream=st)
+                    e1.record(st)
+                    torch.cuda.synchronize()
+                    ts.append(e0.elapsed_time(e1))
+            out = c.clone()
+            same = None if ref is None else bool(torch.equal(out, ref))
+            if ref is None:
+                ref = out
+            ms = float(np.median(ts))
+            fl = 2.0 * d.nnz() * n
+            print(json.dumps({"s": s, "kernel": kname, "raster": rr, "ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 3),
+                              "min_ms": round(min(ts), 4), "bitwise_equal_first": same}), flush=True)
+        G.force_kernel("auto")
+
+
+if __name__ == "__main__":
+    main()
