@@ -98,7 +98,6 @@ def lib():
     _sig(L, "gcoo_generate_powerlaw_coo_f32", _int, [_i64, _dbl, _dbl, _u64, _i64, _vp, _vp, _vp, C.POINTER(_i64)])
     _sig(L, "gcoo_derive_seed", _u64, [_u64, _u64, _u64])
     _sig(L, "gcoo_debug_force_kernel", _int, [_int])
-    _sig(L, "gcoo_debug_raster_rows", _int, [_int])
     _lib = L
     return L
 
@@ -132,17 +131,12 @@ def set_device(device: int) -> None:
     _check(lib().gcoo_set_device(device))
 
 
-KERNELS = {"auto": -1, "rowtile": 0, "panel_wide": 1, "panel_tall": 2, "panel_k128": 3, "panel_k96": 4}
+KERNELS = {"auto": -1, "rowtile": 0, "tile_v4": 5, "tacc_v4": 8, "tacc_v2": 9}
 
 
 def force_kernel(which: str = "auto") -> None:
     """Test/benchmark hook: pin the fp32 multiply kernel (auto = heuristic)."""
     lib().gcoo_debug_force_kernel(KERNELS[which])
-
-
-def raster_rows(rows: int = 0) -> None:
-    """Tuning hook: row blocks per rasterisation band of the panel kernel (0 = all)."""
-    lib().gcoo_debug_raster_rows(rows)
 
 
 def launch_count() -> int:

@@ -3,7 +3,7 @@
 // Host-side orchestration only: argument validation in the reference's order
 // (so the same inputs raise the same exception class), device buffers from the
 // stream-ordered pool, copies, and kernel launches.  All arithmetic on matrix
-// data happens in the CUDA kernels (spdm_rowtile.cuh, spdm_panel.cuh,
+// data happens in the CUDA kernels (spdm_rowtile.cuh, spdm_tile.cuh, spdm_tacc.cuh,
 // construct.cuh); there is no host compute path.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -17,8 +17,9 @@
 
 #include "common.cuh"
 #include "construct.cuh"
-#include "spdm_panel.cuh"
 #include "spdm_rowtile.cuh"
+#include "spdm_tile.cuh"
+#include "spdm_tacc.cuh"
 
 namespace gcoo_b200 {
 
@@ -163,7 +164,7 @@ void launch_rowtile_p(const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T
   }
 }
 
-// ------------------------------------------------------- panel path -----
+// --------------------------------------------------- TMA tensor maps -----
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -193,53 +194,99 @@ CUtensorMap make_b_map(const float* B, int64_t k, int64_t n, int64_t ldb, int bo
   return map;
 }
 
+// ------------------------------------------------------- tile path ------
 template <class Cfg>
-bool panel_fits(const DevGcoo<float>& a, int64_t n, int64_t ldb, int64_t ldc, const float* B, const float* C) {
-  return a.p <= Cfg::RW && ldb % 4 == 0 && ldc % Cfg::V == 0 && n % Cfg::V == 0 &&
-         (reinterpret_cast<uintptr_t>(B) % 16) == 0 && (reinterpret_cast<uintptr_t>(C) % (4 * Cfg::V)) == 0 &&
-         a.k <= (int64_t)INT32_MAX - Cfg::KC && n <= INT32_MAX;
+bool tile_fits(const DevGcoo<float>& a, int64_t n, int64_t ldb, int64_t ldc, const float* B, const float* C) {
+  return ldb % 4 == 0 && ldc % Cfg::V == 0 && n % Cfg::V == 0 && (reinterpret_cast<uintptr_t>(B) % 16) == 0 &&
+         (reinterpret_cast<uintptr_t>(C) % (4 * Cfg::V)) == 0 && a.k <= (int64_t)INT32_MAX - Cfg::KC &&
+         n <= INT32_MAX && a.m <= (int64_t)INT32_MAX;
 }
 
-int g_raster_rows = 0;  // tuning hook: row blocks per rasterisation band (0 = all)
-
+// Planner (device, no host synchronisation) + the multiply, all on stream s.
 template <class Cfg>
-void launch_panel(const DevGcoo<float>& a, int64_t n, const float* B, int64_t ldb, float* C, int64_t ldc,
-                  cudaStream_t s) {
+void launch_tile(const DevGcoo<float>& a, int64_t n, const float* B, int64_t ldb, float* C, int64_t ldc,
+                 cudaStream_t s) {
   static bool attr_set[64] = {};
   int d = 0;
   GCOO_CUDA(cudaGetDevice(&d));
   if (!attr_set[d]) {
-    GCOO_CUDA(cudaFuncSetAttribute(spdm_panel_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    GCOO_CUDA(cudaFuncSetAttribute(spdm_tile_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)Cfg::SMEM));
     attr_set[d] = true;
   }
-  const int64_t tiles = ceil_div(a.m, Cfg::RW);
-  const int nchunks = (int)ceil_div(a.k, Cfg::KC);
-  const int64_t nseg = tiles * (int64_t)nchunks;
-  // planner: segment lengths -> offsets -> entries + headers
-  DevBuf<int64_t> seg_len(nseg, s), seg_off(nseg + 1, s);
-  GCOO_LAUNCH(plan_count_kernel<Cfg>, grid_for(nseg, 256), 256, 0, s, a.p, a.groups, a.nnz, a.cols, a.gidx, tiles,
-              nchunks, seg_len.get());
-  exclusive_scan(seg_len.get(), seg_off.get(), nseg, s);
-  int64_t stream_len = 0;
-  d2h(&stream_len, seg_off.get() + nseg, 1, s);
-  GCOO_CUDA(cudaStreamSynchronize(s));
-  DevBuf<uint2> ent(stream_len + Cfg::CAP, s);
-  GCOO_LAUNCH(plan_fill_kernel<Cfg>, (unsigned)std::min<int64_t>(tiles, (int64_t)sm_count() * 8), kPlanThreads, 0,
-              s, a.p, a.groups, a.nnz, a.vals, a.rows, a.cols, a.gidx, seg_off.get(), ent.get(), tiles, nchunks);
-  const CUtensorMap map = make_b_map(B, a.k, n, ldb, Cfg::W, Cfg::KC);
+  const int64_t units = ceil_div(a.m, Cfg::RW);
   const int64_t row_blocks = ceil_div(a.m, Cfg::RB);
+  const int nchunks = (int)ceil_div(a.k, Cfg::KC);
+  const int64_t nseg = row_blocks * nchunks;
+  DevBuf<uint32_t> cnt(units * nchunks * Cfg::RW, s);
+  GCOO_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
+  if (a.nnz > 0)
+    GCOO_LAUNCH(tile_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks, cnt.get());
+  DevBuf<int64_t> seg_len(nseg, s), seg_off(nseg + 1, s);
+  GCOO_LAUNCH(tile_size_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
+              seg_len.get());
+  exclusive_scan(seg_len.get(), seg_off.get(), nseg, s);
+  // upper bound of the stream (see tile_warp_size): headers + 16*G bytes per entry
+  const int64_t bound = nseg * (Cfg::TABLE + Cfg::NW * Cfg::HDR) + (int64_t)Cfg::REC * a.nnz + 16;
+  DevBuf<unsigned char> ent(bound, s);
+  DevBuf<int64_t> slot_pos(nseg * Cfg::NW * Cfg::RW, s);
+  GCOO_LAUNCH(tile_header_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
+              seg_off.get(), ent.get(), slot_pos.get());
+  if (a.nnz > 0)
+    GCOO_LAUNCH(tile_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols, a.gidx,
+                nchunks, slot_pos.get(), ent.get());
+  const CUtensorMap map = make_b_map(B, a.k, n, ldb, Cfg::W, Cfg::KC);
   const int64_t col_tiles = ceil_div(n, Cfg::W);
   const int64_t grid = row_blocks * col_tiles;
   if (grid > INT32_MAX) fail(GCOO_EINVAL, "spdm_gcoo: problem too large for one launch");
-  const int64_t group_rows = g_raster_rows > 0 ? std::min<int64_t>(g_raster_rows, row_blocks) : row_blocks;
-  GCOO_LAUNCH(spdm_panel_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n, ent.get(),
-              seg_off.get(), C, ldc, row_blocks, col_tiles, group_rows, tiles, nchunks);
+  GCOO_LAUNCH(spdm_tile_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n, ent.get(),
+              seg_off.get(), C, ldc, row_blocks, nchunks);
 }
 
-// Which fp32 kernel runs: a panel configuration whenever the layout allows
+// TMEM-accumulator variant (spdm_tacc.cuh); same planner protocol.
+template <class Cfg>
+void launch_tacc(const DevGcoo<float>& a, int64_t n, const float* B, int64_t ldb, float* C, int64_t ldc,
+                 cudaStream_t s) {
+  static bool attr_set[64] = {};
+  int d = 0;
+  GCOO_CUDA(cudaGetDevice(&d));
+  if (!attr_set[d]) {
+    GCOO_CUDA(cudaFuncSetAttribute(spdm_tacc_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)Cfg::SMEM));
+    attr_set[d] = true;
+  }
+  const int64_t units = ceil_div(a.m, Cfg::RW);
+  const int64_t row_blocks = ceil_div(a.m, Cfg::RB);
+  const int nchunks = (int)ceil_div(a.k, Cfg::KC);
+  const int64_t nseg = row_blocks * nchunks;
+  DevBuf<uint32_t> cnt(units * nchunks * Cfg::RW, s);
+  GCOO_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
+  if (a.nnz > 0)
+    GCOO_LAUNCH(tacc_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks, cnt.get());
+  DevBuf<int64_t> seg_len(nseg, s), seg_off(nseg + 1, s);
+  GCOO_LAUNCH(tacc_size_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
+              seg_len.get());
+  exclusive_scan(seg_len.get(), seg_off.get(), nseg, s);
+  // upper bound of the stream (see tile_warp_size): headers + 16*G bytes per entry
+  const int64_t bound = nseg * (Cfg::TABLE + Cfg::NW * Cfg::HDR) + (int64_t)Cfg::REC * a.nnz + 16;
+  DevBuf<unsigned char> ent(bound, s);
+  DevBuf<int64_t> slot_pos(nseg * Cfg::NW * Cfg::RW, s);
+  GCOO_LAUNCH(tacc_header_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
+              seg_off.get(), ent.get(), slot_pos.get());
+  if (a.nnz > 0)
+    GCOO_LAUNCH(tacc_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols, a.gidx,
+                nchunks, slot_pos.get(), ent.get());
+  const CUtensorMap map = make_b_map(B, a.k, n, ldb, Cfg::W, Cfg::KC);
+  const int64_t col_tiles = ceil_div(n, Cfg::W);
+  const int64_t grid = row_blocks * col_tiles;
+  if (grid > INT32_MAX) fail(GCOO_EINVAL, "spdm_gcoo: problem too large for one launch");
+  GCOO_LAUNCH(spdm_tacc_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n, ent.get(),
+              seg_off.get(), C, ldc, row_blocks, nchunks);
+}
+
+// Which fp32 kernel runs: a tiled configuration whenever the layout allows
 // (chosen by density), the row-tile kernel for everything else.
-int g_force_kernel = -1;  // test hook: -1 auto, 0 row-tile, 1.. panel configs
+int g_force_kernel = -1;  // test hook: -1 auto, 0 row-tile, 5 tile_v4, 8 tacc_v4, 9 tacc_v2
 
 template <typename T>
 void launch_spdm(const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C, int64_t ldc, int flavor,
@@ -250,19 +297,16 @@ void launch_spdm(const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C, 
     if (fma && g_force_kernel != 0) {
       const double density = (double)a.nnz / ((double)a.m * (double)a.k);
       int pick = g_force_kernel;
-      if (pick < 0) pick = density * PanelWide::RB >= 12.0 ? 1 : 3;
+      if (pick < 0) pick = density >= 0.03 ? 5 : 8;
       switch (pick) {
-        case 1:
-          if (panel_fits<PanelWide>(a, n, ldb, ldc, B, C)) return launch_panel<PanelWide>(a, n, B, ldb, C, ldc, s);
+        case 5:
+          if (tile_fits<TileV4>(a, n, ldb, ldc, B, C)) return launch_tile<TileV4>(a, n, B, ldb, C, ldc, s);
           break;
-        case 2:
-          if (panel_fits<PanelTall>(a, n, ldb, ldc, B, C)) return launch_panel<PanelTall>(a, n, B, ldb, C, ldc, s);
+        case 8:
+          if (tile_fits<TaccV4>(a, n, ldb, ldc, B, C)) return launch_tacc<TaccV4>(a, n, B, ldb, C, ldc, s);
           break;
-        case 3:
-          if (panel_fits<PanelK128>(a, n, ldb, ldc, B, C)) return launch_panel<PanelK128>(a, n, B, ldb, C, ldc, s);
-          break;
-        case 4:
-          if (panel_fits<PanelK96>(a, n, ldb, ldc, B, C)) return launch_panel<PanelK96>(a, n, B, ldb, C, ldc, s);
+        case 9:
+          if (tile_fits<TaccV2>(a, n, ldb, ldc, B, C)) return launch_tacc<TaccV2>(a, n, B, ldb, C, ldc, s);
           break;
         default:
           break;
@@ -629,10 +673,6 @@ int gcoo_debug_force_kernel(int which) {
   return GCOO_OK;
 }
 
-int gcoo_debug_raster_rows(int rows) {
-  g_raster_rows = rows;
-  return GCOO_OK;
-}
 
 int gcoo_stream_sync(void* stream) {
   return guarded([&] { GCOO_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream))); });

@@ -2,7 +2,7 @@
 //
 // Replaces detail::spdm_gcoo_impl (kernels.hpp:240-327).  This is the
 // always-applicable path (fp64, n not a multiple of 4, unaligned B/C, any p);
-// the tuned fp32 path is spdm_panel.cuh.
+// the tuned fp32 paths are spdm_tacc.cuh and spdm_tile.cuh.
 //
 // Work decomposition (B200-first, not the reference's OpenMP tile loop):
 //   * one warp owns a ROW TILE of PMAX consecutive rows x 32*V columns

@@ -1,0 +1,369 @@
+// spdm_tacc.cuh — K1-fast: fp32 GCOOSpDM with the accumulators in TENSOR
+// MEMORY, a TMA-fed shared-memory B ring and a flat slot-major record stream.
+//
+// Replaces detail::spdm_gcoo_impl (kernels.hpp:240-327) for fp32 inputs whose
+// B/C rows are 16-byte aligned.  Design (ceilings measured in
+// profiles/r01_microbench*.json):
+//
+//   * The path is bound by how fast B reaches the FMA units: each
+//     multiply-add needs one B element, almost never reused from registers at
+//     s >= 0.99.  Shared memory delivers 128 B/clk/SM (32 FMA/clk); an entry
+//     is broadcast to the warp with one wavefront and its B row segment is one
+//     vector LDS per lane.
+//   * A CTA stages B[chunk of KC rows, strip of W = 32*V columns] once per
+//     chunk and all its RB rows' nonzeros in the chunk read it, so the L2->SM
+//     bytes per FMA are 4 / (RB * density): RB must be large.  Register-held
+//     accumulators cap RB*W at ~30K; here they live in TMEM (128 lanes x 512
+//     columns = 64K fp32 per SM), so RB doubles: 16 consumer warps, warp w
+//     owns TMEM lane quadrant w%4 and 128 columns = RW = 128/V rows x V
+//     columns per lane.  V=4: W=128, RB=512; V=2: W=64, RB=1024; V=1: W=32,
+//     RB=2048.
+//   * A warp walks its chunk's records in one flat loop: a record carries up
+//     to two entries of one row slot {v0, v1, off0 | slot << 24, off1}.  The
+//     slot's V accumulators are pulled into registers from TMEM
+//     (tcgen05.ld.32x32b) when the slot changes and pushed back
+//     (tcgen05.st) when it is left: one ld/st pair per visited (slot, chunk),
+//     no per-slot control flow for empty slots and no register-indexed
+//     accumulator arrays.
+//   * Producer warp: per chunk one 2-D TMA of the B tile and one 1-D bulk copy
+//     of the CTA's record segment into a STAGES-deep ring (mbarrier
+//     complete_tx); consumers release a stage with one arrive per warp.
+//
+// Per C element the FMAs run over the row's nonzeros in ascending column
+// order (chunks in order, a (row, chunk)'s entries in column order), one
+// rounding each: bit-identical to the reference built with FMA contraction.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace gcoo_b200 {
+
+template <int V_, int KC_, int STAGES_, int CAP_>
+struct TaccCfg {
+  static constexpr int V = V_;             // floats per lane
+  static constexpr int W = 32 * V_;        // columns per CTA strip
+  static constexpr int NW = 16;            // consumer warps: 4 per TMEM lane quadrant
+  static constexpr int TCOLS = 512 / (NW / 4);  // TMEM columns per warp (128)
+  static constexpr int RW = TCOLS / V_;    // rows (slots) per warp
+  static constexpr int RB = NW * RW;       // rows per CTA
+  static constexpr int KC = KC_;           // B rows per chunk
+  static constexpr int STAGES = STAGES_;
+  static constexpr int THREADS = (NW + 1) * 32;
+  static constexpr uint32_t BTILE = (uint32_t)KC_ * W * 4;
+  static constexpr uint32_t CAP = CAP_;    // record-segment bytes per stage
+  static constexpr uint32_t STAGE_BYTES = BTILE + CAP_;
+  static constexpr int HDR = 16;           // per-warp header: record count
+  static constexpr int REC = 16;           // bytes per record
+  static constexpr int TABLE = 64;         // per-segment warp offset table (16 x u32)
+  static constexpr size_t SMEM = (size_t)STAGES_ * STAGE_BYTES + 2 * STAGES_ * 8 + 16;
+  static_assert(KC_ <= 256, "TMA box rows");
+  static_assert(BTILE < (1u << 24) && RW <= 256, "24-bit B offsets, 8-bit slots");
+  static_assert(CAP_ % 16 == 0 && BTILE % 16 == 0, "16-byte stages");
+  static_assert(SMEM <= 227 * 1024 && SMEM > 116 * 1024, "one CTA per SM (it owns all 512 TMEM columns)");
+};
+
+//                      V  KC   S  CAP
+using TaccV4 = TaccCfg<4, 192, 2, 16384>;   // W=128, RB=512 : density >~ 2%
+using TaccV2 = TaccCfg<2, 256, 2, 16384>;   // W=64,  RB=1024: density ~ 1%
+
+// ---------------------------------------------------------------- planner --
+// P1: per (unit u = row / RW, chunk, slot = row % RW) entry counts.
+template <class Cfg>
+__global__ void tacc_count_kernel(int64_t nnz, const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
+                                  int nchunks, uint32_t* __restrict__ cnt) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = rows[e];
+    const int32_t c = cols[e] / Cfg::KC;
+    atomicAdd(&cnt[((int64_t)(r / Cfg::RW) * nchunks + c) * Cfg::RW + (r % Cfg::RW)], 1u);
+  }
+}
+
+template <class Cfg>
+__device__ __forceinline__ uint32_t tacc_warp_records(const uint32_t* __restrict__ cnt, int64_t units, int nchunks,
+                                                      int64_t u, int c) {
+  if (u >= units) return 0u;
+  const uint32_t* p = cnt + (u * nchunks + c) * Cfg::RW;
+  uint32_t r = 0;
+#pragma unroll 8
+  for (int s = 0; s < Cfg::RW; ++s) r += (p[s] + 1) >> 1;
+  return r;
+}
+
+// P2: one warp per (rb, c): segment length (table + warp segments).
+template <class Cfg>
+__global__ void tacc_size_kernel(const uint32_t* __restrict__ cnt, int64_t units, int nchunks, int64_t nseg,
+                                 int64_t* __restrict__ seg_len) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t x = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < nseg;
+       x += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t rb = x / nchunks;
+    const int c = (int)(x % nchunks);
+    uint32_t sz = lane < Cfg::NW
+                      ? Cfg::HDR + Cfg::REC * tacc_warp_records<Cfg>(cnt, units, nchunks, rb * Cfg::NW + lane, c)
+                      : 0u;
+#pragma unroll
+    for (int d = 16; d; d >>= 1) sz += __shfl_xor_sync(0xffffffffu, sz, d);
+    if (lane == 0) seg_len[x] = Cfg::TABLE + sz;
+  }
+}
+
+// P4: one warp per (rb, c): warp offset table, per-warp record counts, the
+// "absent second entry" marks, and the stream position of every (warp, slot)
+// record run for the scatter.
+template <class Cfg>
+__global__ void tacc_header_kernel(const uint32_t* __restrict__ cnt, int64_t units, int nchunks, int64_t nseg,
+                                   const int64_t* __restrict__ seg_off, unsigned char* __restrict__ ent,
+                                   int64_t* __restrict__ slot_pos) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t x = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < nseg;
+       x += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t rb = x / nchunks;
+    const int c = (int)(x % nchunks);
+    const int64_t u = rb * Cfg::NW + lane;
+    const uint32_t nrec = lane < Cfg::NW ? tacc_warp_records<Cfg>(cnt, units, nchunks, u, c) : 0u;
+    const uint32_t sz = lane < Cfg::NW ? Cfg::HDR + Cfg::REC * nrec : 0u;
+    uint32_t incl = sz;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    if (lane < Cfg::NW) {
+      const uint32_t woff = Cfg::TABLE + incl - sz;
+      unsigned char* seg = ent + seg_off[x];
+      reinterpret_cast<uint32_t*>(seg)[lane] = woff;
+      *reinterpret_cast<uint4*>(seg + woff) = make_uint4(nrec, 0u, 0u, 0u);
+      int64_t pos = seg_off[x] + woff + Cfg::HDR;
+      int64_t* sp = slot_pos + (x * Cfg::NW + lane) * Cfg::RW;
+      const uint32_t* p = cnt + (u * nchunks + c) * Cfg::RW;
+      for (int s = 0; s < Cfg::RW; ++s) {
+        const uint32_t ns = u < units ? (p[s] + 1) >> 1 : 0u;
+        sp[s] = pos;
+        uint32_t* rec = reinterpret_cast<uint32_t*>(ent + pos);
+        for (uint32_t j = 0; j < ns; ++j) rec[4 * j + 3] = ~0u;  // overwritten when the entry exists
+        pos += (int64_t)Cfg::REC * ns;
+      }
+    }
+  }
+}
+
+// P5: scatter every entry into its record.  Its rank among its row's entries
+// in the same chunk comes from the (col,row)-sorted group slice: the entries
+// of the chunk are contiguous there, so count same-row ones before it.
+template <class Cfg>
+__global__ void tacc_fill_kernel(int64_t nnz, int32_t p, const float* __restrict__ vals,
+                                 const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
+                                 const int64_t* __restrict__ gidx, int nchunks,
+                                 const int64_t* __restrict__ slot_pos, unsigned char* __restrict__ ent) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = rows[e], col = cols[e];
+    const int c = col / Cfg::KC;
+    const int32_t lo_col = c * Cfg::KC;
+    const int64_t glo = gidx[r / p];
+    uint32_t rank = 0;
+    for (int64_t j = e - 1; j >= glo; --j) {
+      if (cols[j] < lo_col) break;
+      rank += rows[j] == r;
+    }
+    const int64_t u = r / Cfg::RW;
+    const int64_t rb = u / Cfg::NW;
+    const int w = (int)(u % Cfg::NW);
+    const uint32_t slot = (uint32_t)(r % Cfg::RW);
+    const int64_t base = slot_pos[((rb * nchunks + c) * Cfg::NW + w) * Cfg::RW + slot];
+    uint32_t* word = reinterpret_cast<uint32_t*>(ent + base + (int64_t)Cfg::REC * (rank >> 1));
+    const uint32_t off = (uint32_t)(col - lo_col) * (uint32_t)(Cfg::W * 4);
+    word[rank & 1] = __float_as_uint(vals[e]);
+    word[2 + (rank & 1)] = (rank & 1) ? off : (off | (slot << 24));
+  }
+}
+
+// ---------------------------------------------------------- main kernel --
+template <bool GLOBAL>
+struct RecSrc;
+template <>
+struct RecSrc<false> {  // staged in shared memory
+  using addr_t = uint32_t;
+  static __device__ __forceinline__ uint4 ld(addr_t a) { return lds128u(a); }
+  static __device__ __forceinline__ uint32_t ld32(addr_t a) { return lds32u(a); }
+};
+template <>
+struct RecSrc<true> {  // segment larger than a stage: read from global memory
+  using addr_t = const unsigned char*;
+  static __device__ __forceinline__ uint4 ld(addr_t a) { return __ldg(reinterpret_cast<const uint4*>(a)); }
+  static __device__ __forceinline__ uint32_t ld32(addr_t a) { return __ldg(reinterpret_cast<const uint32_t*>(a)); }
+};
+
+template <class Cfg>
+__device__ __forceinline__ void tacc_switch(float (&acc)[Cfg::V], uint32_t& cur, uint32_t tacc, uint32_t s) {
+  if (s != cur) {  // warp-uniform: swap the slot's accumulators through TMEM
+    if (cur != ~0u) tmem_st<Cfg::V>(tacc + cur * Cfg::V, acc);
+    tmem_ld<Cfg::V>(tacc + s * Cfg::V, acc);
+    tmem_wait_ld();
+    cur = s;
+  }
+}
+
+template <int V>
+__device__ __forceinline__ void tacc_fma(float (&acc)[V], float a, const float (&b)[V]) {
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = __fmaf_rn(a, b[v], acc[v]);
+}
+
+// One warp walks its records for one chunk, two records per step (both
+// records and their B rows are in flight before the first FMA).  `cur` (the
+// slot whose accumulators are in registers) persists across chunks.
+template <class Cfg, bool GLOBAL>
+__device__ __forceinline__ void tacc_consume(float (&acc)[Cfg::V], uint32_t& cur, uint32_t tacc,
+                                             typename RecSrc<GLOBAL>::addr_t seg, int warp, uint32_t bbase) {
+  using Src = RecSrc<GLOBAL>;
+  constexpr int V = Cfg::V;
+  const uint32_t woff = Src::ld32(seg + 4 * warp);
+  const auto wseg = seg + woff;
+  const uint32_t nrec = Src::ld32(wseg);
+  auto rec = wseg + Cfg::HDR;
+  for (uint32_t r = 0; r < nrec; r += 2, rec += 2 * Cfg::REC) {
+    const bool hasB = r + 1 < nrec;
+    const uint4 qa = Src::ld(rec);
+    uint4 qb = make_uint4(0u, 0u, 0u, ~0u);
+    if (hasB) qb = Src::ld(rec + Cfg::REC);
+    float ba0[V], ba1[V], bb0[V], bb1[V];
+    lds_vec<V>(bbase + (qa.z & 0xffffffu), ba0);
+    const bool a2 = qa.w != ~0u;
+    if (a2) lds_vec<V>(bbase + qa.w, ba1);
+    if (hasB) lds_vec<V>(bbase + (qb.z & 0xffffffu), bb0);
+    const bool b2 = qb.w != ~0u;
+    if (b2) lds_vec<V>(bbase + qb.w, bb1);
+    tacc_switch<Cfg>(acc, cur, tacc, qa.z >> 24);
+    tacc_fma<V>(acc, __uint_as_float(qa.x), ba0);
+    if (a2) tacc_fma<V>(acc, __uint_as_float(qa.y), ba1);
+    if (hasB) {
+      tacc_switch<Cfg>(acc, cur, tacc, qb.z >> 24);
+      tacc_fma<V>(acc, __uint_as_float(qb.x), bb0);
+      if (b2) tacc_fma<V>(acc, __uint_as_float(qb.y), bb1);
+    }
+  }
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, 1)
+spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t n, const unsigned char* __restrict__ ent,
+                 const int64_t* __restrict__ seg_off, float* __restrict__ C, int64_t ldc, int64_t row_blocks,
+                 int nchunks) {
+  constexpr int W = Cfg::W, NW = Cfg::NW, S = Cfg::STAGES, V = Cfg::V, RW = Cfg::RW;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + S);
+  const uint32_t smem0 = smem_u32(smem_raw);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t rb = blockIdx.x % row_blocks;  // row blocks fastest: co-resident CTAs share a B strip
+  const int64_t ct = blockIdx.x / row_blocks;
+  const int64_t* so = seg_off + rb * nchunks;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == NW) {
+    // ------------- producer: B tile (TMA 2-D) + record segment (bulk 1-D)
+    if (lane == 0) {
+      const int32_t x = (int32_t)(ct * W);
+      int64_t lo = so[0], hi = so[1];
+      for (int c = 0; c < nchunks; ++c) {
+        const int s = c % S;
+        const int64_t hi_next = so[c + 2 <= nchunks ? c + 2 : nchunks];  // prefetch
+        const uint32_t len = (uint32_t)(hi - lo);
+        const uint32_t bytes = len <= Cfg::CAP ? len : 0u;  // oversize: consumers read global memory
+        if (c >= S) mbar_wait(&empty[s], (uint32_t)((c / S) - 1) & 1u);
+        unsigned char* stage = smem_raw + (size_t)s * Cfg::STAGE_BYTES;
+        mbar_arrive_expect_tx(&full[s], Cfg::BTILE + bytes);
+        tma_load_2d(stage, &tmap_b, x, c * Cfg::KC, &full[s]);
+        if (bytes) bulk_g2s(smem_u32(stage + Cfg::BTILE), ent + lo, bytes, &full[s]);
+        lo = hi;
+        hi = hi_next;
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  // my accumulators: TMEM lanes 32*(warp%4).., columns (warp/4)*TCOLS + slot*V + v
+  const uint32_t tacc = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * Cfg::TCOLS);
+#pragma unroll
+  for (int c0 = 0; c0 < Cfg::TCOLS; c0 += 16) tmem_st16_zero(tacc + c0);
+  tmem_wait_st();
+
+  float acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = 0.f;
+  uint32_t cur = ~0u;
+
+  int64_t lo = so[0], hi = so[1];
+  for (int c = 0; c < nchunks; ++c) {
+    const int s_idx = c % S;
+    const int64_t hi_next = so[c + 2 <= nchunks ? c + 2 : nchunks];  // prefetch
+    mbar_wait(&full[s_idx], (uint32_t)(c / S) & 1u);
+    tmem_wait_st();  // slots pushed during earlier chunks are complete before they are pulled again
+    const uint32_t stage = smem0 + (uint32_t)s_idx * Cfg::STAGE_BYTES;
+    const uint32_t bbase = stage + (uint32_t)(lane * V * 4);
+    if (hi - lo <= (int64_t)Cfg::CAP) {
+      tacc_consume<Cfg, false>(acc, cur, tacc, stage + Cfg::BTILE, warp, bbase);
+    } else {
+      tacc_consume<Cfg, true>(acc, cur, tacc, ent + lo, warp, bbase);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s_idx]);
+    lo = hi;
+    hi = hi_next;
+  }
+  if (cur != ~0u) tmem_st<V>(tacc + cur * V, acc);
+  tmem_wait_st();
+
+  // read back and single write of the tile: slot s, value v at column s*V + v
+  const int64_t row0 = (rb * NW + warp) * (int64_t)RW;
+  const int64_t j = ct * W + lane * V;
+#pragma unroll 1
+  for (int c0 = 0; c0 < Cfg::TCOLS; c0 += 16) {
+    float r[16];
+    tmem_ld16(tacc + c0, r);
+    tmem_wait_ld();
+    if (j < n) {
+#pragma unroll
+      for (int k = 0; k < 16 / V; ++k) {
+        const int64_t row = row0 + c0 / V + k;
+        if (row < m) {
+          float* dst = C + row * ldc + j;
+          if constexpr (V == 4) {
+            *reinterpret_cast<float4*>(dst) = make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+          } else if constexpr (V == 2) {
+            *reinterpret_cast<float2*>(dst) = make_float2(r[2 * k], r[2 * k + 1]);
+          } else {
+            *dst = r[k];
+          }
+        }
+      }
+    }
+  }
+
+  // free TMEM once every consumer warp is done with it
+  tmem_fence_before();
+  named_bar_sync(1, NW * 32);
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc(tbase, 512);
+}
+
+}  // namespace gcoo_b200

@@ -22,9 +22,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=8000)
     ap.add_argument("--s", type=float, nargs="+", default=[0.9, 0.99, 0.995])
-    ap.add_argument("--kernels", nargs="+", default=["auto", "panel_wide", "panel_k96", "panel_k128", "panel_tall", "rowtile"])
+    ap.add_argument("--kernels", nargs="+", default=["auto", "tile_v4", "tacc_v4", "tacc_v2", "rowtile"])
     ap.add_argument("--reps", type=int, default=5)
-    ap.add_argument("--raster", type=int, nargs="+", default=[0])
     args = ap.parse_args()
     n = args.n
     dev = torch.device("cuda")
@@ -37,9 +36,8 @@ def main():
         d = G.dense_to_gcoo_dev(torch.from_numpy(G.generate_uniform_sparse(n, s, 1)).to(dev), 4)
         torch.cuda.synchronize()
         ref = None
-        for kname, rr in [(k_, r_) for k_ in args.kernels for r_ in args.raster]:
+        for kname in args.kernels:
             G.force_kernel(kname)
-            G.raster_rows(rr)
             with torch.cuda.stream(st):
                 for _ in range(2):
                     G.spdm_gcoo_dev(d, b, c, stream=st)
@@ -58,8 +56,8 @@ def main():
                 ref = out
             ms = float(np.median(ts))
             fl = 2.0 * d.nnz() * n
-            print(json.dumps({"s": s, "kernel": kname, "raster": rr, "ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 3),
-                              "min_ms": round(min(ts), 4), "bitwise_equal_first": same}), flush=True)
+            print(json.dumps({"s": s, "kernel": kname, "ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 3),
+                              "min_ms": round(min(ts), 4), "bitwise_equal_first": same, "all_ms": [round(t, 3) for t in ts]}), flush=True)
         G.force_kernel("auto")
 
 

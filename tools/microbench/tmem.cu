@@ -158,6 +158,54 @@ __global__ void __launch_bounds__(512, 1) k_tmem(float* out, int iters, int acti
 #pragma unroll
         for (int u = 0; u < 8; ++u) st_x4(qa + ((c0 + u * 4) & 511), r);
         wait_st();
+      } else if constexpr (MODE == 7 || MODE == 8 || MODE == 9) {
+        // entries distributed by SHFL from a coalesced LDS.64 (one per 32 entries);
+        // B from LDS.128 (7), TMEM x4 (8) or alternating (9); 4 FFMA per entry
+        const uint2 ent = reinterpret_cast<const uint2*>(sm4)[((i & 63) * 32 + lane) & 8191];
+#pragma unroll
+        for (int k = 0; k < 32; k += 2) {
+          const float a0 = __shfl_sync(0xffffffffu, __uint_as_float(ent.x), k);
+          const uint32_t o0 = __shfl_sync(0xffffffffu, ent.y & 0x3ff0u, k);
+          const float a1 = __shfl_sync(0xffffffffu, __uint_as_float(ent.x), k + 1);
+          const uint32_t o1 = __shfl_sync(0xffffffffu, ent.y & 0x3ff0u, k + 1);
+          float b0[4], b1[4];
+          uint32_t r0[4], r1[4];
+          if constexpr (MODE == 8) ld_x4(qa + ((o0 >> 2) & 508), r0);
+          if constexpr (MODE != 7) ld_x4(qa + ((o1 >> 2) & 508), r1);
+          if constexpr (MODE == 7 || MODE == 9) {
+            const float4 v = sm4[(o0 + lane) & 4095];
+            b0[0] = v.x; b0[1] = v.y; b0[2] = v.z; b0[3] = v.w;
+          }
+          if constexpr (MODE == 7) {
+            const float4 v = sm4[(o1 + lane) & 4095];
+            b1[0] = v.x; b1[1] = v.y; b1[2] = v.z; b1[3] = v.w;
+          }
+          if constexpr (MODE != 7) {
+            wait_ld();
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              if constexpr (MODE == 8) b0[v] = __uint_as_float(r0[v]);
+              b1[v] = __uint_as_float(r1[v]);
+            }
+          }
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            acc[(k & 2) * 2 + v] = fmaf(a0, b0[v], acc[(k & 2) * 2 + v]);
+            acc[8 + (k & 2) * 2 + v] = fmaf(a1, b1[v], acc[8 + (k & 2) * 2 + v]);
+          }
+        }
+      } else if constexpr (MODE == 10) {
+        // broadcast-entry baseline: LDS.64 broadcast per entry + LDS.128 B + 4 FFMA
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint2 e = reinterpret_cast<const uint2*>(sm4)[(i * 8 + k) & 8191];
+          const float4 v = sm4[((e.y & 0x3ff0u) + lane) & 4095];
+          const float a = __uint_as_float(e.x) + 1.0f;
+          acc[(k & 3) * 4 + 0] = fmaf(a, v.x, acc[(k & 3) * 4 + 0]);
+          acc[(k & 3) * 4 + 1] = fmaf(a, v.y, acc[(k & 3) * 4 + 1]);
+          acc[(k & 3) * 4 + 2] = fmaf(a, v.z, acc[(k & 3) * 4 + 2]);
+          acc[(k & 3) * 4 + 3] = fmaf(a, v.w, acc[(k & 3) * 4 + 3]);
+        }
       }
     }
   }
@@ -223,5 +271,10 @@ int main() {
   run<4>("mix_split_tmem_lds", sms, out, 16, (8 * 128.0 + 8 * 512.0) / 2, (8 * 32.0 + 32 * 32.0) / 2);
   run<5>("mix_interleaved", sms, out, 16, 8 * 128.0 + 4 * 512.0, 8 * 32.0 + 16 * 32.0);
   for (int w : {4, 16}) run<6>("tmem_st_x4", sms, out, w, 8 * 512.0, 0);
+  // per iteration 32 entries x 4 FMA per lane = 4096 FMA per warp
+  for (int w : {8, 16}) run<7>("shfl_entries_lds_b", sms, out, w, 32 * 512.0 + 256, 32 * 128.0);
+  for (int w : {8, 16}) run<8>("shfl_entries_tmem_b", sms, out, w, 32 * 512.0, 32 * 128.0);
+  for (int w : {8, 16}) run<9>("shfl_entries_mix_b", sms, out, w, 32 * 512.0 + 256, 32 * 128.0);
+  for (int w : {8, 16}) run<10>("bcast_entries_lds_b", sms, out, w, 8 * 512.0, 8 * 128.0);
   return 0;
 }
