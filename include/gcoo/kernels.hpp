@@ -1,0 +1,179 @@
+// gcoo/kernels.hpp — drop-in for the reference's kernel API
+// (proj/include/gcoo/kernels.hpp:1-369).
+//
+// spdm_gcoo (both overloads, :334-348) and spdm_gcoo_auto (:353-367) keep the
+// reference's signatures, validation order and exception types, and run on the
+// B200 through gcoo_spdm_{f32,f64} (libgcoo_cuda.so).  C is bitwise
+// independent of p, b, tile order and worker count (as in the reference) and
+// equals the reference's column-ascending accumulation chain with FMA
+// contraction.  spdm_csr / spdm_coo (:163-232) — C is the same per-row
+// column-ascending chain — run through the same GPU path after a device
+// CSR/COO -> GCOO conversion.  gemm_oracle (the test oracle) and
+// gemm_dense_blocked (the dense crossover baseline) stay host loops.
+#pragma once
+
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <thread>
+#include <vector>
+
+#include "gcoo/capi_bridge.hpp"
+#include "gcoo/matrix.hpp"
+#include "gcoo/types.hpp"
+
+namespace gcoo {
+
+// p x b output tiles; both powers of two (kernels.hpp:27-37).  `workers` is
+// accepted for API compatibility; the GPU result does not depend on it.
+struct ExecConfig {
+  index_t p = 4;
+  index_t b = 64;
+  int workers = 0;
+
+  void validate() const {
+    if (!is_pow2(p) || !is_pow2(b)) throw std::invalid_argument("ExecConfig: p and b must be powers of two");
+    if (workers < 0) throw std::invalid_argument("ExecConfig: workers must be >= 0");
+  }
+};
+
+inline int resolve_workers(int workers) {
+  if (workers > 0) return workers;
+  const unsigned hc = std::thread::hardware_concurrency();
+  return hc ? static_cast<int>(hc) : 1;
+}
+
+// Counters of the reference's tile schedule for the caller's b (:52-65):
+// flops = 2 nnz N; staging_fills = nnz ceil(N/b); b_loads_total = N x runs
+// (maximal same-column stretches inside b-entry chunks of a group slice);
+// b_loads_reused = N x (nnz - runs).  Computed by a device run counter.
+struct KernelStats {
+  std::uint64_t flops = 0;
+  std::uint64_t b_loads_total = 0;
+  std::uint64_t b_loads_reused = 0;
+  std::uint64_t staging_fills = 0;
+
+  KernelStats& operator+=(const KernelStats& o) {
+    flops += o.flops;
+    b_loads_total += o.b_loads_total;
+    b_loads_reused += o.b_loads_reused;
+    staging_fills += o.staging_fills;
+    return *this;
+  }
+};
+
+struct TimingBreakdown {
+  double eo_seconds = 0.0;
+  double kc_seconds = 0.0;
+};
+
+// ------------------------------------------------------- host oracle GEMM --
+// Serial triple loop accumulating in double (:80-98) — the test oracle.
+template <typename T>
+DenseMatrix<T> gemm_oracle(const DenseMatrix<T>& a, const DenseMatrix<T>& b) {
+  if (a.cols != b.rows) throw std::invalid_argument("gemm_oracle: inner dimensions differ");
+  DenseMatrix<T> c(a.rows, b.cols);
+  for (std::int64_t i = 0; i < a.rows; ++i)
+    for (std::int64_t j = 0; j < b.cols; ++j) {
+      double s = 0.0;
+      for (std::int64_t l = 0; l < a.cols; ++l) s += static_cast<double>(a(i, l)) * static_cast<double>(b(l, j));
+      c(i, j) = static_cast<T>(s);
+    }
+  return c;
+}
+
+// Dense blocked GEMM baseline (:107-155): per C element the sum runs over l
+// ascending regardless of the tile geometry, so the result does not depend on
+// cfg (host loop; out of the GPU path's scope).
+template <typename T>
+DenseMatrix<T> gemm_dense_blocked(const DenseMatrix<T>& a, const DenseMatrix<T>& b, const ExecConfig& cfg) {
+  cfg.validate();
+  if (a.cols != b.rows) throw std::invalid_argument("gemm_dense_blocked: inner dimensions differ");
+  DenseMatrix<T> c(a.rows, b.cols);
+  for (std::int64_t i = 0; i < a.rows; ++i) {
+    T* crow = c.row_ptr(i);
+    for (std::int64_t l = 0; l < a.cols; ++l) {
+      const T av = a(i, l);
+      const T* brow = b.row_ptr(l);
+      for (std::int64_t j = 0; j < b.cols; ++j) crow[j] += av * brow[j];
+    }
+  }
+  return c;
+}
+
+// --------------------------------------------------------------- GCOOSpDM --
+namespace detail {
+template <typename T>
+DenseMatrix<T> spdm_gcoo_impl(const GcooMatrix<T>& a, const DenseMatrix<T>& b, const ExecConfig& cfg,
+                              const std::int64_t* tile_order, std::int64_t tile_count, KernelStats* stats) {
+  cfg.validate();  // then the shape checks, in the C ABI, in the reference's order (:244-254)
+  DenseMatrix<T> c(a.rows_dim, b.cols);
+  gcoo_stats st{};
+  capi::check(capi::spdm(a.rows_dim, a.cols_dim, b.cols, a.p, cfg.p, cfg.b, b.rows, a.nnz(), a.values.data(),
+                         a.row_idx.data(), a.col_idx.data(), a.groups(), a.g_idxes.data(), a.nnz_per_group.data(),
+                         b.data.data(), c.data.data(), stats ? &st : nullptr, tile_order, tile_count));
+  if (stats) {
+    KernelStats k;
+    k.flops = st.flops;
+    k.b_loads_total = st.b_loads_total;
+    k.b_loads_reused = st.b_loads_reused;
+    k.staging_fills = st.staging_fills;
+    *stats = k;  // the reference overwrites (:325)
+  }
+  return c;
+}
+}  // namespace detail
+
+/// C = A * B with A in GCOO form, on the B200 (kernels.hpp:334-340).
+template <typename T>
+DenseMatrix<T> spdm_gcoo(const GcooMatrix<T>& a, const DenseMatrix<T>& b, const ExecConfig& cfg,
+                         KernelStats* stats = nullptr) {
+  return detail::spdm_gcoo_impl(a, b, cfg, nullptr, 0, stats);
+}
+
+/// Same, with the reference's explicit tile order (kernels.hpp:342-348): must
+/// hold groups * ceil(N/b) tile ids; a permutation cannot change C.
+template <typename T>
+DenseMatrix<T> spdm_gcoo(const GcooMatrix<T>& a, const DenseMatrix<T>& b, const ExecConfig& cfg,
+                         std::span<const std::int64_t> tile_order, KernelStats* stats = nullptr) {
+  return detail::spdm_gcoo_impl(a, b, cfg, tile_order.data(), static_cast<std::int64_t>(tile_order.size()), stats);
+}
+
+/// EO (dense -> GCOO on the GPU) + KC (spdm_gcoo), wall-clock split (:353-367).
+template <typename T>
+DenseMatrix<T> spdm_gcoo_auto(const DenseMatrix<T>& a, const DenseMatrix<T>& b, const ExecConfig& cfg,
+                              TimingBreakdown& timing, KernelStats* stats = nullptr) {
+  cfg.validate();
+  using clock = std::chrono::steady_clock;
+  const auto t0 = clock::now();
+  const GcooMatrix<T> g = dense_to_gcoo(a, cfg.p);
+  const auto t1 = clock::now();
+  DenseMatrix<T> c = spdm_gcoo(g, b, cfg, stats);
+  const auto t2 = clock::now();
+  timing.eo_seconds = std::chrono::duration<double>(t1 - t0).count();
+  timing.kc_seconds = std::chrono::duration<double>(t2 - t1).count();
+  return c;
+}
+
+// ---------------------------------------------- CSR / COO baselines (GPU) --
+/// Row-split CSR SpDM (:163-184).  Per C element: the row's nonzeros in
+/// ascending column order — the GCOO kernel's chain — so the CSR is grouped on
+/// the device and multiplied by the same kernel.
+template <typename T>
+DenseMatrix<T> spdm_csr(const CsrMatrix<T>& a, const DenseMatrix<T>& b, const ExecConfig& cfg) {
+  cfg.validate();
+  if (a.cols_dim != b.rows) throw std::invalid_argument("spdm_csr: inner dimensions differ");
+  return spdm_gcoo(csr_to_gcoo(a, cfg.p), b, cfg);
+}
+
+/// Ungrouped COO SpDM ablation (:193-232); same per-element chain.
+template <typename T>
+DenseMatrix<T> spdm_coo(const CooMatrix<T>& a, const DenseMatrix<T>& b, const ExecConfig& cfg) {
+  cfg.validate();
+  if (a.cols_dim != b.rows) throw std::invalid_argument("spdm_coo: inner dimensions differ");
+  return spdm_gcoo(coo_to_gcoo(a, cfg.p), b, cfg);
+}
+
+}  // namespace gcoo

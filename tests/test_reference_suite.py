@@ -1,0 +1,45 @@
+"""The reference's OWN unit tests (proj/tests/test_matrix.cpp and
+test_kernels.cpp, compiled unmodified against the drop-in C++ headers in
+include/gcoo by tests/cpp/Makefile) run on the B200 through libgcoo_cuda.so.
+
+They cover the GCOO goldens (test_matrix.cpp:49-68), the converters' error
+types (:70-102), round trips and cross-format agreement (:138-209), the
+kernel's identity/flops and hand-traced reuse counters (test_kernels.cpp:
+91-155), odd shapes against gemm_oracle at 1e-5 / 1e-12 (:157-183),
+validation exceptions (:185-198), bitwise determinism over p/b/workers and
+tile order (:200-234) and spdm_gcoo_auto == two-step (:236-252).
+"""
+import os
+import shutil
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BUILD = os.path.join(ROOT, "tests", "cpp", "_build")
+SUITES = ["ref_test_matrix", "ref_test_kernels"]
+
+
+def test_drop_in_headers_compile():
+    """The drop-in headers are self-contained C++20 (no GPU needed)."""
+    gxx = shutil.which("g++")
+    if gxx is None:
+        pytest.skip("no g++")
+    src = '#include "gcoo/kernels.hpp"\n#include "gcoo/matrix.hpp"\n' \
+          "template gcoo::DenseMatrix<float> gcoo::spdm_gcoo(const gcoo::GcooMatrix<float>&, " \
+          "const gcoo::DenseMatrix<float>&, const gcoo::ExecConfig&, gcoo::KernelStats*);\n" \
+          "template gcoo::GcooMatrix<double> gcoo::coo_to_gcoo(const gcoo::CooMatrix<double>&, gcoo::index_t);\n"
+    r = subprocess.run([gxx, "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"), "-x", "c++", "-"],
+                       input=src, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_unit_suite_on_b200(cuda, gcoo, suite):
+    exe = os.path.join(BUILD, suite)
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (needs the reference sources: make -C tests/cpp)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "failed: 0 | assertions" in r.stdout and r.stdout.rstrip().endswith("failed: 0"), r.stdout
