@@ -98,6 +98,8 @@ def lib():
     _sig(L, "gcoo_generate_powerlaw_coo_f32", _int, [_i64, _dbl, _dbl, _u64, _i64, _vp, _vp, _vp, C.POINTER(_i64)])
     _sig(L, "gcoo_derive_seed", _u64, [_u64, _u64, _u64])
     _sig(L, "gcoo_debug_force_kernel", _int, [_int])
+    _sig(L, "gcoo_debug_kernel_timing", _int, [_int])
+    _sig(L, "gcoo_debug_kernel_time", _int, [C.POINTER(_dbl), C.POINTER(_i64)])
     _lib = L
     return L
 
@@ -137,6 +139,19 @@ KERNELS = {"auto": -1, "rowtile": 0, "tile_v4": 5, "tacc_v4": 8, "tacc_v2": 9}
 def force_kernel(which: str = "auto") -> None:
     """Test/benchmark hook: pin the fp32 multiply kernel (auto = heuristic)."""
     lib().gcoo_debug_force_kernel(KERNELS[which])
+
+
+def kernel_timing(enable: bool = True) -> None:
+    """Benchmark hook: record CUDA events around every multiply-kernel launch
+    (planner kernels excluded); enable=True starts a fresh record."""
+    _check(lib().gcoo_debug_kernel_timing(1 if enable else 0))
+
+
+def kernel_time():
+    """(total ms, launches) of the multiply kernels recorded since kernel_timing(True)."""
+    t, n = _dbl(0.0), _i64(0)
+    _check(lib().gcoo_debug_kernel_time(C.byref(t), C.byref(n)))
+    return float(t.value), int(n.value)
 
 
 def launch_count() -> int:

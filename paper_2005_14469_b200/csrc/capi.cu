@@ -25,6 +25,33 @@ namespace gcoo_b200 {
 
 std::atomic<uint64_t> g_launches{0};
 
+// Optional CUDA-event timing of the multiply kernel itself (not the planner):
+// bench.py reports the dominant kernel's average duration from these events,
+// recorded on the launching stream around each launch.
+namespace {
+std::mutex g_kt_mu;
+bool g_kt_on = false;
+std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_kt_events;
+}  // namespace
+
+cudaEvent_t kt_start(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_kt_mu);
+  if (!g_kt_on) return nullptr;
+  cudaEvent_t e;
+  GCOO_CUDA(cudaEventCreate(&e));
+  GCOO_CUDA(cudaEventRecord(e, s));
+  return e;
+}
+
+void kt_stop(cudaStream_t s, cudaEvent_t start) {
+  if (!start) return;
+  cudaEvent_t e;
+  GCOO_CUDA(cudaEventCreate(&e));
+  GCOO_CUDA(cudaEventRecord(e, s));
+  std::lock_guard<std::mutex> lk(g_kt_mu);
+  g_kt_events.emplace_back(start, e);
+}
+
 namespace {
 
 thread_local std::string t_error;
@@ -144,9 +171,11 @@ void launch_rowtile(const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* 
   const int64_t col_tiles = ceil_div(n, 32 * V);
   const int64_t grid = row_blocks * col_tiles;
   if (grid > INT32_MAX) fail(GCOO_EINVAL, "spdm_gcoo: problem too large for one launch");
+  const cudaEvent_t kt0 = kt_start(s);
   GCOO_LAUNCH((spdm_rowtile_kernel<T, PMAX, VEC, FMA>), (unsigned)grid, kRowTileWarps * 32, 0, s, a.m,
               a.k, n, a.p, a.groups, a.vals, a.rows, a.cols, a.gidx, a.gnnz, B, ldb, C, ldc, row_tiles,
               row_blocks);
+  kt_stop(s, kt0);
 }
 
 template <typename T, bool FMA>
@@ -239,8 +268,10 @@ void launch_tile(const DevGcoo<float>& a, int64_t n, const float* B, int64_t ldb
   const int64_t col_tiles = ceil_div(n, Cfg::W);
   const int64_t grid = row_blocks * col_tiles;
   if (grid > INT32_MAX) fail(GCOO_EINVAL, "spdm_gcoo: problem too large for one launch");
+  const cudaEvent_t kt0 = kt_start(s);
   GCOO_LAUNCH(spdm_tile_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n, ent.get(),
               seg_off.get(), C, ldc, row_blocks, nchunks);
+  kt_stop(s, kt0);
 }
 
 // TMEM-accumulator variant (spdm_tacc.cuh); same planner protocol.
@@ -280,8 +311,10 @@ void launch_tacc(const DevGcoo<float>& a, int64_t n, const float* B, int64_t ldb
   const int64_t col_tiles = ceil_div(n, Cfg::W);
   const int64_t grid = row_blocks * col_tiles;
   if (grid > INT32_MAX) fail(GCOO_EINVAL, "spdm_gcoo: problem too large for one launch");
+  const cudaEvent_t kt0 = kt_start(s);
   GCOO_LAUNCH(spdm_tacc_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n, ent.get(),
               seg_off.get(), C, ldc, row_blocks, nchunks);
+  kt_stop(s, kt0);
 }
 
 // Which fp32 kernel runs: a tiled configuration whenever the layout allows
@@ -666,6 +699,36 @@ int gcoo_set_device(int device) {
 }
 
 uint64_t gcoo_launch_count(void) { return g_launches.load(); }
+
+// Test/benchmark hooks (not in the public header): CUDA-event timing of the
+// multiply kernel launches.  enable=1 starts a fresh record, 0 stops.
+int gcoo_debug_kernel_timing(int enable) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_kt_mu);
+    for (auto& pr : g_kt_events) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    g_kt_events.clear();
+    g_kt_on = enable != 0;
+  });
+}
+
+// Sum of the recorded launches' durations (synchronises on their events).
+int gcoo_debug_kernel_time(double* total_ms, int64_t* launches) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_kt_mu);
+    double t = 0;
+    for (auto& pr : g_kt_events) {
+      GCOO_CUDA(cudaEventSynchronize(pr.second));
+      float ms = 0;
+      GCOO_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+      t += ms;
+    }
+    *total_ms = t;
+    *launches = (int64_t)g_kt_events.size();
+  });
+}
 
 // Test/benchmark hook (not in the public header): pin the fp32 kernel choice.
 int gcoo_debug_force_kernel(int which) {
