@@ -231,89 +231,91 @@ bool tile_fits(const DevGcoo<float>& a, int64_t n, int64_t ldb, int64_t ldc, con
          n <= INT32_MAX && a.m <= (int64_t)INT32_MAX;
 }
 
-// Planner (device, no host synchronisation) + the multiply, all on stream s.
-template <class Cfg>
-void launch_tile(const DevGcoo<float>& a, int64_t n, const float* B, int64_t ldb, float* C, int64_t ldc,
-                 cudaStream_t s) {
-  static bool attr_set[64] = {};
-  int d = 0;
-  GCOO_CUDA(cudaGetDevice(&d));
-  if (!attr_set[d]) {
-    GCOO_CUDA(cudaFuncSetAttribute(spdm_tile_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)Cfg::SMEM));
-    attr_set[d] = true;
-  }
-  const int64_t units = ceil_div(a.m, Cfg::RW);
-  const int64_t row_blocks = ceil_div(a.m, Cfg::RB);
-  const int nchunks = (int)ceil_div(a.k, Cfg::KC);
-  const int64_t nseg = row_blocks * nchunks;
-  DevBuf<uint32_t> cnt(units * nchunks * Cfg::RW, s);
-  GCOO_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
-  if (a.nnz > 0)
-    GCOO_LAUNCH(tile_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks, cnt.get());
-  DevBuf<int64_t> seg_len(nseg, s), seg_off(nseg + 1, s);
-  GCOO_LAUNCH(tile_size_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
-              seg_len.get());
-  exclusive_scan(seg_len.get(), seg_off.get(), nseg, s);
-  // upper bound of the stream (see tile_warp_size): headers + 16*G bytes per entry
-  const int64_t bound = nseg * (Cfg::TABLE + Cfg::NW * Cfg::HDR) + (int64_t)Cfg::REC * a.nnz + 16;
-  DevBuf<unsigned char> ent(bound, s);
-  DevBuf<int64_t> slot_pos(nseg * Cfg::NW * Cfg::RW, s);
-  GCOO_LAUNCH(tile_header_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
-              seg_off.get(), ent.get(), slot_pos.get());
-  if (a.nnz > 0)
-    GCOO_LAUNCH(tile_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols, a.gidx,
-                nchunks, slot_pos.get(), ent.get());
-  const CUtensorMap map = make_b_map(B, a.k, n, ldb, Cfg::W, Cfg::KC);
-  const int64_t col_tiles = ceil_div(n, Cfg::W);
-  const int64_t grid = row_blocks * col_tiles;
-  if (grid > INT32_MAX) fail(GCOO_EINVAL, "spdm_gcoo: problem too large for one launch");
-  const cudaEvent_t kt0 = kt_start(s);
-  GCOO_LAUNCH(spdm_tile_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n, ent.get(),
-              seg_off.get(), C, ldc, row_blocks, nchunks);
-  kt_stop(s, kt0);
-}
+// A prepared multiply: the kernel choice and, for the tiled kernels, the
+// device record stream built from A by the planner (no host sync).  One plan
+// serves any number of B/C column strips with the same layout class
+// (the host-pointer path pipelines strips through one plan).
+struct SpdmPlan {
+  int kind = 0;  // 0 row-tile, 5 tile_v4, 8 tacc_v4, 9 tacc_v2
+  DevBuf<int64_t> seg_off;
+  DevBuf<unsigned char> ent;
+  int64_t row_blocks = 0;
+  int nchunks = 0;
+};
 
-// TMEM-accumulator variant (spdm_tacc.cuh); same planner protocol.
-template <class Cfg>
-void launch_tacc(const DevGcoo<float>& a, int64_t n, const float* B, int64_t ldb, float* C, int64_t ldc,
-                 cudaStream_t s) {
+template <class Cfg, bool TACC>
+void set_smem_attr() {
   static bool attr_set[64] = {};
   int d = 0;
   GCOO_CUDA(cudaGetDevice(&d));
-  if (!attr_set[d]) {
+  if (attr_set[d]) return;
+  if constexpr (TACC)
     GCOO_CUDA(cudaFuncSetAttribute(spdm_tacc_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)Cfg::SMEM));
-    attr_set[d] = true;
-  }
+  else
+    GCOO_CUDA(cudaFuncSetAttribute(spdm_tile_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)Cfg::SMEM));
+  attr_set[d] = true;
+}
+
+// Planner: counts -> segment sizes -> scan -> headers -> scatter, on stream s.
+template <class Cfg, bool TACC>
+void build_plan(SpdmPlan& P, const DevGcoo<float>& a, cudaStream_t s) {
+  set_smem_attr<Cfg, TACC>();
   const int64_t units = ceil_div(a.m, Cfg::RW);
-  const int64_t row_blocks = ceil_div(a.m, Cfg::RB);
-  const int nchunks = (int)ceil_div(a.k, Cfg::KC);
-  const int64_t nseg = row_blocks * nchunks;
+  P.row_blocks = ceil_div(a.m, Cfg::RB);
+  P.nchunks = (int)ceil_div(a.k, Cfg::KC);
+  const int nchunks = P.nchunks;
+  const int64_t nseg = P.row_blocks * nchunks;
   DevBuf<uint32_t> cnt(units * nchunks * Cfg::RW, s);
   GCOO_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
-  if (a.nnz > 0)
-    GCOO_LAUNCH(tacc_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks, cnt.get());
-  DevBuf<int64_t> seg_len(nseg, s), seg_off(nseg + 1, s);
-  GCOO_LAUNCH(tacc_size_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
-              seg_len.get());
-  exclusive_scan(seg_len.get(), seg_off.get(), nseg, s);
-  // upper bound of the stream (see tile_warp_size): headers + 16*G bytes per entry
+  if (a.nnz > 0) {
+    if constexpr (TACC)
+      GCOO_LAUNCH(tacc_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks, cnt.get());
+    else
+      GCOO_LAUNCH(tile_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks, cnt.get());
+  }
+  DevBuf<int64_t> seg_len(nseg, s);
+  P.seg_off = DevBuf<int64_t>(nseg + 1, s);
+  if constexpr (TACC)
+    GCOO_LAUNCH(tacc_size_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
+                seg_len.get());
+  else
+    GCOO_LAUNCH(tile_size_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
+                seg_len.get());
+  exclusive_scan(seg_len.get(), P.seg_off.get(), nseg, s);
+  // upper bound of the stream: headers + one record (16 B) per entry
   const int64_t bound = nseg * (Cfg::TABLE + Cfg::NW * Cfg::HDR) + (int64_t)Cfg::REC * a.nnz + 16;
-  DevBuf<unsigned char> ent(bound, s);
+  P.ent = DevBuf<unsigned char>(bound, s);
   DevBuf<int64_t> slot_pos(nseg * Cfg::NW * Cfg::RW, s);
-  GCOO_LAUNCH(tacc_header_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
-              seg_off.get(), ent.get(), slot_pos.get());
-  if (a.nnz > 0)
-    GCOO_LAUNCH(tacc_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols, a.gidx,
-                nchunks, slot_pos.get(), ent.get());
+  if constexpr (TACC) {
+    GCOO_LAUNCH(tacc_header_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
+                P.seg_off.get(), P.ent.get(), slot_pos.get());
+    if (a.nnz > 0)
+      GCOO_LAUNCH(tacc_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols,
+                  a.gidx, nchunks, slot_pos.get(), P.ent.get());
+  } else {
+    GCOO_LAUNCH(tile_header_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
+                P.seg_off.get(), P.ent.get(), slot_pos.get());
+    if (a.nnz > 0)
+      GCOO_LAUNCH(tile_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols,
+                  a.gidx, nchunks, slot_pos.get(), P.ent.get());
+  }
+}
+
+template <class Cfg, bool TACC>
+void run_plan(const SpdmPlan& P, const DevGcoo<float>& a, int64_t n, const float* B, int64_t ldb, float* C,
+              int64_t ldc, cudaStream_t s) {
   const CUtensorMap map = make_b_map(B, a.k, n, ldb, Cfg::W, Cfg::KC);
-  const int64_t col_tiles = ceil_div(n, Cfg::W);
-  const int64_t grid = row_blocks * col_tiles;
+  const int64_t grid = P.row_blocks * ceil_div(n, Cfg::W);
   if (grid > INT32_MAX) fail(GCOO_EINVAL, "spdm_gcoo: problem too large for one launch");
   const cudaEvent_t kt0 = kt_start(s);
-  GCOO_LAUNCH(spdm_tacc_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n, ent.get(),
-              seg_off.get(), C, ldc, row_blocks, nchunks);
+  if constexpr (TACC)
+    GCOO_LAUNCH(spdm_tacc_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n, P.ent.get(),
+                P.seg_off.get(), C, ldc, P.row_blocks, P.nchunks);
+  else
+    GCOO_LAUNCH(spdm_tile_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n, P.ent.get(),
+                P.seg_off.get(), C, ldc, P.row_blocks, P.nchunks);
   kt_stop(s, kt0);
 }
 
@@ -322,32 +324,51 @@ void launch_tacc(const DevGcoo<float>& a, int64_t n, const float* B, int64_t ldb
 int g_force_kernel = -1;  // test hook: -1 auto, 0 row-tile, 5 tile_v4, 8 tacc_v4, 9 tacc_v2
 
 template <typename T>
+int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const T* B, const T* C, int flavor) {
+  if constexpr (std::is_same<T, float>::value) {
+    if (flavor == GCOO_FLAVOR_MUL_ADD || g_force_kernel == 0 || a.m == 0) return 0;
+    const double density = (double)a.nnz / ((double)a.m * (double)a.k);
+    const int pick = g_force_kernel > 0 ? g_force_kernel : density >= 0.03 ? 5 : 8;
+    switch (pick) {
+      case 5: return tile_fits<TileV4>(a, n, ldb, ldc, B, C) ? 5 : 0;
+      case 8: return tile_fits<TaccV4>(a, n, ldb, ldc, B, C) ? 8 : 0;
+      case 9: return tile_fits<TaccV2>(a, n, ldb, ldc, B, C) ? 9 : 0;
+      default: return 0;
+    }
+  }
+  return 0;
+}
+
+template <typename T>
+void make_plan(SpdmPlan& P, const DevGcoo<T>& a, int kind, cudaStream_t s) {
+  P.kind = kind;
+  if constexpr (std::is_same<T, float>::value) {
+    if (kind == 5) build_plan<TileV4, false>(P, a, s);
+    if (kind == 8) build_plan<TaccV4, true>(P, a, s);
+    if (kind == 9) build_plan<TaccV2, true>(P, a, s);
+  }
+}
+
+template <typename T>
+void run_spdm(const SpdmPlan& P, const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C, int64_t ldc,
+              int flavor, cudaStream_t s) {
+  if (a.m == 0 || n == 0) return;
+  if constexpr (std::is_same<T, float>::value) {
+    if (P.kind == 5) return run_plan<TileV4, false>(P, a, n, B, ldb, C, ldc, s);
+    if (P.kind == 8) return run_plan<TaccV4, true>(P, a, n, B, ldb, C, ldc, s);
+    if (P.kind == 9) return run_plan<TaccV2, true>(P, a, n, B, ldb, C, ldc, s);
+  }
+  if (flavor != GCOO_FLAVOR_MUL_ADD) launch_rowtile_p<T, true>(a, n, B, ldb, C, ldc, s);
+  else launch_rowtile_p<T, false>(a, n, B, ldb, C, ldc, s);
+}
+
+template <typename T>
 void launch_spdm(const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C, int64_t ldc, int flavor,
                  cudaStream_t s) {
   if (a.m == 0 || n == 0) return;
-  const bool fma = flavor != GCOO_FLAVOR_MUL_ADD;
-  if constexpr (std::is_same<T, float>::value) {
-    if (fma && g_force_kernel != 0) {
-      const double density = (double)a.nnz / ((double)a.m * (double)a.k);
-      int pick = g_force_kernel;
-      if (pick < 0) pick = density >= 0.03 ? 5 : 8;
-      switch (pick) {
-        case 5:
-          if (tile_fits<TileV4>(a, n, ldb, ldc, B, C)) return launch_tile<TileV4>(a, n, B, ldb, C, ldc, s);
-          break;
-        case 8:
-          if (tile_fits<TaccV4>(a, n, ldb, ldc, B, C)) return launch_tacc<TaccV4>(a, n, B, ldb, C, ldc, s);
-          break;
-        case 9:
-          if (tile_fits<TaccV2>(a, n, ldb, ldc, B, C)) return launch_tacc<TaccV2>(a, n, B, ldb, C, ldc, s);
-          break;
-        default:
-          break;
-      }
-    }
-  }
-  if (fma) launch_rowtile_p<T, true>(a, n, B, ldb, C, ldc, s);
-  else launch_rowtile_p<T, false>(a, n, B, ldb, C, ldc, s);
+  SpdmPlan P;
+  make_plan<T>(P, a, choose_kind<T>(a, n, ldb, ldc, B, C, flavor), s);
+  run_spdm<T>(P, a, n, B, ldb, C, ldc, flavor, s);
 }
 
 // KernelStats for the caller's b (flops, staging and run counts; see
@@ -429,6 +450,35 @@ bool tile_order_is_permutation(const int64_t* order, int64_t count) {
   return perm;
 }
 
+// Host-pointer multiply.  Large problems are pipelined over column strips of
+// B/C (C is bitwise independent of the column partition): the H2D copy of
+// strip j+1, the multiply of strip j and the D2H copy of strip j-1 run on
+// three streams, with one plan (record stream) built from A for all strips.
+int64_t pipeline_strip(int64_t m, int64_t k, int64_t n) {
+  if (n < 2048 || (m + k) * n < (int64_t)32 << 20) return 0;  // small: one shot
+  int64_t w = ceil_div(ceil_div(n, 16), 128) * 128;
+  return std::max<int64_t>(w, 256);
+}
+
+cudaStream_t aux_stream(int which) {
+  thread_local cudaStream_t streams[64][2] = {};
+  const int d = current_device();
+  if (!streams[d][which]) GCOO_CUDA(cudaStreamCreateWithFlags(&streams[d][which], cudaStreamNonBlocking));
+  return streams[d][which];
+}
+
+struct Events {
+  std::vector<cudaEvent_t> ev;
+  explicit Events(int count) : ev(count, nullptr) {
+    for (auto& e : ev) GCOO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  ~Events() {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  cudaEvent_t operator[](int i) const { return ev[i]; }
+};
+
 template <typename T>
 void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int32_t cfg_b, int64_t b_rows,
                int64_t nnz, const T* values, const int32_t* row_idx, const int32_t* col_idx, int64_t groups,
@@ -437,7 +487,7 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
   validate_spdm(m, k, n, a_p, cfg_p, cfg_b, b_rows, nnz, groups, tile_order, tile_count);
   const bool perm = tile_order ? tile_order_is_permutation(tile_order, tile_count) : true;
   cudaStream_t s = thread_stream();
-  DevBuf<T> d_vals(nnz, s), d_B(k * n, s), d_C(m * n, s);
+  DevBuf<T> d_vals(nnz, s);
   DevBuf<int32_t> d_rows(nnz, s), d_cols(nnz, s);
   DevBuf<int64_t> d_gidx(groups, s), d_gnnz(groups, s);
   h2d(d_vals.get(), values, nnz, s);
@@ -445,15 +495,54 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
   h2d(d_cols.get(), col_idx, nnz, s);
   h2d(d_gidx.get(), g_idxes, groups, s);
   h2d(d_gnnz.get(), gnnz, groups, s);
-  h2d(d_B.get(), B, k * n, s);
   DevGcoo<T> a{m, k, nnz, groups, a_p, d_vals.get(), d_rows.get(), d_cols.get(), d_gidx.get(), d_gnnz.get()};
-  launch_spdm<T>(a, n, d_B.get(), n, d_C.get(), n, flavor, s);
-  if (!perm) {
-    apply_tile_list<T>(a, n, cfg_b, tile_order, tile_count, d_C.get(), n, stats, s);
-  } else if (stats) {
-    device_stats(nnz, n, a_p, cfg_b, groups, d_rows.get(), d_cols.get(), d_gidx.get(), stats, s);
+  const int64_t W = perm ? pipeline_strip(m, k, n) : 0;
+  if (W == 0) {
+    DevBuf<T> d_B(k * n, s), d_C(m * n, s);
+    h2d(d_B.get(), B, k * n, s);
+    launch_spdm<T>(a, n, d_B.get(), n, d_C.get(), n, flavor, s);
+    if (!perm) {
+      apply_tile_list<T>(a, n, cfg_b, tile_order, tile_count, d_C.get(), n, stats, s);
+    } else if (stats) {
+      device_stats(nnz, n, a_p, cfg_b, groups, d_rows.get(), d_cols.get(), d_gidx.get(), stats, s);
+    }
+    d2h(C, d_C.get(), m * n, s);
+    GCOO_CUDA(cudaStreamSynchronize(s));
+    return;
   }
-  d2h(C, d_C.get(), m * n, s);
+  // ---- pipelined: double-buffered strips of W columns (ld = W)
+  cudaStream_t s_in = aux_stream(0), s_out = aux_stream(1);
+  DevBuf<T> dB0(k * W, s), dB1(k * W, s), dC0(m * W, s), dC1(m * W, s);
+  T* dB[2] = {dB0.get(), dB1.get()};
+  T* dC[2] = {dC0.get(), dC1.get()};
+  SpdmPlan P;
+  make_plan<T>(P, a, choose_kind<T>(a, W, W, W, dB[0], dC[0], flavor), s);
+  Events ev(7);  // 0: ready, 1-2: in_done[b], 3-4: cmp_done[b], 5-6: out_done[b]
+  GCOO_CUDA(cudaEventRecord(ev[0], s));
+  GCOO_CUDA(cudaStreamWaitEvent(s_in, ev[0], 0));
+  GCOO_CUDA(cudaStreamWaitEvent(s_out, ev[0], 0));
+  const int64_t nstrips = ceil_div(n, W);
+  for (int64_t j = 0; j < nstrips; ++j) {
+    const int b = (int)(j & 1);
+    const int64_t c0 = j * W, w = std::min<int64_t>(W, n - c0);
+    if (j >= 2) GCOO_CUDA(cudaStreamWaitEvent(s_in, ev[3 + b], 0));  // dB[b] consumed by strip j-2
+    GCOO_CUDA(cudaMemcpy2DAsync(dB[b], W * sizeof(T), B + c0, n * sizeof(T), w * sizeof(T), k,
+                                cudaMemcpyHostToDevice, s_in));
+    GCOO_CUDA(cudaEventRecord(ev[1 + b], s_in));
+    GCOO_CUDA(cudaStreamWaitEvent(s, ev[1 + b], 0));
+    if (j >= 2) GCOO_CUDA(cudaStreamWaitEvent(s, ev[5 + b], 0));  // dC[b] drained by strip j-2
+    run_spdm<T>(P, a, w, dB[b], W, dC[b], W, flavor, s);
+    GCOO_CUDA(cudaEventRecord(ev[3 + b], s));
+    GCOO_CUDA(cudaStreamWaitEvent(s_out, ev[3 + b], 0));
+    GCOO_CUDA(cudaMemcpy2DAsync(C + c0, n * sizeof(T), dC[b], W * sizeof(T), w * sizeof(T), m,
+                                cudaMemcpyDeviceToHost, s_out));
+    GCOO_CUDA(cudaEventRecord(ev[5 + b], s_out));
+  }
+  if (stats) device_stats(nnz, n, a_p, cfg_b, groups, d_rows.get(), d_cols.get(), d_gidx.get(), stats, s);
+  // the strip buffers are freed (stream-ordered on s) only after the last copy-out
+  GCOO_CUDA(cudaStreamWaitEvent(s, ev[5 + (int)((nstrips - 1) & 1)], 0));
+  if (nstrips >= 2) GCOO_CUDA(cudaStreamWaitEvent(s, ev[5 + (int)((nstrips - 2) & 1)], 0));
+  GCOO_CUDA(cudaStreamSynchronize(s_out));
   GCOO_CUDA(cudaStreamSynchronize(s));
 }
 

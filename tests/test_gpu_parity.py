@@ -290,3 +290,32 @@ def test_full_size_n8000_matches_reference_hashes(gcoo, cuda, oracle, golden_has
     gcoo.spdm_gcoo_dev(d, bt, ct, flavor=gcoo.FLAVOR_MUL_ADD)
     torch.cuda.synchronize()
     assert oracle.fnv(ct.cpu().numpy()) == ent["C_mad"]["fnv"]
+    # the public host API pipelines this size over column strips: same bits
+    c_host = gcoo.spdm_gcoo(g, bm, gcoo.ExecConfig(), stats=(st2 := gcoo.KernelStats()))
+    assert oracle.fnv(c_host) == ent["C_fma"]["fnv"]
+    assert [st2.flops, st2.b_loads_total, st2.b_loads_reused, st2.staging_fills] == ent["stats_p4_b64"]
+
+
+@pytest.mark.parametrize("n", [2048, 2304, 2050, 3001])
+def test_host_pipeline_strips_bitwise_equal(gcoo, cuda, oracle, n):
+    """The host-pointer path splits B/C into column strips on three streams
+    (n >= 2048); every strip width, including a ragged last strip (n % 4 != 0),
+    must give the one-shot device result bit for bit, and the stats."""
+    import torch
+    rng = np.random.default_rng(n)
+    m = k = 8192
+    a = rand_dense(rng, m, k, 0.01)
+    bm = (1.0 - rng.random((k, n))).astype(np.float32)
+    g = gcoo.dense_to_gcoo(a, 4)
+    st = gcoo.KernelStats()
+    c_host = gcoo.spdm_gcoo(g, bm, gcoo.ExecConfig(), stats=st)
+    d = gcoo.DeviceGcoo.from_host(g)
+    ct = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    gcoo.force_kernel("rowtile")
+    try:
+        gcoo.spdm_gcoo_dev(d, torch.from_numpy(bm).cuda(), ct)
+        torch.cuda.synchronize()
+    finally:
+        gcoo.force_kernel("auto")
+    assert np.array_equal(c_host, ct.cpu().numpy())
+    assert st.flops == 2 * g.nnz() * n
