@@ -133,7 +133,7 @@ def set_device(device: int) -> None:
     _check(lib().gcoo_set_device(device))
 
 
-KERNELS = {"auto": -1, "rowtile": 0, "tile_v4": 5, "tacc_v4": 8, "tacc_v2": 9}
+KERNELS = {"auto": -1, "rowtile": 0, "tile_v4": 5, "tacc_v4": 8, "tacc_v2": 9, "tacc_v4w": 10}
 
 
 def force_kernel(which: str = "auto") -> None:

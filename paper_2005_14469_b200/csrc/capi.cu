@@ -328,11 +328,14 @@ int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const 
   if constexpr (std::is_same<T, float>::value) {
     if (flavor == GCOO_FLAVOR_MUL_ADD || g_force_kernel == 0 || a.m == 0) return 0;
     const double density = (double)a.nnz / ((double)a.m * (double)a.k);
-    const int pick = g_force_kernel > 0 ? g_force_kernel : density >= 0.03 ? 5 : 8;
+    // measured crossovers at n=8000 (profiles/r01_kernel_sweep.jsonl): register tiles win at
+    // s <= 0.95, TMEM accumulators with 24 warps for 0.95 < s < 0.998, 16 warps beyond
+    const int pick = g_force_kernel > 0 ? g_force_kernel : density >= 0.035 ? 5 : density >= 0.002 ? 10 : 8;
     switch (pick) {
       case 5: return tile_fits<TileV4>(a, n, ldb, ldc, B, C) ? 5 : 0;
       case 8: return tile_fits<TaccV4>(a, n, ldb, ldc, B, C) ? 8 : 0;
       case 9: return tile_fits<TaccV2>(a, n, ldb, ldc, B, C) ? 9 : 0;
+      case 10: return tile_fits<TaccV4W>(a, n, ldb, ldc, B, C) ? 10 : 0;
       default: return 0;
     }
   }
@@ -346,6 +349,7 @@ void make_plan(SpdmPlan& P, const DevGcoo<T>& a, int kind, cudaStream_t s) {
     if (kind == 5) build_plan<TileV4, false>(P, a, s);
     if (kind == 8) build_plan<TaccV4, true>(P, a, s);
     if (kind == 9) build_plan<TaccV2, true>(P, a, s);
+    if (kind == 10) build_plan<TaccV4W, true>(P, a, s);
   }
 }
 
@@ -357,6 +361,7 @@ void run_spdm(const SpdmPlan& P, const DevGcoo<T>& a, int64_t n, const T* B, int
     if (P.kind == 5) return run_plan<TileV4, false>(P, a, n, B, ldb, C, ldc, s);
     if (P.kind == 8) return run_plan<TaccV4, true>(P, a, n, B, ldb, C, ldc, s);
     if (P.kind == 9) return run_plan<TaccV2, true>(P, a, n, B, ldb, C, ldc, s);
+    if (P.kind == 10) return run_plan<TaccV4W, true>(P, a, n, B, ldb, C, ldc, s);
   }
   if (flavor != GCOO_FLAVOR_MUL_ADD) launch_rowtile_p<T, true>(a, n, B, ldb, C, ldc, s);
   else launch_rowtile_p<T, false>(a, n, B, ldb, C, ldc, s);

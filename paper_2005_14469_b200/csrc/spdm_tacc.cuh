@@ -42,12 +42,12 @@
 
 namespace gcoo_b200 {
 
-template <int V_, int KC_, int STAGES_, int CAP_>
+template <int V_, int KC_, int STAGES_, int CAP_, int NW_ = 16>
 struct TaccCfg {
   static constexpr int V = V_;             // floats per lane
   static constexpr int W = 32 * V_;        // columns per CTA strip
-  static constexpr int NW = 16;            // consumer warps: 4 per TMEM lane quadrant
-  static constexpr int TCOLS = 512 / (NW / 4);  // TMEM columns per warp (128)
+  static constexpr int NW = NW_;           // consumer warps: NW/4 per TMEM lane quadrant
+  static constexpr int TCOLS = (512 / (NW_ / 4)) & ~15;  // TMEM columns per warp (128 for 16 warps)
   static constexpr int RW = TCOLS / V_;    // rows (slots) per warp
   static constexpr int RB = NW * RW;       // rows per CTA
   static constexpr int KC = KC_;           // B rows per chunk
@@ -58,9 +58,10 @@ struct TaccCfg {
   static constexpr uint32_t STAGE_BYTES = BTILE + CAP_;
   static constexpr int HDR = 16;           // per-warp header: record count
   static constexpr int REC = 16;           // bytes per record
-  static constexpr int TABLE = 64;         // per-segment warp offset table (16 x u32)
+  static constexpr int TABLE = (4 * NW_ + 15) & ~15;  // per-segment warp offset table (NW x u32)
   static constexpr size_t SMEM = (size_t)STAGES_ * STAGE_BYTES + 2 * STAGES_ * 8 + 16;
   static_assert(KC_ <= 256, "TMA box rows");
+  static_assert(NW_ % 4 == 0 && NW_ <= 28 && TCOLS % (4 * V_) == 0, "warps tile the 4 TMEM lane quadrants");
   static_assert(BTILE < (1u << 24) && RW <= 256, "24-bit B offsets, 8-bit slots");
   static_assert(CAP_ % 16 == 0 && BTILE % 16 == 0, "16-byte stages");
   static_assert(SMEM <= 227 * 1024 && SMEM > 116 * 1024, "one CTA per SM (it owns all 512 TMEM columns)");
@@ -69,6 +70,7 @@ struct TaccCfg {
 //                      V  KC   S  CAP
 using TaccV4 = TaccCfg<4, 192, 2, 16384>;   // W=128, RB=512 : density >~ 2%
 using TaccV2 = TaccCfg<2, 256, 2, 16384>;   // W=64,  RB=1024: density ~ 1%
+using TaccV4W = TaccCfg<4, 192, 2, 16384, 24>;  // W=128, RB=480, 24 consumer warps (more latency hiding)
 
 // ---------------------------------------------------------------- planner --
 // P1: per (unit u = row / RW, chunk, slot = row % RW) entry counts.

@@ -98,7 +98,7 @@ def test_random_shapes_bit_exact(gcoo, cuda, oracle, seed):
         assert max_rel(c, c_mad) <= 1e-5
 
 
-@pytest.mark.parametrize("kernel", ["rowtile", "tile_v4", "tacc_v4", "tacc_v2", "auto"])
+@pytest.mark.parametrize("kernel", ["rowtile", "tile_v4", "tacc_v4", "tacc_v2", "tacc_v4w", "auto"])
 def test_each_fp32_kernel_bit_exact(gcoo, cuda, oracle, kernel):
     """Every fp32 kernel variant, on shapes that hit its edges (m not a multiple
     of the row block, k not a multiple of the chunk, n not a multiple of the

@@ -39,17 +39,17 @@ def main():
         for kname in args.kernels:
             G.force_kernel(kname)
             with torch.cuda.stream(st):
-                for _ in range(2):
+                for _ in range(3):
                     G.spdm_gcoo_dev(d, b, c, stream=st)
-                ts = []
-                for _ in range(args.reps):
+                evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                       for _ in range(args.reps)]
+                for e0, e1 in evs:  # back to back (no host sync between reps), L2 flushed before each
                     flush.zero_()
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(st)
                     G.spdm_gcoo_dev(d, b, c, stream=st)
                     e1.record(st)
-                    torch.cuda.synchronize()
-                    ts.append(e0.elapsed_time(e1))
+                torch.cuda.synchronize()
+                ts = [e0.elapsed_time(e1) for e0, e1 in evs]
             out = c.clone()
             same = None if ref is None else bool(torch.equal(out, ref))
             if ref is None:
