@@ -280,6 +280,9 @@ def run_ours(args):
                                "fp32_frac": round(f2 / (ms2 * 1e-3) / 1e12 / fp_peak, 4)}
             del dg2
 
+    if rank == 0 and world == 1 and not args.no_sweep:
+        extra.update(other_configs(G, dev, stream, flush, hbm_peak, fp_peak))
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(g_host, b_host, n)
@@ -327,6 +330,41 @@ def run_ours(args):
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
+
+
+def other_configs(G, dev, stream, flush, hbm_peak, fp_peak, steps=5):
+    """BASELINE configs[3] (power-law A, n=16384, s=0.99) and configs[4]'s
+    single-GPU point (n=32768, s=0.99): A from this repo's power-law generator
+    / the reference's uniform sample (as COO, grouped on the GPU); B uniform
+    (0,1] generated on the device (its values do not change the work)."""
+    import torch
+    out = {}
+    cases = [("powerlaw_n16384_s0.99", 16384, lambda: G.generate_powerlaw_coo(16384, 0.99, 1.0, SEED)),
+             ("uniform_n32768_s0.99", 32768, lambda: G.generate_uniform_sparse_coo(32768, 0.99, SEED))]
+    for name, n, gen in cases:
+        try:
+            v, r, c = gen()
+            dg = G.coo_to_gcoo_dev(n, n, torch.from_numpy(v).to(dev), torch.from_numpy(r).to(dev),
+                                   torch.from_numpy(c).to(dev), P)
+            k_nz = int(torch.unique(dg.col_idx).numel())
+            gen_b = torch.Generator(device=dev).manual_seed(SEED)
+            dB = 1.0 - torch.rand((n, n), device=dev, dtype=torch.float32, generator=gen_b)
+            dC = torch.empty((n, n), device=dev, dtype=torch.float32)
+            torch.cuda.synchronize()
+            ms, ms_min, _, kms = time_kernel(G, dg, dB, dC, steps, 3, stream, flush)
+            nnz = dg.nnz()
+            f = 2.0 * nnz * n
+            cb = compulsory_bytes(nnz, n, n, n, P, k_nz)
+            rows = torch.bincount(dg.row_idx.long(), minlength=n)
+            out[name] = {"n": n, "nnz": nnz, "max_row_nnz": int(rows.max()), "ms": round(ms, 4),
+                         "kernel_ms": round(kms, 4), "gflops": round(f / ms / 1e6, 1),
+                         "hbm_frac": round(cb / (kms * 1e-3) / 1e9 / hbm_peak, 4),
+                         "fp32_frac": round(f / (kms * 1e-3) / 1e12 / fp_peak, 4)}
+            del dg, dB, dC
+            torch.cuda.empty_cache()
+        except Exception as e:  # noqa: BLE001
+            out[name] = {"error": str(e)[:200]}
+    return out
 
 
 def cpu_baseline(g_host, b_host, n):

@@ -319,3 +319,38 @@ def test_host_pipeline_strips_bitwise_equal(gcoo, cuda, oracle, n):
         gcoo.force_kernel("auto")
     assert np.array_equal(c_host, ct.cpu().numpy())
     assert st.flops == 2 * g.nnz() * n
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("case", ["powerlaw_n16384", "uniform_n32768"])
+def test_large_configs_sampled_rows_bit_exact(gcoo, cuda, oracle, case):
+    """BASELINE configs[3] and [4] at full size: C from the device path on a
+    sample of rows x columns equals the oracle's FMA chain on the same
+    entries, bit for bit (the per-element chain depends only on the row's
+    entries and the column of B, so a sample is an exact check)."""
+    import torch
+    if case == "powerlaw_n16384":
+        n = 16384
+        v, r, c = gcoo.generate_powerlaw_coo(n, 0.99, 1.0, 1)
+    else:
+        n = 32768
+        v, r, c = gcoo.generate_uniform_sparse_coo(n, 0.99, 1)
+    dg = gcoo.coo_to_gcoo_dev(n, n, torch.from_numpy(v).cuda(), torch.from_numpy(r).cuda(),
+                              torch.from_numpy(c).cuda(), 4)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    dB = 1.0 - torch.rand((n, n), device="cuda", dtype=torch.float32, generator=gen)
+    dC = torch.empty((n, n), device="cuda", dtype=torch.float32)
+    gcoo.spdm_gcoo_dev(dg, dB, dC)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(5)
+    counts = np.bincount(r, minlength=n)
+    rows = np.unique(np.concatenate([rng.choice(n, 48, replace=False), [int(np.argmax(counts))]]))
+    cols = np.sort(rng.choice(n, 256, replace=False))
+    sel = np.isin(r, rows)
+    remap = {int(x): i for i, x in enumerate(rows)}
+    a_sub = np.zeros((len(rows), n), np.float32)
+    a_sub[[remap[int(x)] for x in r[sel]], c[sel]] = v[sel]
+    b_sub = np.ascontiguousarray(dB[:, torch.from_numpy(cols).cuda()].cpu().numpy())
+    c_ref, _ = oracle.spdm(oracle.dense_to_gcoo(a_sub, 4), b_sub, 64, fma=True)
+    c_gpu = dC[torch.from_numpy(rows).cuda()][:, torch.from_numpy(cols).cuda()].cpu().numpy()
+    assert np.array_equal(c_gpu, c_ref)
