@@ -236,11 +236,13 @@ bool tile_fits(const DevGcoo<float>& a, int64_t n, int64_t ldb, int64_t ldc, con
 // serves any number of B/C column strips with the same layout class
 // (the host-pointer path pipelines strips through one plan).
 struct SpdmPlan {
-  int kind = 0;  // 0 row-tile, 5 tile_v4, 8 tacc_v4, 9 tacc_v2
+  int kind = 0;  // 0 row-tile, 5 tile_v4, 8 tacc_v4, 9 tacc_v2, 10 tacc_v4w
   DevBuf<int64_t> seg_off;
   DevBuf<unsigned char> ent;
   int64_t row_blocks = 0;
   int nchunks = 0;
+  // TMEM kernels: row placement (original row -> unit row, and back; -1 = padding)
+  DevBuf<int32_t> unit_of, row_of;
 };
 
 template <class Cfg, bool TACC>
@@ -262,16 +264,33 @@ void set_smem_attr() {
 template <class Cfg, bool TACC>
 void build_plan(SpdmPlan& P, const DevGcoo<float>& a, cudaStream_t s) {
   set_smem_attr<Cfg, TACC>();
-  const int64_t units = ceil_div(a.m, Cfg::RW);
   P.row_blocks = ceil_div(a.m, Cfg::RB);
+  // TMEM kernels place rows anywhere in their row block's warps: every warp is a unit
+  const int64_t units = TACC ? P.row_blocks * Cfg::NW : ceil_div(a.m, Cfg::RW);
   P.nchunks = (int)ceil_div(a.k, Cfg::KC);
   const int nchunks = P.nchunks;
   const int64_t nseg = P.row_blocks * nchunks;
   DevBuf<uint32_t> cnt(units * nchunks * Cfg::RW, s);
   GCOO_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
+  if constexpr (TACC) {
+    // load-balanced row placement: heaviest rows first, dealt over a block's warps
+    DevBuf<int32_t> row_nnz(a.m, s), hist(33, s), cursor(33, s);
+    GCOO_CUDA(cudaMemsetAsync(row_nnz.get(), 0, row_nnz.bytes(), s));
+    GCOO_CUDA(cudaMemsetAsync(hist.get(), 0, hist.bytes(), s));
+    GCOO_CUDA(cudaMemsetAsync(cursor.get(), 0, cursor.bytes(), s));
+    if (a.nnz > 0) GCOO_LAUNCH(row_nnz_kernel, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, row_nnz.get());
+    GCOO_LAUNCH(bucket_hist_kernel, grid_for(a.m, 256), 256, 0, s, a.m, row_nnz.get(), hist.get());
+    P.unit_of = DevBuf<int32_t>(a.m, s);
+    P.row_of = DevBuf<int32_t>(P.row_blocks * Cfg::RB, s);
+    GCOO_CUDA(cudaMemsetAsync(P.row_of.get(), 0xff, P.row_of.bytes(), s));
+    GCOO_LAUNCH(row_balance_kernel, grid_for(a.m, 256), 256, 0, s, a.m, row_nnz.get(), hist.get(), cursor.get(),
+                (int32_t)Cfg::RB, (int32_t)Cfg::NW, (int32_t)Cfg::RW,
+                (int32_t)std::min<int64_t>(INT32_MAX, 4 * ceil_div(a.nnz, a.m) + 16), P.unit_of.get(), P.row_of.get());
+  }
   if (a.nnz > 0) {
     if constexpr (TACC)
-      GCOO_LAUNCH(tacc_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks, cnt.get());
+      GCOO_LAUNCH(tacc_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks, cnt.get(),
+                  P.unit_of.get());
     else
       GCOO_LAUNCH(tile_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks, cnt.get());
   }
@@ -293,7 +312,7 @@ void build_plan(SpdmPlan& P, const DevGcoo<float>& a, cudaStream_t s) {
                 P.seg_off.get(), P.ent.get(), slot_pos.get());
     if (a.nnz > 0)
       GCOO_LAUNCH(tacc_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols,
-                  a.gidx, nchunks, slot_pos.get(), P.ent.get());
+                  a.gidx, nchunks, slot_pos.get(), P.ent.get(), P.unit_of.get());
   } else {
     GCOO_LAUNCH(tile_header_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
                 P.seg_off.get(), P.ent.get(), slot_pos.get());
@@ -312,7 +331,7 @@ void run_plan(const SpdmPlan& P, const DevGcoo<float>& a, int64_t n, const float
   const cudaEvent_t kt0 = kt_start(s);
   if constexpr (TACC)
     GCOO_LAUNCH(spdm_tacc_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n, P.ent.get(),
-                P.seg_off.get(), C, ldc, P.row_blocks, P.nchunks);
+                P.seg_off.get(), C, ldc, P.row_blocks, P.nchunks, P.row_of.get());
   else
     GCOO_LAUNCH(spdm_tile_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n, P.ent.get(),
                 P.seg_off.get(), C, ldc, P.row_blocks, P.nchunks);

@@ -325,4 +325,72 @@ __global__ void zero_uncovered_kernel(int64_t m, int64_t n, int32_t p, int32_t b
   }
 }
 
+// ------------------------------------------------- row load balancing --
+// Entries per row; lanes holding the same row combine first (one atomic per
+// distinct row per warp: a dense power-law row is not 16K same-address atomics).
+__global__ void row_nnz_kernel(int64_t nnz, const int32_t* __restrict__ rows, int32_t* __restrict__ row_nnz) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~int64_t(31); base < nnz;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = base + lane;
+    const bool valid = e < nnz;
+    const int32_t r = valid ? rows[e] : -1;
+    const unsigned same = __match_any_sync(0xffffffffu, r);
+    if (valid && lane == __ffs(same) - 1) atomicAdd(&row_nnz[r], __popc(same));
+  }
+}
+
+// Load-balanced placement of rows into (row block, warp, slot) units for the
+// TMEM kernels: rows are ordered by log2(nnz) bucket, heaviest first (a
+// counting sort; order inside a bucket is arbitrary — C does not depend on
+// where a row is computed), then sorted position i goes to row block
+// i / RB, warp (i % RB) % NW, slot (i % RB) / NW.
+__device__ __forceinline__ int nnz_bucket(int32_t c) { return 31 - (c > 0 ? 31 - __clz(c) : -1) - 1; }
+
+// hist[1..32]: rows per bucket; hist[0]: the largest row.
+__global__ void bucket_hist_kernel(int64_t m, const int32_t* __restrict__ row_nnz, int32_t* __restrict__ hist) {
+  __shared__ int32_t h[33];
+  if (threadIdx.x < 33) h[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    atomicAdd(&h[nnz_bucket(row_nnz[r]) + 1], 1);
+    atomicMax(&h[0], row_nnz[r]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&hist[0], h[0]);
+  if (threadIdx.x >= 1 && threadIdx.x < 33 && h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+}
+
+// Rows stay in place (identity placement) unless the largest row exceeds
+// `skew` entries: uniform matrices keep their natural order.
+__global__ void row_balance_kernel(int64_t m, const int32_t* __restrict__ row_nnz, const int32_t* __restrict__ hist,
+                                   int32_t* __restrict__ cursor, int32_t rb_rows, int32_t nw, int32_t rw,
+                                   int32_t skew, int32_t* __restrict__ unit_of, int32_t* __restrict__ row_of) {
+  __shared__ int32_t off[33];
+  if (threadIdx.x == 0) {
+    int32_t acc = 0;
+    off[0] = 0;
+    for (int b = 1; b < 33; ++b) {
+      off[b] = acc;
+      acc += hist[b];
+    }
+  }
+  __syncthreads();
+  if (hist[0] <= skew) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+      unit_of[r] = (int32_t)r;
+      row_of[r] = (int32_t)r;
+    }
+    return;
+  }
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    const int b = nnz_bucket(row_nnz[r]) + 1;
+    const int64_t i = off[b] + atomicAdd(&cursor[b], 1);
+    const int64_t j = i % rb_rows;
+    const int64_t u = (i / rb_rows) * rb_rows + (j % nw) * rw + j / nw;
+    unit_of[r] = (int32_t)u;
+    row_of[u] = (int32_t)r;
+  }
+}
+
 }  // namespace gcoo_b200

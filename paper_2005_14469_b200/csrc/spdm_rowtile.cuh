@@ -88,24 +88,16 @@ __device__ __forceinline__ void accumulate(T (&acc)[PMAX][V], int slot, T a, con
 
 constexpr int kRowTileWarps = 8;
 
+// One warp computes row tile rt (rows [rt*PMAX, rt*PMAX + PMAX)) x column
+// tile ct (32V columns).
 template <typename T, int PMAX, bool VEC, bool FMA>
-__global__ void __launch_bounds__(kRowTileWarps * 32)
-spdm_rowtile_kernel(int64_t m, int64_t k, int64_t n, int32_t p, int64_t groups,
-                    const T* __restrict__ vals, const int32_t* __restrict__ rows,
-                    const int32_t* __restrict__ cols, const int64_t* __restrict__ gidx,
-                    const int64_t* __restrict__ gnnz, const T* __restrict__ B, int64_t ldb,
-                    T* __restrict__ C, int64_t ldc, int64_t row_tiles, int64_t row_blocks) {
-  static_assert(PMAX <= 16 && (PMAX & (PMAX - 1)) == 0, "PMAX must be a power of two <= 16");
+__device__ __forceinline__ void rowtile_warp(StagedEntry<T>* stage, int64_t rt, int64_t ct, int64_t m, int64_t k,
+                                             int64_t n, int32_t p, int64_t groups, const T* __restrict__ vals,
+                                             const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
+                                             const int64_t* __restrict__ gidx, const int64_t* __restrict__ gnnz,
+                                             const T* __restrict__ B, int64_t ldb, T* __restrict__ C, int64_t ldc) {
   constexpr int V = VecOf<T>::V;
-  __shared__ StagedEntry<T> stage[kRowTileWarps][32];
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // Row blocks vary fastest so co-resident CTAs share one B column strip
-  // (k x 32V, L2-resident) and walk it in the same ascending-column order.
-  const int64_t rb = blockIdx.x % row_blocks;
-  const int64_t ct = blockIdx.x / row_blocks;
-  const int64_t rt = rb * kRowTileWarps + warp;
-  if (rt >= row_tiles) return;  // warp-uniform; no block-wide barriers below
+  const int lane = threadIdx.x & 31;
   const int64_t r0 = rt * PMAX;
   const int64_t j0 = ct * (32 * V) + (int64_t)lane * V;
 
@@ -134,22 +126,33 @@ spdm_rowtile_kernel(int64_t m, int64_t k, int64_t n, int32_t p, int64_t groups,
         r = rows[e];
       }
       // keep entries of this tile's rows whose column is addressable
-      const bool mine = valid && (!filter || (r >= r0 && r < r0 + PMAX)) &&
-                        (uint32_t)c < (uint64_t)k;
+      const bool mine = valid && (!filter || (r >= r0 && r < r0 + PMAX)) && (uint32_t)c < (uint64_t)k;
       const unsigned mask = __ballot_sync(0xffffffffu, mine);
       if (mine) {
         StagedEntry<T> se;
         se.val = v;
         se.col = c;
         se.slot = r & (PMAX - 1);
-        stage[warp][__popc(mask & lt_mask)] = se;
+        stage[__popc(mask & lt_mask)] = se;
       }
       __syncwarp();
       const int count = __popc(mask);
       int q = 0;
+      // 8 independent B loads in flight per lane before their FMAs (latency-bound
+      // when a tile holds a long row: one B row segment per entry from L2)
+      for (; q + 8 <= count; q += 8) {
+        StagedEntry<T> e[8];
+        T bv[8][V];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) e[u] = stage[q + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) load_b<T, V, VEC>(B, ldb, e[u].col, j0, n, bv[u]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) accumulate<T, PMAX, V, FMA>(acc, e[u].slot, e[u].val, bv[u]);
+      }
       for (; q + 4 <= count; q += 4) {
-        StagedEntry<T> e0 = stage[warp][q], e1 = stage[warp][q + 1];
-        StagedEntry<T> e2 = stage[warp][q + 2], e3 = stage[warp][q + 3];
+        StagedEntry<T> e0 = stage[q], e1 = stage[q + 1];
+        StagedEntry<T> e2 = stage[q + 2], e3 = stage[q + 3];
         T b0[V], b1[V], b2[V], b3[V];
         load_b<T, V, VEC>(B, ldb, e0.col, j0, n, b0);
         load_b<T, V, VEC>(B, ldb, e1.col, j0, n, b1);
@@ -161,7 +164,7 @@ spdm_rowtile_kernel(int64_t m, int64_t k, int64_t n, int32_t p, int64_t groups,
         accumulate<T, PMAX, V, FMA>(acc, e3.slot, e3.val, b3);
       }
       for (; q < count; ++q) {
-        StagedEntry<T> e0 = stage[warp][q];
+        StagedEntry<T> e0 = stage[q];
         T b0[V];
         load_b<T, V, VEC>(B, ldb, e0.col, j0, n, b0);
         accumulate<T, PMAX, V, FMA>(acc, e0.slot, e0.val, b0);
@@ -190,6 +193,26 @@ spdm_rowtile_kernel(int64_t m, int64_t k, int64_t n, int32_t p, int64_t groups,
         if (j0 + v < n) dst[v] = acc[s][v];
     }
   }
+}
+
+template <typename T, int PMAX, bool VEC, bool FMA>
+__global__ void __launch_bounds__(kRowTileWarps * 32)
+spdm_rowtile_kernel(int64_t m, int64_t k, int64_t n, int32_t p, int64_t groups,
+                    const T* __restrict__ vals, const int32_t* __restrict__ rows,
+                    const int32_t* __restrict__ cols, const int64_t* __restrict__ gidx,
+                    const int64_t* __restrict__ gnnz, const T* __restrict__ B, int64_t ldb,
+                    T* __restrict__ C, int64_t ldc, int64_t row_tiles, int64_t row_blocks) {
+  static_assert(PMAX <= 16 && (PMAX & (PMAX - 1)) == 0, "PMAX must be a power of two <= 16");
+  __shared__ StagedEntry<T> stage[kRowTileWarps][32];
+  const int warp = threadIdx.x >> 5;
+  // Row blocks vary fastest so co-resident CTAs share one B column strip
+  // (k x 32V, L2-resident) and walk it in the same ascending-column order.
+  const int64_t rb = blockIdx.x % row_blocks;
+  const int64_t ct = blockIdx.x / row_blocks;
+  const int64_t rt = rb * kRowTileWarps + warp;
+  if (rt >= row_tiles) return;  // warp-uniform; no block-wide barriers
+  rowtile_warp<T, PMAX, VEC, FMA>(stage[warp], rt, ct, m, k, n, p, groups, vals, rows, cols, gidx, gnnz, B, ldb, C,
+                                  ldc);
 }
 
 }  // namespace gcoo_b200

@@ -42,6 +42,8 @@
 
 namespace gcoo_b200 {
 
+__device__ __forceinline__ int64_t ceil_div_dev(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
 template <int V_, int KC_, int STAGES_, int CAP_, int NW_ = 16>
 struct TaccCfg {
   static constexpr int V = V_;             // floats per lane
@@ -74,11 +76,14 @@ using TaccV4W = TaccCfg<4, 192, 2, 16384, 24>;  // W=128, RB=480, 24 consumer wa
 
 // ---------------------------------------------------------------- planner --
 // P1: per (unit u = row / RW, chunk, slot = row % RW) entry counts.
+// Rows are placed into (row block, warp, slot) by `unit_of` (see
+// row_balance_kernel): heaviest rows first, dealt round-robin over a row
+// block's warps, so warps carry similar loads on skewed (power-law) matrices.
 template <class Cfg>
 __global__ void tacc_count_kernel(int64_t nnz, const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
-                                  int nchunks, uint32_t* __restrict__ cnt) {
+                                  int nchunks, uint32_t* __restrict__ cnt, const int32_t* __restrict__ unit_of) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r = rows[e];
+    const int32_t r = unit_of[rows[e]];
     const int32_t c = cols[e] / Cfg::KC;
     atomicAdd(&cnt[((int64_t)(r / Cfg::RW) * nchunks + c) * Cfg::RW + (r % Cfg::RW)], 1u);
   }
@@ -160,7 +165,8 @@ template <class Cfg>
 __global__ void tacc_fill_kernel(int64_t nnz, int32_t p, const float* __restrict__ vals,
                                  const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
                                  const int64_t* __restrict__ gidx, int nchunks,
-                                 const int64_t* __restrict__ slot_pos, unsigned char* __restrict__ ent) {
+                                 const int64_t* __restrict__ slot_pos, unsigned char* __restrict__ ent,
+                                 const int32_t* __restrict__ unit_of) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
     const int32_t r = rows[e], col = cols[e];
     const int c = col / Cfg::KC;
@@ -171,10 +177,11 @@ __global__ void tacc_fill_kernel(int64_t nnz, int32_t p, const float* __restrict
       if (cols[j] < lo_col) break;
       rank += rows[j] == r;
     }
-    const int64_t u = r / Cfg::RW;
+    const int32_t ur = unit_of[r];
+    const int64_t u = ur / Cfg::RW;
     const int64_t rb = u / Cfg::NW;
     const int w = (int)(u % Cfg::NW);
-    const uint32_t slot = (uint32_t)(r % Cfg::RW);
+    const uint32_t slot = (uint32_t)(ur % Cfg::RW);
     const int64_t base = slot_pos[((rb * nchunks + c) * Cfg::NW + w) * Cfg::RW + slot];
     uint32_t* word = reinterpret_cast<uint32_t*>(ent + base + (int64_t)Cfg::REC * (rank >> 1));
     const uint32_t off = (uint32_t)(col - lo_col) * (uint32_t)(Cfg::W * 4);
@@ -254,7 +261,7 @@ template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
 spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t n, const unsigned char* __restrict__ ent,
                  const int64_t* __restrict__ seg_off, float* __restrict__ C, int64_t ldc, int64_t row_blocks,
-                 int nchunks) {
+                 int nchunks, const int32_t* __restrict__ row_of) {
   constexpr int W = Cfg::W, NW = Cfg::NW, S = Cfg::STAGES, V = Cfg::V, RW = Cfg::RW;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * Cfg::STAGE_BYTES);
@@ -263,8 +270,19 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
   const uint32_t smem0 = smem_u32(smem_raw);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t rb = blockIdx.x % row_blocks;  // row blocks fastest: co-resident CTAs share a B strip
-  const int64_t ct = blockIdx.x / row_blocks;
+  // Row block 0 holds the heaviest rows (row_balance_kernel): its CTAs go
+  // first, then row blocks vary fastest so co-resident CTAs share a B strip.
+  const int64_t col_tiles = ceil_div_dev(n, W);
+  int64_t rb, ct;
+  if (row_blocks > 1 && (int64_t)blockIdx.x < col_tiles) {
+    rb = 0;
+    ct = blockIdx.x;
+  } else {
+    const int64_t x = row_blocks > 1 ? (int64_t)blockIdx.x - col_tiles : (int64_t)blockIdx.x;
+    const int64_t rest = row_blocks > 1 ? row_blocks - 1 : 1;
+    rb = (row_blocks > 1 ? 1 : 0) + x % rest;
+    ct = x / rest;
+  }
   const int64_t* so = seg_off + rb * nchunks;
 
   if (threadIdx.x == 0) {
@@ -346,8 +364,8 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
     if (j < n) {
 #pragma unroll
       for (int k = 0; k < 16 / V; ++k) {
-        const int64_t row = row0 + c0 / V + k;
-        if (row < m) {
+        const int64_t row = row_of[row0 + c0 / V + k];  // -1: padding slot
+        if (row >= 0) {
           float* dst = C + row * ldc + j;
           if constexpr (V == 4) {
             *reinterpret_cast<float4*>(dst) = make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);

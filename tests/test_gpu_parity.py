@@ -354,3 +354,26 @@ def test_large_configs_sampled_rows_bit_exact(gcoo, cuda, oracle, case):
     c_ref, _ = oracle.spdm(oracle.dense_to_gcoo(a_sub, 4), b_sub, 64, fma=True)
     c_gpu = dC[torch.from_numpy(rows).cuda()][:, torch.from_numpy(cols).cuda()].cpu().numpy()
     assert np.array_equal(c_gpu, c_ref)
+
+
+@pytest.mark.parametrize("kernel", ["tacc_v4", "tacc_v4w", "tacc_v2"])
+def test_heavy_rows_balanced_placement(gcoo, cuda, oracle, kernel):
+    """The TMEM kernels place rows heaviest-first across warps (a permutation
+    of rows into accumulator slots): with very uneven rows C must still be
+    bit-exact for every group size."""
+    rng = np.random.default_rng(11)
+    m, k, n = 1500, 3000, 384
+    a = rand_dense(rng, m, k, 0.004)
+    for r in (0, 17, 700, 1499):  # dense rows
+        a[r] = (1.0 - rng.random(k)).astype(np.float32)
+    a[900, ::2] = 0.5
+    bm = (1.0 - rng.random((k, n))).astype(np.float32)
+    gcoo.force_kernel(kernel)
+    try:
+        for p in (1, 4, 16, 32):
+            go = oracle.dense_to_gcoo(a, p)
+            c_ref, _ = oracle.spdm(go, bm, 64, fma=True)
+            c = gcoo.spdm_gcoo(to_prod(gcoo, go), bm, gcoo.ExecConfig(p=p))
+            assert np.array_equal(c, c_ref), (kernel, p)
+    finally:
+        gcoo.force_kernel("auto")
