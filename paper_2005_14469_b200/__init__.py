@@ -99,6 +99,7 @@ def lib():
     _sig(L, "gcoo_derive_seed", _u64, [_u64, _u64, _u64])
     _sig(L, "gcoo_debug_force_kernel", _int, [_int])
     _sig(L, "gcoo_debug_kernel_timing", _int, [_int])
+    _sig(L, "gcoo_debug_pipeline_strips", _int, [_int])
     _sig(L, "gcoo_debug_kernel_time", _int, [C.POINTER(_dbl), C.POINTER(_i64)])
     _lib = L
     return L

@@ -478,9 +478,11 @@ bool tile_order_is_permutation(const int64_t* order, int64_t count) {
 // B/C (C is bitwise independent of the column partition): the H2D copy of
 // strip j+1, the multiply of strip j and the D2H copy of strip j-1 run on
 // three streams, with one plan (record stream) built from A for all strips.
+int g_pipeline_strips = 32;  // tuning hook (gcoo_debug_pipeline_strips)
+
 int64_t pipeline_strip(int64_t m, int64_t k, int64_t n) {
-  if (n < 2048 || (m + k) * n < (int64_t)32 << 20) return 0;  // small: one shot
-  int64_t w = ceil_div(ceil_div(n, 16), 128) * 128;
+  if (g_pipeline_strips <= 1 || n < 2048 || (m + k) * n < (int64_t)32 << 20) return 0;  // small: one shot
+  int64_t w = ceil_div(ceil_div(n, g_pipeline_strips), 128) * 128;
   return std::max<int64_t>(w, 256);
 }
 
@@ -511,6 +513,30 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
   validate_spdm(m, k, n, a_p, cfg_p, cfg_b, b_rows, nnz, groups, tile_order, tile_count);
   const bool perm = tile_order ? tile_order_is_permutation(tile_order, tile_count) : true;
   cudaStream_t s = thread_stream();
+  const int64_t W = perm ? pipeline_strip(m, k, n) : 0;
+  // pipelined path: strip buffers first, so B strip 0 can start crossing PCIe
+  // while A is uploaded and planned on the compute stream
+  DevBuf<T> dB0(W ? k * W : 0, s), dB1(W ? k * W : 0, s), dC0(W ? m * W : 0, s), dC1(W ? m * W : 0, s);
+  Events ev(W ? 7 : 0);  // 0: buffers ready, 1-2: in_done[b], 3-4: cmp_done[b], 5-6: out_done[b]
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  if (W) {
+    s_in = aux_stream(0);
+    s_out = aux_stream(1);
+    GCOO_CUDA(cudaEventRecord(ev[0], s));
+    GCOO_CUDA(cudaStreamWaitEvent(s_in, ev[0], 0));
+    GCOO_CUDA(cudaStreamWaitEvent(s_out, ev[0], 0));
+  }
+  T* dB[2] = {dB0.get(), dB1.get()};
+  T* dC[2] = {dC0.get(), dC1.get()};
+  const int64_t nstrips = W ? ceil_div(n, W) : 0;
+  auto h2d_strip = [&](int64_t j) {
+    const int b = (int)(j & 1);
+    const int64_t c0 = j * W, w = std::min<int64_t>(W, n - c0);
+    GCOO_CUDA(cudaMemcpy2DAsync(dB[b], W * sizeof(T), B + c0, n * sizeof(T), w * sizeof(T), k,
+                                cudaMemcpyHostToDevice, s_in));
+    GCOO_CUDA(cudaEventRecord(ev[1 + b], s_in));
+  };
+  if (W) h2d_strip(0);
   DevBuf<T> d_vals(nnz, s);
   DevBuf<int32_t> d_rows(nnz, s), d_cols(nnz, s);
   DevBuf<int64_t> d_gidx(groups, s), d_gnnz(groups, s);
@@ -520,7 +546,6 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
   h2d(d_gidx.get(), g_idxes, groups, s);
   h2d(d_gnnz.get(), gnnz, groups, s);
   DevGcoo<T> a{m, k, nnz, groups, a_p, d_vals.get(), d_rows.get(), d_cols.get(), d_gidx.get(), d_gnnz.get()};
-  const int64_t W = perm ? pipeline_strip(m, k, n) : 0;
   if (W == 0) {
     DevBuf<T> d_B(k * n, s), d_C(m * n, s);
     h2d(d_B.get(), B, k * n, s);
@@ -535,24 +560,15 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
     return;
   }
   // ---- pipelined: double-buffered strips of W columns (ld = W)
-  cudaStream_t s_in = aux_stream(0), s_out = aux_stream(1);
-  DevBuf<T> dB0(k * W, s), dB1(k * W, s), dC0(m * W, s), dC1(m * W, s);
-  T* dB[2] = {dB0.get(), dB1.get()};
-  T* dC[2] = {dC0.get(), dC1.get()};
   SpdmPlan P;
   make_plan<T>(P, a, choose_kind<T>(a, W, W, W, dB[0], dC[0], flavor), s);
-  Events ev(7);  // 0: ready, 1-2: in_done[b], 3-4: cmp_done[b], 5-6: out_done[b]
-  GCOO_CUDA(cudaEventRecord(ev[0], s));
-  GCOO_CUDA(cudaStreamWaitEvent(s_in, ev[0], 0));
-  GCOO_CUDA(cudaStreamWaitEvent(s_out, ev[0], 0));
-  const int64_t nstrips = ceil_div(n, W);
   for (int64_t j = 0; j < nstrips; ++j) {
     const int b = (int)(j & 1);
     const int64_t c0 = j * W, w = std::min<int64_t>(W, n - c0);
-    if (j >= 2) GCOO_CUDA(cudaStreamWaitEvent(s_in, ev[3 + b], 0));  // dB[b] consumed by strip j-2
-    GCOO_CUDA(cudaMemcpy2DAsync(dB[b], W * sizeof(T), B + c0, n * sizeof(T), w * sizeof(T), k,
-                                cudaMemcpyHostToDevice, s_in));
-    GCOO_CUDA(cudaEventRecord(ev[1 + b], s_in));
+    if (j >= 1) {
+      if (j >= 2) GCOO_CUDA(cudaStreamWaitEvent(s_in, ev[3 + b], 0));  // dB[b] consumed by strip j-2
+      h2d_strip(j);
+    }
     GCOO_CUDA(cudaStreamWaitEvent(s, ev[1 + b], 0));
     if (j >= 2) GCOO_CUDA(cudaStreamWaitEvent(s, ev[5 + b], 0));  // dC[b] drained by strip j-2
     run_spdm<T>(P, a, w, dB[b], W, dC[b], W, flavor, s);
@@ -841,6 +857,12 @@ int gcoo_debug_kernel_time(double* total_ms, int64_t* launches) {
     *total_ms = t;
     *launches = (int64_t)g_kt_events.size();
   });
+}
+
+// Tuning hook (not in the public header): column strips of the host pipeline.
+int gcoo_debug_pipeline_strips(int strips) {
+  g_pipeline_strips = strips;
+  return GCOO_OK;
 }
 
 // Test/benchmark hook (not in the public header): pin the fp32 kernel choice.
