@@ -230,6 +230,9 @@ __device__ __forceinline__ void tacc_consume(float (&acc)[Cfg::V], uint32_t& cur
                                              typename RecSrc<GLOBAL>::addr_t seg, int warp, uint32_t bbase) {
   using Src = RecSrc<GLOBAL>;
   constexpr int V = Cfg::V;
+  // keep the stage base in a register (ptxas otherwise rematerialises it from
+  // special registers inside the loop when registers are tight)
+  asm volatile("mov.b32 %0, %0;" : "+r"(bbase));
   const uint32_t woff = Src::ld32(seg + 4 * warp);
   const auto wseg = seg + woff;
   const uint32_t nrec = Src::ld32(wseg);
