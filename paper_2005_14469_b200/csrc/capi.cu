@@ -10,7 +10,11 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <memory>
+#include <tuple>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -261,10 +265,21 @@ void set_smem_attr() {
 }
 
 // Planner: counts -> segment sizes -> scan -> headers -> scatter, on stream s.
+// `min_ctas` (TMEM kernels): spread rows over enough row blocks that a launch
+// over `col_tiles` column tiles has at least that many CTAs (narrow strips of
+// the host pipeline); 0 = full row blocks.
 template <class Cfg, bool TACC>
-void build_plan(SpdmPlan& P, const DevGcoo<float>& a, cudaStream_t s) {
+void build_plan(SpdmPlan& P, const DevGcoo<float>& a, cudaStream_t s, int64_t min_ctas = 0, int64_t col_tiles = 1) {
   set_smem_attr<Cfg, TACC>();
   P.row_blocks = ceil_div(a.m, Cfg::RB);
+  int64_t rpb = Cfg::RB;
+  if (TACC && min_ctas > P.row_blocks * col_tiles) {
+    const int64_t want = std::min<int64_t>(ceil_div(min_ctas, col_tiles), ceil_div(a.m, 32));
+    if (want > P.row_blocks) {
+      rpb = ceil_div(a.m, want);
+      P.row_blocks = ceil_div(a.m, rpb);
+    }
+  }
   // TMEM kernels place rows anywhere in their row block's warps: every warp is a unit
   const int64_t units = TACC ? P.row_blocks * Cfg::NW : ceil_div(a.m, Cfg::RW);
   P.nchunks = (int)ceil_div(a.k, Cfg::KC);
@@ -285,7 +300,8 @@ void build_plan(SpdmPlan& P, const DevGcoo<float>& a, cudaStream_t s) {
     GCOO_CUDA(cudaMemsetAsync(P.row_of.get(), 0xff, P.row_of.bytes(), s));
     GCOO_LAUNCH(row_balance_kernel, grid_for(a.m, 256), 256, 0, s, a.m, row_nnz.get(), hist.get(), cursor.get(),
                 (int32_t)Cfg::RB, (int32_t)Cfg::NW, (int32_t)Cfg::RW,
-                (int32_t)std::min<int64_t>(INT32_MAX, 4 * ceil_div(a.nnz, a.m) + 16), P.unit_of.get(), P.row_of.get());
+                (int32_t)std::min<int64_t>(INT32_MAX, 4 * ceil_div(a.nnz, a.m) + 16), (int32_t)rpb, P.unit_of.get(),
+                P.row_of.get());
   }
   if (a.nnz > 0) {
     if constexpr (TACC)
@@ -361,14 +377,17 @@ int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const 
   return 0;
 }
 
+// strip_n > 0: the plan will serve column strips of that width (host pipeline)
+// — TMEM kernels then spread rows over enough blocks for one full wave.
 template <typename T>
-void make_plan(SpdmPlan& P, const DevGcoo<T>& a, int kind, cudaStream_t s) {
+void make_plan(SpdmPlan& P, const DevGcoo<T>& a, int kind, cudaStream_t s, int64_t strip_n = 0) {
   P.kind = kind;
+  const int64_t wave = strip_n ? sm_count() : 0;
   if constexpr (std::is_same<T, float>::value) {
     if (kind == 5) build_plan<TileV4, false>(P, a, s);
-    if (kind == 8) build_plan<TaccV4, true>(P, a, s);
-    if (kind == 9) build_plan<TaccV2, true>(P, a, s);
-    if (kind == 10) build_plan<TaccV4W, true>(P, a, s);
+    if (kind == 8) build_plan<TaccV4, true>(P, a, s, wave, ceil_div(strip_n, TaccV4::W));
+    if (kind == 9) build_plan<TaccV2, true>(P, a, s, wave, ceil_div(strip_n, TaccV2::W));
+    if (kind == 10) build_plan<TaccV4W, true>(P, a, s, wave, ceil_div(strip_n, TaccV4W::W));
   }
 }
 
@@ -477,13 +496,30 @@ bool tile_order_is_permutation(const int64_t* order, int64_t count) {
 // Host-pointer multiply.  Large problems are pipelined over column strips of
 // B/C (C is bitwise independent of the column partition): the H2D copy of
 // strip j+1, the multiply of strip j and the D2H copy of strip j-1 run on
-// three streams, with one plan (record stream) built from A for all strips.
+// three streams through a ring of NBUF strip buffers, with one plan (record
+// stream) built from A for all strips.  The first strip is narrow so that C
+// starts crossing PCIe (the other direction) as soon as A is planned: the
+// link runs both directions at once (profiles/r01_pcie_probe.jsonl: 99 GB/s
+// H2D+D2H vs 55 GB/s one way), so the D2H stream's start is the critical path.
 int g_pipeline_strips = 32;  // tuning hook (gcoo_debug_pipeline_strips)
+constexpr int NBUF = 3;
 
 int64_t pipeline_strip(int64_t m, int64_t k, int64_t n) {
   if (g_pipeline_strips <= 1 || n < 2048 || (m + k) * n < (int64_t)32 << 20) return 0;  // small: one shot
   int64_t w = ceil_div(ceil_div(n, g_pipeline_strips), 128) * 128;
   return std::max<int64_t>(w, 256);
+}
+
+// Column strips [c0, c0 + w): a 128-column lead strip, then strips of W.
+std::vector<std::pair<int64_t, int64_t>> pipeline_strips(int64_t n, int64_t W) {
+  std::vector<std::pair<int64_t, int64_t>> v;
+  int64_t c0 = 0;
+  if (W > 128) {
+    v.emplace_back(0, 128);
+    c0 = 128;
+  }
+  for (; c0 < n; c0 += W) v.emplace_back(c0, std::min<int64_t>(W, n - c0));
+  return v;
 }
 
 cudaStream_t aux_stream(int which) {
@@ -505,6 +541,35 @@ struct Events {
   cudaEvent_t operator[](int i) const { return ev[i]; }
 };
 
+// Debug timeline of the host pipeline (GCOO_TRACE_PIPELINE=1): timing events
+// per stage, printed to stderr as "stage strip ms-from-start".
+struct PipeTrace {
+  cudaEvent_t t0;
+  std::vector<std::tuple<int, int64_t, cudaEvent_t>> marks;
+  explicit PipeTrace(cudaStream_t s) {
+    GCOO_CUDA(cudaEventCreate(&t0));
+    GCOO_CUDA(cudaEventRecord(t0, s));
+  }
+  void mark(cudaStream_t s, int stage, int64_t j) {
+    cudaEvent_t e;
+    GCOO_CUDA(cudaEventCreate(&e));
+    GCOO_CUDA(cudaEventRecord(e, s));
+    marks.emplace_back(stage, j, e);
+  }
+  void dump(int64_t) {
+    GCOO_CUDA(cudaDeviceSynchronize());
+    static const char* names[] = {"a_up", "planned", "h2d_done", "cmp_start", "cmp_done", "d2h_done"};
+    for (auto& [st, j, e] : marks) {
+      float ms = 0.f;
+      GCOO_CUDA(cudaEventElapsedTime(&ms, t0, e));
+      std::fprintf(stderr, "trace %s %lld %.3f\n", names[st], (long long)j, ms);
+      cudaEventDestroy(e);
+    }
+    cudaEventDestroy(t0);
+    marks.clear();
+  }
+};
+
 template <typename T>
 void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int32_t cfg_b, int64_t b_rows,
                int64_t nnz, const T* values, const int32_t* row_idx, const int32_t* col_idx, int64_t groups,
@@ -516,8 +581,17 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
   const int64_t W = perm ? pipeline_strip(m, k, n) : 0;
   // pipelined path: strip buffers first, so B strip 0 can start crossing PCIe
   // while A is uploaded and planned on the compute stream
-  DevBuf<T> dB0(W ? k * W : 0, s), dB1(W ? k * W : 0, s), dC0(W ? m * W : 0, s), dC1(W ? m * W : 0, s);
-  Events ev(W ? 7 : 0);  // 0: buffers ready, 1-2: in_done[b], 3-4: cmp_done[b], 5-6: out_done[b]
+  const int nb = W ? NBUF : 0;
+  std::vector<DevBuf<T>> dBv, dCv;
+  for (int b = 0; b < nb; ++b) {
+    dBv.emplace_back(k * W, s);
+    dCv.emplace_back(m * W, s);
+  }
+  // events: 0 buffers ready, then per ring slot b: in_done 1+b, cmp_done 1+NBUF+b, out_done 1+2*NBUF+b
+  Events ev(W ? 1 + 3 * NBUF : 0);
+  auto in_done = [&](int b) { return ev[1 + b]; };
+  auto cmp_done = [&](int b) { return ev[1 + NBUF + b]; };
+  auto out_done = [&](int b) { return ev[1 + 2 * NBUF + b]; };
   cudaStream_t s_in = nullptr, s_out = nullptr;
   if (W) {
     s_in = aux_stream(0);
@@ -526,15 +600,17 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
     GCOO_CUDA(cudaStreamWaitEvent(s_in, ev[0], 0));
     GCOO_CUDA(cudaStreamWaitEvent(s_out, ev[0], 0));
   }
-  T* dB[2] = {dB0.get(), dB1.get()};
-  T* dC[2] = {dC0.get(), dC1.get()};
-  const int64_t nstrips = W ? ceil_div(n, W) : 0;
+  const auto strips = W ? pipeline_strips(n, W) : std::vector<std::pair<int64_t, int64_t>>{};
+  std::unique_ptr<PipeTrace> trace;
+  if (W && std::getenv("GCOO_TRACE_PIPELINE")) trace.reset(new PipeTrace(s));
+  const int64_t nstrips = (int64_t)strips.size();
   auto h2d_strip = [&](int64_t j) {
-    const int b = (int)(j & 1);
-    const int64_t c0 = j * W, w = std::min<int64_t>(W, n - c0);
-    GCOO_CUDA(cudaMemcpy2DAsync(dB[b], W * sizeof(T), B + c0, n * sizeof(T), w * sizeof(T), k,
+    const int b = (int)(j % NBUF);
+    const int64_t c0 = strips[j].first, w = strips[j].second;
+    GCOO_CUDA(cudaMemcpy2DAsync(dBv[b].get(), W * sizeof(T), B + c0, n * sizeof(T), w * sizeof(T), k,
                                 cudaMemcpyHostToDevice, s_in));
-    GCOO_CUDA(cudaEventRecord(ev[1 + b], s_in));
+    GCOO_CUDA(cudaEventRecord(in_done(b), s_in));
+    if (trace) trace->mark(s_in, 2, j);
   };
   if (W) h2d_strip(0);
   DevBuf<T> d_vals(nnz, s);
@@ -559,29 +635,35 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
     GCOO_CUDA(cudaStreamSynchronize(s));
     return;
   }
-  // ---- pipelined: double-buffered strips of W columns (ld = W)
+  // ---- pipelined: a ring of NBUF strip buffers (ld = W)
+  if (trace) trace->mark(s, 0, -1);  // A uploaded
   SpdmPlan P;
-  make_plan<T>(P, a, choose_kind<T>(a, W, W, W, dB[0], dC[0], flavor), s);
+  make_plan<T>(P, a, choose_kind<T>(a, W, W, W, dBv[0].get(), dCv[0].get(), flavor), s, W);
+  if (trace) trace->mark(s, 1, -1);  // planned
   for (int64_t j = 0; j < nstrips; ++j) {
-    const int b = (int)(j & 1);
-    const int64_t c0 = j * W, w = std::min<int64_t>(W, n - c0);
+    const int b = (int)(j % NBUF);
+    const int64_t c0 = strips[j].first, w = strips[j].second;
     if (j >= 1) {
-      if (j >= 2) GCOO_CUDA(cudaStreamWaitEvent(s_in, ev[3 + b], 0));  // dB[b] consumed by strip j-2
+      if (j >= NBUF) GCOO_CUDA(cudaStreamWaitEvent(s_in, cmp_done(b), 0));  // dB[b] consumed by strip j-NBUF
       h2d_strip(j);
     }
-    GCOO_CUDA(cudaStreamWaitEvent(s, ev[1 + b], 0));
-    if (j >= 2) GCOO_CUDA(cudaStreamWaitEvent(s, ev[5 + b], 0));  // dC[b] drained by strip j-2
-    run_spdm<T>(P, a, w, dB[b], W, dC[b], W, flavor, s);
-    GCOO_CUDA(cudaEventRecord(ev[3 + b], s));
-    GCOO_CUDA(cudaStreamWaitEvent(s_out, ev[3 + b], 0));
-    GCOO_CUDA(cudaMemcpy2DAsync(C + c0, n * sizeof(T), dC[b], W * sizeof(T), w * sizeof(T), m,
+    GCOO_CUDA(cudaStreamWaitEvent(s, in_done(b), 0));
+    if (j >= NBUF) GCOO_CUDA(cudaStreamWaitEvent(s, out_done(b), 0));  // dC[b] drained by strip j-NBUF
+    if (trace) trace->mark(s, 3, j);
+    run_spdm<T>(P, a, w, dBv[b].get(), W, dCv[b].get(), W, flavor, s);
+    if (trace) trace->mark(s, 4, j);
+    GCOO_CUDA(cudaEventRecord(cmp_done(b), s));
+    GCOO_CUDA(cudaStreamWaitEvent(s_out, cmp_done(b), 0));
+    GCOO_CUDA(cudaMemcpy2DAsync(C + c0, n * sizeof(T), dCv[b].get(), W * sizeof(T), w * sizeof(T), m,
                                 cudaMemcpyDeviceToHost, s_out));
-    GCOO_CUDA(cudaEventRecord(ev[5 + b], s_out));
+    GCOO_CUDA(cudaEventRecord(out_done(b), s_out));
+    if (trace) trace->mark(s_out, 5, j);
   }
   if (stats) device_stats(nnz, n, a_p, cfg_b, groups, d_rows.get(), d_cols.get(), d_gidx.get(), stats, s);
-  // the strip buffers are freed (stream-ordered on s) only after the last copy-out
-  GCOO_CUDA(cudaStreamWaitEvent(s, ev[5 + (int)((nstrips - 1) & 1)], 0));
-  if (nstrips >= 2) GCOO_CUDA(cudaStreamWaitEvent(s, ev[5 + (int)((nstrips - 2) & 1)], 0));
+  if (trace) trace->dump(nstrips);
+  // the strip buffers are freed (stream-ordered on s) only after the last copy-outs
+  for (int64_t j = std::max<int64_t>(0, nstrips - NBUF); j < nstrips; ++j)
+    GCOO_CUDA(cudaStreamWaitEvent(s, out_done((int)(j % NBUF)), 0));
   GCOO_CUDA(cudaStreamSynchronize(s_out));
   GCOO_CUDA(cudaStreamSynchronize(s));
 }

@@ -362,10 +362,14 @@ __global__ void bucket_hist_kernel(int64_t m, const int32_t* __restrict__ row_nn
 }
 
 // Rows stay in place (identity placement) unless the largest row exceeds
-// `skew` entries: uniform matrices keep their natural order.
+// `skew` entries: uniform matrices keep their natural order.  A row block may
+// hold fewer rows than the kernel's RB (`rpb` <= rb_rows): narrow column strips
+// then still give the GPU enough CTAs; block b takes sorted rows
+// [b*rpb, (b+1)*rpb), dealt over its warps, and its remaining slots are padding.
 __global__ void row_balance_kernel(int64_t m, const int32_t* __restrict__ row_nnz, const int32_t* __restrict__ hist,
                                    int32_t* __restrict__ cursor, int32_t rb_rows, int32_t nw, int32_t rw,
-                                   int32_t skew, int32_t* __restrict__ unit_of, int32_t* __restrict__ row_of) {
+                                   int32_t skew, int32_t rpb, int32_t* __restrict__ unit_of,
+                                   int32_t* __restrict__ row_of) {
   __shared__ int32_t off[33];
   if (threadIdx.x == 0) {
     int32_t acc = 0;
@@ -376,7 +380,8 @@ __global__ void row_balance_kernel(int64_t m, const int32_t* __restrict__ row_nn
     }
   }
   __syncthreads();
-  if (hist[0] <= skew) {
+  const bool skewed = hist[0] > skew;
+  if (!skewed && rpb == rb_rows) {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
       unit_of[r] = (int32_t)r;
       row_of[r] = (int32_t)r;
@@ -384,10 +389,13 @@ __global__ void row_balance_kernel(int64_t m, const int32_t* __restrict__ row_nn
     return;
   }
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
-    const int b = nnz_bucket(row_nnz[r]) + 1;
-    const int64_t i = off[b] + atomicAdd(&cursor[b], 1);
-    const int64_t j = i % rb_rows;
-    const int64_t u = (i / rb_rows) * rb_rows + (j % nw) * rw + j / nw;
+    int64_t i = r;
+    if (skewed) {
+      const int b = nnz_bucket(row_nnz[r]) + 1;
+      i = off[b] + atomicAdd(&cursor[b], 1);
+    }
+    const int64_t j = i % rpb;
+    const int64_t u = (i / rpb) * rb_rows + (j % nw) * rw + j / nw;
     unit_of[r] = (int32_t)u;
     row_of[u] = (int32_t)r;
   }

@@ -248,6 +248,18 @@ def test_powerlaw_construction_and_multiply(gcoo, cuda, oracle):
     assert np.array_equal(gcoo.spdm_gcoo(g, bm), oracle.spdm(go, bm, 64, True)[0])
 
 
+def test_powerlaw_host_pipeline_bit_exact(gcoo, cuda, oracle):
+    """Skewed rows through the pipelined host path: the plan spreads the
+    heaviest-first placement over extra, partly filled row blocks (narrow
+    strips still fill the GPU); C equals the oracle's FMA chain bit for bit."""
+    n = 4096
+    v, r, c = gcoo.generate_powerlaw_coo(n, 0.99, 1.0, 7)
+    g = gcoo.coo_to_gcoo(n, n, v, r, c, 4)
+    go = oracle.coo_to_gcoo(n, n, v, r, c, 4)
+    bm = oracle.uniform_sparse(n, 0.0, 13)[:, :2304].copy()
+    assert np.array_equal(gcoo.spdm_gcoo(g, bm), oracle.spdm(go, bm, 64, True)[0])
+
+
 def test_device_construction_paths(gcoo, cuda, oracle):
     import torch
     rng = np.random.default_rng(21)
