@@ -145,6 +145,9 @@ def time_kernel(G, dg, dB, dC, steps, warmup, stream, flush):
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         l0 = G.launch_count()
         G.kernel_timing(True)  # CUDA events around each multiply-kernel launch, same stream
+        # the device sleeps ~5 ms first so the host queues the timed steps ahead of it:
+        # per-step device times then never include host enqueue latency
+        torch.cuda._sleep(int(1e7))
         for i in range(steps):
             flush.zero_()  # > L2 (126 MB): every timed launch starts cold
             starts[i].record(stream)

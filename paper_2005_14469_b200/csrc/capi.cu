@@ -139,19 +139,36 @@ void ensure_pool_retains() {
 }
 
 // ------------------------------------------------------------ scan --------
-void exclusive_scan(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s) {
+// Scratch (int64 elements) exclusive_scan needs for n inputs: per level the
+// tile sums and their scan.
+int64_t scan_scratch(int64_t n) {
+  if (n == 0) return 0;
+  const int64_t tiles = ceil_div(n, kScanTile);
+  return tiles + (tiles + 1) + (tiles > 1 ? scan_scratch(tiles) : 0);
+}
+
+// out[0..n] = exclusive scan of in[0..n) plus the total in out[n]; kernels are
+// PDL-chained and use caller-provided scratch, so no allocation interrupts a
+// planner chain.
+void exclusive_scan(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s, int64_t* scratch) {
   if (n == 0) {
     GCOO_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), s));
     return;
   }
   const int64_t tiles = ceil_div(n, kScanTile);
-  DevBuf<int64_t> sums(tiles, s), sums_scan(tiles + 1, s);
-  GCOO_LAUNCH(scan_tiles_kernel, (unsigned)tiles, kScanThreads, 0, s, in, out, n, sums.get());
+  int64_t* sums = scratch;
+  int64_t* sums_scan = scratch + tiles;
+  GCOO_LAUNCH_PDL(scan_tiles_kernel, (unsigned)tiles, kScanThreads, 0, s, in, out, n, sums);
   if (tiles > 1) {
-    exclusive_scan(sums.get(), sums_scan.get(), tiles, s);
-    GCOO_LAUNCH(add_tile_offsets_kernel, (unsigned)ceil_div(n, 256), 256, 0, s, out, n, sums_scan.get());
+    exclusive_scan(sums, sums_scan, tiles, s, scratch + 2 * tiles + 1);
+    GCOO_LAUNCH_PDL(add_tile_offsets_kernel, (unsigned)ceil_div(n, 256), 256, 0, s, out, n, (const int64_t*)sums_scan);
   }
-  GCOO_LAUNCH(write_total_kernel, 1, 1, 0, s, in, out, n);
+  GCOO_LAUNCH_PDL(write_total_kernel, 1, 1, 0, s, in, out, n);
+}
+
+void exclusive_scan(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s) {
+  DevBuf<int64_t> scratch(scan_scratch(n), s);
+  exclusive_scan(in, out, n, s, scratch.get());
 }
 
 // ------------------------------------------------------------ spdm --------
@@ -285,56 +302,61 @@ void build_plan(SpdmPlan& P, const DevGcoo<float>& a, cudaStream_t s, int64_t mi
   P.nchunks = (int)ceil_div(a.k, Cfg::KC);
   const int nchunks = P.nchunks;
   const int64_t nseg = P.row_blocks * nchunks;
+  // every buffer first: the kernels below form one uninterrupted PDL chain
   DevBuf<uint32_t> cnt(units * nchunks * Cfg::RW, s);
-  GCOO_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
-  if constexpr (TACC) {
-    // load-balanced row placement: heaviest rows first, dealt over a block's warps
-    DevBuf<int32_t> row_nnz(a.m, s), hist(33, s), cursor(33, s);
-    GCOO_CUDA(cudaMemsetAsync(row_nnz.get(), 0, row_nnz.bytes(), s));
-    GCOO_CUDA(cudaMemsetAsync(hist.get(), 0, hist.bytes(), s));
-    GCOO_CUDA(cudaMemsetAsync(cursor.get(), 0, cursor.bytes(), s));
-    if (a.nnz > 0) GCOO_LAUNCH(row_nnz_kernel, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, row_nnz.get());
-    GCOO_LAUNCH(bucket_hist_kernel, grid_for(a.m, 256), 256, 0, s, a.m, row_nnz.get(), hist.get());
+  DevBuf<int32_t> row_nnz(TACC ? a.m : 0, s), hist(TACC ? 33 : 0, s), cursor(TACC ? 33 : 0, s);
+  if (TACC) {
     P.unit_of = DevBuf<int32_t>(a.m, s);
     P.row_of = DevBuf<int32_t>(P.row_blocks * Cfg::RB, s);
-    GCOO_CUDA(cudaMemsetAsync(P.row_of.get(), 0xff, P.row_of.bytes(), s));
-    GCOO_LAUNCH(row_balance_kernel, grid_for(a.m, 256), 256, 0, s, a.m, row_nnz.get(), hist.get(), cursor.get(),
-                (int32_t)Cfg::RB, (int32_t)Cfg::NW, (int32_t)Cfg::RW,
-                (int32_t)std::min<int64_t>(INT32_MAX, 4 * ceil_div(a.nnz, a.m) + 16), (int32_t)rpb, P.unit_of.get(),
-                P.row_of.get());
   }
-  if (a.nnz > 0) {
-    if constexpr (TACC)
-      GCOO_LAUNCH(tacc_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks, cnt.get(),
-                  P.unit_of.get());
-    else
-      GCOO_LAUNCH(tile_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks, cnt.get());
-  }
-  DevBuf<int64_t> seg_len(nseg, s);
+  DevBuf<int64_t> seg_len(nseg, s), scan_tmp(scan_scratch(nseg), s);
   P.seg_off = DevBuf<int64_t>(nseg + 1, s);
-  if constexpr (TACC)
-    GCOO_LAUNCH(tacc_size_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
-                seg_len.get());
-  else
-    GCOO_LAUNCH(tile_size_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
-                seg_len.get());
-  exclusive_scan(seg_len.get(), P.seg_off.get(), nseg, s);
   // upper bound of the stream: headers + one record (16 B) per entry
   const int64_t bound = nseg * (Cfg::TABLE + Cfg::NW * Cfg::HDR) + (int64_t)Cfg::REC * a.nnz + 16;
   P.ent = DevBuf<unsigned char>(bound, s);
   DevBuf<int64_t> slot_pos(nseg * Cfg::NW * Cfg::RW, s);
+
+  const int64_t init_n = std::max<int64_t>((int64_t)cnt.count, TACC ? std::max<int64_t>(a.m, (int64_t)P.row_of.count) : 0);
+  GCOO_LAUNCH_PDL(plan_init_kernel, grid_for(init_n, 256), 256, 0, s, cnt.get(), (int64_t)cnt.count,
+                  row_nnz.get(), TACC ? a.m : (int64_t)0, hist.get(), cursor.get(), P.row_of.get(),
+                  TACC ? (int64_t)P.row_of.count : (int64_t)0);
   if constexpr (TACC) {
-    GCOO_LAUNCH(tacc_header_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
-                P.seg_off.get(), P.ent.get(), slot_pos.get());
+    // load-balanced row placement: heaviest rows first, dealt over a block's warps
     if (a.nnz > 0)
-      GCOO_LAUNCH(tacc_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols,
-                  a.gidx, nchunks, slot_pos.get(), P.ent.get(), P.unit_of.get());
+      GCOO_LAUNCH_PDL(row_nnz_kernel, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, row_nnz.get());
+    GCOO_LAUNCH_PDL(bucket_hist_kernel, grid_for(a.m, 256), 256, 0, s, a.m, (const int32_t*)row_nnz.get(), hist.get());
+    GCOO_LAUNCH_PDL(row_balance_kernel, grid_for(a.m, 256), 256, 0, s, a.m, (const int32_t*)row_nnz.get(),
+                    (const int32_t*)hist.get(), cursor.get(), (int32_t)Cfg::RB, (int32_t)Cfg::NW, (int32_t)Cfg::RW,
+                    (int32_t)std::min<int64_t>(INT32_MAX, 4 * ceil_div(a.nnz, a.m) + 16), (int32_t)rpb,
+                    P.unit_of.get(), P.row_of.get());
+  }
+  if (a.nnz > 0) {
+    if constexpr (TACC)
+      GCOO_LAUNCH_PDL(tacc_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks,
+                      cnt.get(), (const int32_t*)P.unit_of.get());
+    else
+      GCOO_LAUNCH_PDL(tile_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks,
+                      cnt.get());
+  }
+  if constexpr (TACC)
+    GCOO_LAUNCH_PDL(tacc_size_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, (const uint32_t*)cnt.get(), units,
+                    nchunks, nseg, seg_len.get());
+  else
+    GCOO_LAUNCH_PDL(tile_size_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, (const uint32_t*)cnt.get(), units,
+                    nchunks, nseg, seg_len.get());
+  exclusive_scan(seg_len.get(), P.seg_off.get(), nseg, s, scan_tmp.get());
+  if constexpr (TACC) {
+    GCOO_LAUNCH_PDL(tacc_header_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, (const uint32_t*)cnt.get(), units,
+                    nchunks, nseg, (const int64_t*)P.seg_off.get(), P.ent.get(), slot_pos.get());
+    if (a.nnz > 0)
+      GCOO_LAUNCH_PDL(tacc_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols,
+                      a.gidx, nchunks, (const int64_t*)slot_pos.get(), P.ent.get(), (const int32_t*)P.unit_of.get());
   } else {
-    GCOO_LAUNCH(tile_header_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, cnt.get(), units, nchunks, nseg,
-                P.seg_off.get(), P.ent.get(), slot_pos.get());
+    GCOO_LAUNCH_PDL(tile_header_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, (const uint32_t*)cnt.get(), units,
+                    nchunks, nseg, (const int64_t*)P.seg_off.get(), P.ent.get(), slot_pos.get());
     if (a.nnz > 0)
-      GCOO_LAUNCH(tile_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols,
-                  a.gidx, nchunks, slot_pos.get(), P.ent.get());
+      GCOO_LAUNCH_PDL(tile_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols,
+                      a.gidx, nchunks, (const int64_t*)slot_pos.get(), P.ent.get());
   }
 }
 
@@ -346,11 +368,13 @@ void run_plan(const SpdmPlan& P, const DevGcoo<float>& a, int64_t n, const float
   if (grid > INT32_MAX) fail(GCOO_EINVAL, "spdm_gcoo: problem too large for one launch");
   const cudaEvent_t kt0 = kt_start(s);
   if constexpr (TACC)
-    GCOO_LAUNCH(spdm_tacc_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n, P.ent.get(),
-                P.seg_off.get(), C, ldc, P.row_blocks, P.nchunks, P.row_of.get());
+    GCOO_LAUNCH_PDL(spdm_tacc_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n,
+                    (const unsigned char*)P.ent.get(), (const int64_t*)P.seg_off.get(), C, ldc, P.row_blocks,
+                    P.nchunks, (const int32_t*)P.row_of.get());
   else
-    GCOO_LAUNCH(spdm_tile_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n, P.ent.get(),
-                P.seg_off.get(), C, ldc, P.row_blocks, P.nchunks);
+    GCOO_LAUNCH_PDL(spdm_tile_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n,
+                    (const unsigned char*)P.ent.get(), (const int64_t*)P.seg_off.get(), C, ldc, P.row_blocks,
+                    P.nchunks);
   kt_stop(s, kt0);
 }
 

@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -41,6 +42,34 @@ extern std::atomic<uint64_t> g_launches;
     ::gcoo_b200::check_cuda(cudaGetLastError(), #kernel);                    \
     ::gcoo_b200::g_launches.fetch_add(1, std::memory_order_relaxed);         \
   } while (0)
+
+// Programmatic dependent launch (PDL) for chains of small kernels on one
+// stream (the multiply's planner): the next kernel is launched while the
+// previous one drains, and waits in griddep_wait() for its predecessor's
+// completion and memory.  Every kernel launched this way must call
+// griddep_wait() before it touches memory an earlier kernel wrote.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(const char* name, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  static const bool pdl_off = std::getenv("GCOO_NO_PDL") != nullptr;  // A/B switch for measurements
+  cfg.numAttrs = pdl_off ? 0 : 1;
+  check_cuda(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...), name);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+#define GCOO_LAUNCH_PDL(kernel, grid, block, smem, stream, ...) \
+  ::gcoo_b200::launch_pdl(#kernel, kernel, (grid), (block), (smem), (stream), __VA_ARGS__)
 
 // Stream-ordered scratch buffer from the device's default memory pool (the
 // pool keeps freed blocks, so steady-state calls do not hit cudaMalloc).

@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "common.cuh"
+
 namespace gcoo_b200 {
 
 constexpr int kScanThreads = 512;
@@ -56,6 +58,7 @@ __device__ __forceinline__ int64_t block_exclusive_scan(int64_t x, int64_t& tota
 __global__ void __launch_bounds__(kScanThreads)
 scan_tiles_kernel(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t n,
                   int64_t* __restrict__ tile_sums) {
+  griddep_wait();  // PDL: predecessor complete
   const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
   int64_t v[kScanItems], s = 0;
 #pragma unroll
@@ -75,11 +78,13 @@ scan_tiles_kernel(const int64_t* __restrict__ in, int64_t* __restrict__ out, int
 
 __global__ void add_tile_offsets_kernel(int64_t* __restrict__ out, int64_t n,
                                         const int64_t* __restrict__ tile_off) {
+  griddep_wait();  // PDL: predecessor complete
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] += tile_off[i / kScanTile];
 }
 
 __global__ void write_total_kernel(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t n) {
+  griddep_wait();  // PDL: predecessor complete
   out[n] = n > 0 ? out[n - 1] + in[n - 1] : 0;
 }
 
@@ -329,6 +334,7 @@ __global__ void zero_uncovered_kernel(int64_t m, int64_t n, int32_t p, int32_t b
 // Entries per row; lanes holding the same row combine first (one atomic per
 // distinct row per warp: a dense power-law row is not 16K same-address atomics).
 __global__ void row_nnz_kernel(int64_t nnz, const int32_t* __restrict__ rows, int32_t* __restrict__ row_nnz) {
+  griddep_wait();  // PDL: predecessor complete
   const int lane = threadIdx.x & 31;
   for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~int64_t(31); base < nnz;
        base += (int64_t)gridDim.x * blockDim.x) {
@@ -337,6 +343,25 @@ __global__ void row_nnz_kernel(int64_t nnz, const int32_t* __restrict__ rows, in
     const int32_t r = valid ? rows[e] : -1;
     const unsigned same = __match_any_sync(0xffffffffu, r);
     if (valid && lane == __ffs(same) - 1) atomicAdd(&row_nnz[r], __popc(same));
+  }
+}
+
+// Planner scratch initialisation in one launch (replaces five memsets so the
+// planner's kernel chain stays programmatically dependent end to end).
+__global__ void plan_init_kernel(uint32_t* __restrict__ cnt, int64_t cnt_n, int32_t* __restrict__ row_nnz,
+                                 int64_t m, int32_t* __restrict__ hist, int32_t* __restrict__ cursor,
+                                 int32_t* __restrict__ row_of, int64_t row_of_n) {
+  griddep_wait();  // PDL: predecessor complete
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t i = t0; i < cnt_n; i += stride) cnt[i] = 0u;
+  if (row_nnz)
+    for (int64_t i = t0; i < m; i += stride) row_nnz[i] = 0;
+  if (row_of)
+    for (int64_t i = t0; i < row_of_n; i += stride) row_of[i] = -1;
+  if (hist && t0 < 33) {
+    hist[t0] = 0;
+    cursor[t0] = 0;
   }
 }
 
@@ -349,6 +374,7 @@ __device__ __forceinline__ int nnz_bucket(int32_t c) { return 31 - (c > 0 ? 31 -
 
 // hist[1..32]: rows per bucket; hist[0]: the largest row.
 __global__ void bucket_hist_kernel(int64_t m, const int32_t* __restrict__ row_nnz, int32_t* __restrict__ hist) {
+  griddep_wait();  // PDL: predecessor complete
   __shared__ int32_t h[33];
   if (threadIdx.x < 33) h[threadIdx.x] = 0;
   __syncthreads();
@@ -370,6 +396,7 @@ __global__ void row_balance_kernel(int64_t m, const int32_t* __restrict__ row_nn
                                    int32_t* __restrict__ cursor, int32_t rb_rows, int32_t nw, int32_t rw,
                                    int32_t skew, int32_t rpb, int32_t* __restrict__ unit_of,
                                    int32_t* __restrict__ row_of) {
+  griddep_wait();  // PDL: predecessor complete
   __shared__ int32_t off[33];
   if (threadIdx.x == 0) {
     int32_t acc = 0;

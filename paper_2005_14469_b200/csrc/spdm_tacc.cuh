@@ -38,6 +38,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "common.cuh"
+
 #include "ptx.cuh"
 
 namespace gcoo_b200 {
@@ -82,6 +84,7 @@ using TaccV4W = TaccCfg<4, 192, 2, 16384, 24>;  // W=128, RB=480, 24 consumer wa
 template <class Cfg>
 __global__ void tacc_count_kernel(int64_t nnz, const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
                                   int nchunks, uint32_t* __restrict__ cnt, const int32_t* __restrict__ unit_of) {
+  griddep_wait();  // PDL: predecessor complete
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
     const int32_t r = unit_of[rows[e]];
     const int32_t c = cols[e] / Cfg::KC;
@@ -104,6 +107,7 @@ __device__ __forceinline__ uint32_t tacc_warp_records(const uint32_t* __restrict
 template <class Cfg>
 __global__ void tacc_size_kernel(const uint32_t* __restrict__ cnt, int64_t units, int nchunks, int64_t nseg,
                                  int64_t* __restrict__ seg_len) {
+  griddep_wait();  // PDL: predecessor complete
   const int lane = threadIdx.x & 31;
   for (int64_t x = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < nseg;
        x += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -125,6 +129,7 @@ template <class Cfg>
 __global__ void tacc_header_kernel(const uint32_t* __restrict__ cnt, int64_t units, int nchunks, int64_t nseg,
                                    const int64_t* __restrict__ seg_off, unsigned char* __restrict__ ent,
                                    int64_t* __restrict__ slot_pos) {
+  griddep_wait();  // PDL: predecessor complete
   const int lane = threadIdx.x & 31;
   for (int64_t x = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < nseg;
        x += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -167,6 +172,7 @@ __global__ void tacc_fill_kernel(int64_t nnz, int32_t p, const float* __restrict
                                  const int64_t* __restrict__ gidx, int nchunks,
                                  const int64_t* __restrict__ slot_pos, unsigned char* __restrict__ ent,
                                  const int32_t* __restrict__ unit_of) {
+  griddep_wait();  // PDL: predecessor complete
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
     const int32_t r = rows[e], col = cols[e];
     const int c = col / Cfg::KC;
@@ -300,6 +306,7 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
   __syncthreads();
   tmem_fence_after();
   const uint32_t tbase = *tmem_slot;
+  griddep_wait();  // PDL: the planner's record stream is complete
 
   if (warp == NW) {
     // ------------- producer: B tile (TMA 2-D) + record segment (bulk 1-D)

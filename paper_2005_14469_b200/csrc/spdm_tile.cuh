@@ -38,6 +38,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "common.cuh"
+
 #include "ptx.cuh"
 
 namespace gcoo_b200 {
@@ -73,6 +75,7 @@ using TileV4 = TileCfg<4, 48, 5, 16384>;    // W=128, RB=240 : density >~ 3%
 template <class Cfg>
 __global__ void tile_count_kernel(int64_t nnz, const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
                                   int nchunks, uint32_t* __restrict__ cnt) {
+  griddep_wait();  // PDL: predecessor complete
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
     const int32_t r = rows[e];
     const int32_t c = cols[e] / Cfg::KC;
@@ -95,6 +98,7 @@ __device__ __forceinline__ uint32_t tile_warp_records(const uint32_t* __restrict
 template <class Cfg>
 __global__ void tile_size_kernel(const uint32_t* __restrict__ cnt, int64_t units, int nchunks, int64_t nseg,
                                  int64_t* __restrict__ seg_len) {
+  griddep_wait();  // PDL: predecessor complete
   const int lane = threadIdx.x & 31;
   for (int64_t x = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < nseg;
        x += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -116,6 +120,7 @@ template <class Cfg>
 __global__ void tile_header_kernel(const uint32_t* __restrict__ cnt, int64_t units, int nchunks, int64_t nseg,
                                    const int64_t* __restrict__ seg_off, unsigned char* __restrict__ ent,
                                    int64_t* __restrict__ slot_pos) {
+  griddep_wait();  // PDL: predecessor complete
   const int lane = threadIdx.x & 31;
   for (int64_t x = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < nseg;
        x += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -161,6 +166,7 @@ __global__ void tile_fill_kernel(int64_t nnz, int32_t p, const float* __restrict
                                  const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
                                  const int64_t* __restrict__ gidx, int nchunks,
                                  const int64_t* __restrict__ slot_pos, unsigned char* __restrict__ ent) {
+  griddep_wait();  // PDL: predecessor complete
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
     const int32_t r = rows[e], col = cols[e];
     const int c = col / Cfg::KC;
@@ -260,6 +266,7 @@ spdm_tile_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
     fence_barrier_init();
   }
   __syncthreads();
+  griddep_wait();  // PDL: the planner's record stream is complete
 
   if (warp == NW) {
     // ------------- producer: B tile (TMA 2-D) + record segment (bulk 1-D)
