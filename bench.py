@@ -116,6 +116,21 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def pcie_roofline(nbytes, seconds):
+    """The host-pointer path is PCIe-bound: its bytes per second against the
+    measured concurrent H2D+D2H bandwidth of this pool's B200 host link
+    (tools/pcie_probe.py -> profiles/r01_pcie_probe.jsonl)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_pcie_probe.jsonl")) as f:
+            rows = [json.loads(x) for x in f if x.strip()]
+        peak = max(r["gb_s"] for r in rows if r["probe"].startswith("h2d+d2h"))
+    except Exception:  # noqa: BLE001
+        return {}
+    ach = nbytes / seconds / 1e9
+    return {"pcie_gb_s": round(ach, 1), "pcie_peak_gb_s": peak, "pcie_frac": round(ach / peak, 3),
+            "pcie_peak_source": "measured concurrent H2D+D2H (profiles/r01_pcie_probe.jsonl)"}
+
+
 def make_inputs(G, n, s, seed, dev, n_cols):
     """square_benchmark inputs; B/C column block of width n_cols (same B for
     every rank's block: B is generated once at n x n and tiled)."""
@@ -290,7 +305,25 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(g_host, b_host, n)
 
+    gather = None
     if world > 1:
+        # the optional C gather onto rank 0 (NCCL point to point), timed on its own —
+        # not part of the multiply step
+        from paper_2005_14469_b200.shard import gather_columns
+        shards = [(r * n, (r + 1) * n) for r in range(world)]
+        dist.barrier()
+        torch.cuda.synchronize()
+        g0 = time.perf_counter()
+        full = gather_columns(dC if backend == "nccl" else dC.cpu(), shards, root=0)
+        torch.cuda.synchronize()
+        gt = torch.tensor([time.perf_counter() - g0], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+        gather = {"ms": round(float(gt[0]) * 1e3, 3), "bytes_to_root": int(m * n * 4 * (world - 1)),
+                  "collective": f"{backend} point-to-point onto rank 0"}
+        if full is not None:
+            ok = bool(torch.equal(full[:, :n].to(dC.device), dC))
+            gather["rank0_block_intact"] = ok
+        del full
         dist.barrier()
         dist.destroy_process_group()
     if rank != 0:
@@ -317,8 +350,10 @@ def run_ours(args):
                    "l2": "flushed (256 MiB write) before every timed launch; B+C = 512 MB > L2"},
         "e2e": {"value": round(e2e_value, 2), "unit": "GFLOPS", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_s * 1e3, 3),
-                "path": "paper_2005_14469_b200.spdm_gcoo -> gcoo_spdm_f32 (pinned host buffers)"},
+                "path": "paper_2005_14469_b200.spdm_gcoo -> gcoo_spdm_f32 (pinned host buffers)",
+                **pcie_roofline(h2d + d2h, e2e_s)},
         "gpu_launches": int(launches),
+        "c_gather": gather,
         "roofline": {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved_gbs / hbm_peak, 4), "traffic": traffic,
                      "peak_source": hbm_src, "algorithmic_bytes_per_launch": int(cb),

@@ -42,30 +42,33 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= t for f in _inputs())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """out/defines: variant builds for measurements (e.g. ablations), never the product."""
+    if out is None and not force and up_to_date():
         return LIB
+    lib_path = out or LIB
     os.makedirs(LIB_DIR, exist_ok=True)
     cmd = [
         _nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
         "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v", "-shared",
         "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-        "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES],
+        *["-D" + d for d in defines],
+        "-o", lib_path + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES],
     ]
     # nvcc picks the host compiler from PATH; make sure it is the system gcc
     env = dict(os.environ)
     env.pop("CXX", None)
     env.pop("CC", None)
-    out = subprocess.run(cmd, capture_output=True, text=True, env=env)
-    log = os.path.join(LIB_DIR, "build.log")
+    res = subprocess.run(cmd, capture_output=True, text=True, env=env)
+    log = lib_path + ".log" if out else os.path.join(LIB_DIR, "build.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + out.stdout + out.stderr)
-    if out.returncode != 0:
-        raise RuntimeError("nvcc failed (see %s):\n%s" % (log, out.stderr[-4000:]))
-    os.replace(LIB + ".tmp", LIB)
+        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed (see %s):\n%s" % (log, res.stderr[-4000:]))
+    os.replace(lib_path + ".tmp", lib_path)
     if verbose:
-        print(out.stderr)
-    return LIB
+        print(res.stderr)
+    return lib_path
 
 
 if __name__ == "__main__":

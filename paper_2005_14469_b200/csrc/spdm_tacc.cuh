@@ -212,8 +212,16 @@ struct RecSrc<true> {  // segment larger than a stage: read from global memory
   static __device__ __forceinline__ uint32_t ld32(addr_t a) { return __ldg(reinterpret_cast<const uint32_t*>(a)); }
 };
 
+#ifndef GCOO_ABL
+#define GCOO_ABL 0  // ablation builds (tools/ablate.sh, wrong results): 1 no TMEM swap, 2 no B loads, 3 both
+#endif
+
 template <class Cfg>
 __device__ __forceinline__ void tacc_switch(float (&acc)[Cfg::V], uint32_t& cur, uint32_t tacc, uint32_t s) {
+  if ((GCOO_ABL & 1) && s != cur) {
+    cur = s;
+    return;
+  }
   if (s != cur) {  // warp-uniform: swap the slot's accumulators through TMEM
     if (cur != ~0u) tmem_st<Cfg::V>(tacc + cur * Cfg::V, acc);
     tmem_ld<Cfg::V>(tacc + s * Cfg::V, acc);
@@ -249,12 +257,22 @@ __device__ __forceinline__ void tacc_consume(float (&acc)[Cfg::V], uint32_t& cur
     uint4 qb = make_uint4(0u, 0u, 0u, ~0u);
     if (hasB) qb = Src::ld(rec + Cfg::REC);
     float ba0[V], ba1[V], bb0[V], bb1[V];
-    lds_vec<V>(bbase + (qa.z & 0xffffffu), ba0);
     const bool a2 = qa.w != ~0u;
-    if (a2) lds_vec<V>(bbase + qa.w, ba1);
-    if (hasB) lds_vec<V>(bbase + (qb.z & 0xffffffu), bb0);
     const bool b2 = qb.w != ~0u;
-    if (b2) lds_vec<V>(bbase + qb.w, bb1);
+    if constexpr (GCOO_ABL & 2) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        ba0[v] = __uint_as_float(qa.z + v);
+        ba1[v] = __uint_as_float(qa.w + v);
+        bb0[v] = __uint_as_float(qb.z + v);
+        bb1[v] = __uint_as_float(qb.w + v);
+      }
+    } else {
+      lds_vec<V>(bbase + (qa.z & 0xffffffu), ba0);
+      if (a2) lds_vec<V>(bbase + qa.w, ba1);
+      if (hasB) lds_vec<V>(bbase + (qb.z & 0xffffffu), bb0);
+      if (b2) lds_vec<V>(bbase + qb.w, bb1);
+    }
     tacc_switch<Cfg>(acc, cur, tacc, qa.z >> 24);
     tacc_fma<V>(acc, __uint_as_float(qa.x), ba0);
     if (a2) tacc_fma<V>(acc, __uint_as_float(qa.y), ba1);

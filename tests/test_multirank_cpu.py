@@ -15,7 +15,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2005_14469_b200.shard import column_shards, weak_block
+from paper_2005_14469_b200.shard import column_shards, gather_columns, weak_block
 
 
 def test_column_shards_partition():
@@ -53,12 +53,17 @@ def _worker(rank, world, port, q):
         c_loc, _ = O.spdm(g, np.ascontiguousarray(b[:, lo:hi]), 64, fma=True)
         parts = [None] * world
         dist.all_gather_object(parts, (lo, hi, c_loc))
+        # the optional C gather (point to point onto rank 0) reassembles the same bits
+        gathered = gather_columns(torch.from_numpy(c_loc), column_shards(n, world), root=0)
         t = torch.tensor([1.0 + rank], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         if rank == 0:
             full, _ = O.spdm(g, b, 64, fma=True)
             c = np.concatenate([p[2] for p in sorted(parts, key=lambda x: x[0])], axis=1)
-            q.put((bool(np.array_equal(c, full)), float(t.item())))
+            q.put((bool(np.array_equal(c, full)) and bool(np.array_equal(gathered.numpy(), full)),
+                   float(t.item())))
+        else:
+            assert gathered is None
     finally:
         dist.destroy_process_group()
 
