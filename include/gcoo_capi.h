@@ -116,6 +116,39 @@ int gcoo_stats_dev(int64_t m, int64_t n, int32_t p, int32_t b, int64_t nnz,
                    const int32_t* row_idx, const int32_t* col_idx, int64_t groups,
                    const int64_t* g_idxes, gcoo_stats* stats, void* stream);
 
+/* ------------------------------------------------- traffic model -------- */
+/* TrafficReport / TrafficDetail (traffic.hpp:31-56), same field order. */
+typedef struct gcoo_traffic {
+  uint64_t n_dm;
+  uint64_t n_l2;
+  uint64_t n_shm;
+  uint64_t tex_l1_trans;
+  uint64_t flops;
+} gcoo_traffic;
+typedef struct gcoo_traffic_detail {
+  uint64_t b_element_loads;
+  uint64_t b_element_reused;
+  uint64_t staged_entries;
+  uint64_t b_load_transactions;
+  uint64_t sparse_transactions;
+  uint64_t store_transactions;
+} gcoo_traffic_detail;
+#define GCOO_CACHE_COLD 0        /* CacheMode::cold */
+#define GCOO_CACHE_INFINITE_L2 1 /* CacheMode::infinite_l2 */
+#define GCOO_MODEL_GCOO 0        /* model_gcoo_traffic (traffic.cpp:43-137) */
+#define GCOO_MODEL_CSR 1         /* model_csr_traffic  (traffic.cpp:140-197) */
+/*
+ * The reference's analytical traffic model of an m x k pattern times a dense
+ * k x n operand under cfg (p, b), evaluated on the device.  The pattern is
+ * given as A's GCOO arrays (device pointers, grouped with this p — run
+ * coo_to_gcoo first for an arbitrary coordinate list); counts are exact and
+ * equal the reference's.  `det` may be NULL.  Synchronises `stream`.
+ */
+int gcoo_model_traffic_dev(int kind, int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, int64_t nnz,
+                           const int32_t* row_idx, const int32_t* col_idx, int64_t groups, const int64_t* g_idxes,
+                           const int64_t* nnz_per_group, int cache_mode, gcoo_traffic* rep,
+                           gcoo_traffic_detail* det, void* stream);
+
 /* ------------------------------------------------------ construction ---- */
 /*
  * coo_to_gcoo (matrix.hpp:366-405).  Input: row-major COO, validated exactly

@@ -220,6 +220,21 @@ class Reference:
         L.ref_time_spdm_gcoo_f32.argtypes = [_i64, _i64, _i64, _i32, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp,
                                              _vp, C.c_int, C.c_int, C.c_int, _vp]
 
+    TRAFFIC_FIELDS = ("n_dm", "n_l2", "n_shm", "tex_l1_trans", "flops", "b_element_loads", "b_element_reused",
+                      "staged_entries", "b_load_transactions", "sparse_transactions", "store_transactions")
+
+    def model_traffic(self, rows, cols, m, k, n, p=4, b=64, infinite_l2=False, csr=False):
+        """The reference's model_gcoo_traffic / model_csr_traffic -> dict of the 11 counters."""
+        L = self.lib
+        L.ref_model_traffic.restype = C.c_int
+        L.ref_model_traffic.argtypes = [C.c_int, _i64, _vp, _vp, _i64, _i64, _i64, _i32, _i32, C.c_int, _vp]
+        r = np.ascontiguousarray(rows, dtype=np.int32)
+        c = np.ascontiguousarray(cols, dtype=np.int32)
+        out = np.zeros(11, np.uint64)
+        self._check(L.ref_model_traffic(1 if csr else 0, r.size, r.ctypes.data, c.ctypes.data, m, k, n, p, b,
+                                        1 if infinite_l2 else 0, out.ctypes.data))
+        return dict(zip(self.TRAFFIC_FIELDS, (int(x) for x in out)))
+
     def _check(self, rc: int):
         if rc == 1:
             raise ValueError(self.lib.ref_last_error().decode())
@@ -292,3 +307,100 @@ class Reference:
 
 def have_reference() -> bool:
     return os.path.exists(REF_SO) and os.path.exists(REF_FMA_SO)
+
+
+# --------------------------------------------------------- traffic model --
+def _trans(elems: int) -> int:
+    """traffic.cpp:16-18 — 32-element coalesced transactions."""
+    return -(-elems // 32)
+
+
+def model_traffic(rows, cols, m, k, n, p=4, b=64, infinite_l2=False, csr=False) -> dict:
+    """Plain-Python restatement of model_gcoo_traffic (traffic.cpp:43-137) and
+    model_csr_traffic (:140-197): the same loops over groups/rows, strips and
+    runs, for small patterns (the checker of the device model)."""
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    rep = dict(n_dm=0, n_l2=0, n_shm=0, tex_l1_trans=0, flops=0)
+    det = dict(b_element_loads=0, b_element_reused=0, staged_entries=0, b_load_transactions=0,
+               sparse_transactions=0, store_transactions=0)
+    if csr:
+        segs = -(-n // 32)
+        touched = set()
+        rep["n_dm"] += _trans(m + 1)                      # :162-163
+        det["sparse_transactions"] += _trans(m + 1)
+        by_row = [[] for _ in range(m)]
+        for r, c in zip(rows.tolist(), cols.tolist()):
+            by_row[r].append(c)
+        for r in range(m):
+            cs = sorted(by_row[r])
+            if cs:                                        # :168-173
+                sp = _trans(2 * len(cs))
+                det["sparse_transactions"] += sp
+                rep["n_dm"] += sp
+            for c in cs:                                  # :175-191
+                det["b_element_loads"] += n
+                det["b_load_transactions"] += segs
+                if infinite_l2:
+                    for s_ in range(segs):
+                        if (c, s_) in touched:
+                            rep["n_l2"] += 1
+                        else:
+                            rep["n_dm"] += 1
+                            touched.add((c, s_))
+                else:
+                    rep["n_dm"] += segs
+            rep["n_dm"] += segs                           # :194-196
+            det["store_transactions"] += segs
+            rep["flops"] += 2 * len(cs) * n
+        return {**rep, **det}
+    groups = -(-m // p)
+    strips = -(-n // b)
+    gcols = [[] for _ in range(groups)]
+    for r, c in zip(rows.tolist(), cols.tolist()):
+        gcols[r // p].append(c)
+    touched = set()
+    for gi in range(groups):
+        cs = sorted(gcols[gi])
+        nnz_g = len(cs)
+        h = min(p, m - gi * p)
+        runs = []                                         # :81-91 runs never cross a chunk of b entries
+        for chunk in range(0, nnz_g, b):
+            blk = cs[chunk:chunk + b]
+            e = 0
+            while e < len(blk):
+                ln = 1
+                while e + ln < len(blk) and blk[e + ln] == blk[e]:
+                    ln += 1
+                runs.append((blk[e], ln))
+                e += ln
+        for sj in range(strips):
+            w = min(b, n - sj * b)
+            if nnz_g > 0:                                 # :96-108
+                rep["n_shm"] += 2 * nnz_g
+                det["staged_entries"] += nnz_g
+                sp = _trans(3 * nnz_g)
+                det["sparse_transactions"] += sp
+                if infinite_l2 and sj > 0:
+                    rep["n_l2"] += sp
+                else:
+                    rep["n_dm"] += sp
+            for col, ln in runs:                          # :111-128
+                bt = _trans(w)
+                det["b_load_transactions"] += bt
+                det["b_element_loads"] += w
+                det["b_element_reused"] += (ln - 1) * w
+                rep["tex_l1_trans"] += (ln - 1) * w
+                if infinite_l2:
+                    if (col, sj) in touched:
+                        rep["n_l2"] += bt
+                    else:
+                        rep["n_dm"] += bt
+                        touched.add((col, sj))
+                else:
+                    rep["n_dm"] += bt
+            st = _trans(h * w)                            # :131-133
+            det["store_transactions"] += st
+            rep["n_dm"] += st
+            rep["flops"] += 2 * nnz_g * w
+    return {**rep, **det}

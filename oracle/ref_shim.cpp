@@ -21,6 +21,7 @@
 #include "gcoo/io.hpp"
 #include "gcoo/kernels.hpp"
 #include "gcoo/matrix.hpp"
+#include "gcoo/traffic.hpp"
 
 using namespace gcoo;
 
@@ -237,6 +238,29 @@ int ref_time_spdm_gcoo_f32(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b
     (void)keep;
     out[0] = median(ts);
     out[1] = resolve_workers(workers);
+  });
+}
+
+// model_gcoo_traffic / model_csr_traffic (traffic.cpp:43-197) on a coordinate
+// pattern; out = {n_dm, n_l2, n_shm, tex_l1_trans, flops, b_element_loads,
+// b_element_reused, staged_entries, b_load_transactions, sparse_transactions,
+// store_transactions}.
+int ref_model_traffic(int csr, int64_t nnz, const int32_t* rows, const int32_t* cols, int64_t m, int64_t k,
+                      int64_t n, int32_t p, int32_t b, int infinite_l2, uint64_t* out) {
+  return guarded([&] {
+    std::vector<Coord> pat(static_cast<size_t>(nnz));
+    for (int64_t e = 0; e < nnz; ++e) pat[static_cast<size_t>(e)] = Coord{rows[e], cols[e]};
+    ExecConfig cfg;
+    cfg.p = p;
+    cfg.b = b;
+    const CacheMode mode = infinite_l2 ? CacheMode::infinite_l2 : CacheMode::cold;
+    TrafficDetail det;
+    const TrafficReport r = csr ? model_csr_traffic(pat, m, k, n, cfg, mode, &det)
+                                : model_gcoo_traffic(pat, m, k, n, cfg, mode, &det);
+    const uint64_t v[11] = {r.n_dm, r.n_l2, r.n_shm, r.tex_l1_trans, r.flops, det.b_element_loads,
+                            det.b_element_reused, det.staged_entries, det.b_load_transactions,
+                            det.sparse_transactions, det.store_transactions};
+    std::memcpy(out, v, sizeof v);
   });
 }
 

@@ -83,6 +83,8 @@ def lib():
     _sig(L, "gcoo_spdm_f32_dev", _int, dev_args)
     _sig(L, "gcoo_spdm_f64_dev", _int, dev_args)
     _sig(L, "gcoo_stats_dev", _int, [_i64, _i64, _i32, _i32, _i64, _vp, _vp, _i64, _vp, C.POINTER(_Stats), _vp])
+    _sig(L, "gcoo_model_traffic_dev", _int, [_int, _i64, _i64, _i64, _i32, _i32, _i64, _vp, _vp, _i64, _vp, _vp,
+                                              _int, C.POINTER(_Traffic), C.POINTER(_TrafficDetail), _vp])
     coo_args = [_i64, _i64, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
     _sig(L, "gcoo_coo_to_gcoo_f32", _int, coo_args)
     _sig(L, "gcoo_coo_to_gcoo_f64", _int, coo_args)
@@ -423,6 +425,61 @@ class DeviceGcoo:
         h = lambda x: x.cpu().numpy()
         return GcooMatrix(self.rows_dim, self.cols_dim, self.p, h(self.values), h(self.row_idx),
                           h(self.col_idx), h(self.g_idxes), h(self.nnz_per_group))
+
+
+class _Traffic(C.Structure):
+    _fields_ = [(f, _u64) for f in ("n_dm", "n_l2", "n_shm", "tex_l1_trans", "flops")]
+
+
+class _TrafficDetail(C.Structure):
+    _fields_ = [(f, _u64) for f in ("b_element_loads", "b_element_reused", "staged_entries",
+                                     "b_load_transactions", "sparse_transactions", "store_transactions")]
+
+
+def model_traffic_dev(a: "DeviceGcoo", n: int, cfg: Optional["ExecConfig"] = None, infinite_l2: bool = False,
+                      csr: bool = False, stream=None) -> dict:
+    """The reference's model_gcoo_traffic (csr=False) / model_csr_traffic
+    (csr=True) (traffic.cpp:43-197) of A's pattern times a dense k x n
+    operand, evaluated on the GPU: TrafficReport + TrafficDetail counters as
+    one dict (exact, equal to the reference's).  cfg.p must be A's p."""
+    cfg = cfg or ExecConfig(p=a.p)
+    if cfg.p != a.p:
+        raise ValueError("traffic model: matrix grouped with a different p")
+    r, d = _Traffic(), _TrafficDetail()
+    _check(lib().gcoo_model_traffic_dev(1 if csr else 0, a.rows_dim, a.cols_dim, n, a.p, cfg.b, a.nnz(),
+                                         _p(a.row_idx), _p(a.col_idx), a.groups(), _p(a.g_idxes),
+                                         _p(a.nnz_per_group), 1 if infinite_l2 else 0, C.byref(r), C.byref(d),
+                                         _stream_ptr(stream)))
+    return {**{f: int(getattr(r, f)) for f, _ in _Traffic._fields_},
+            **{f: int(getattr(d, f)) for f, _ in _TrafficDetail._fields_}}
+
+
+# RooflineModel profiles (traffic.cpp:226-233) plus this pool's B200, measured:
+# FP32 FFMA peak (tools/microbench, profiles/r01_microbench.json) and HBM copy
+# bandwidth (MEASURED_PEAKS.json).
+ROOFLINE_PROFILES = {
+    "gtx980": (4.981e12, 224e9),
+    "titanx": (10.97e12, 433e9),
+    "p100": (9.5e12, 732e9),
+    "b200": (72.47e12, 6547.8e9),
+}
+
+
+def operational_intensity(rep: dict, bytes_per_transaction: int = 128) -> float:
+    """operational_intensity (traffic.cpp:201-208): flops per DRAM byte."""
+    if rep["flops"] == 0:
+        return 0.0
+    if rep["n_dm"] == 0 or bytes_per_transaction <= 0:
+        raise ValueError("operational_intensity: undefined without DRAM traffic")
+    return rep["flops"] / (rep["n_dm"] * bytes_per_transaction)
+
+
+def roofline_throughput(r: float, profile: str = "b200") -> float:
+    """roofline_throughput (traffic.cpp:210-213): min(peak, r * bandwidth), FLOP/s."""
+    if r < 0:
+        raise ValueError("roofline_throughput: negative intensity")
+    peak, bw = ROOFLINE_PROFILES[profile.lower()]
+    return min(peak, r * bw)
 
 
 def _stream_ptr(stream) -> Optional[int]:

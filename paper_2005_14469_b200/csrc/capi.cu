@@ -1032,6 +1032,83 @@ int gcoo_stats_dev(int64_t m, int64_t n, int32_t p, int32_t b, int64_t nnz, cons
   });
 }
 
+// model_gcoo_traffic / model_csr_traffic (traffic.cpp:43-197) on the device:
+// four pattern statistics (construct.cuh, traffic_*_kernel) and the model's
+// closed form.  With S strips of b columns (last w_l), T = sum_sj trans(w_sj):
+//   gcoo  n_shm = 2 nnz S; sparse = SP*S (cold) or SP + SP*(S-1) in L2;
+//         B runs R*T, of which D*T first touches (infinite_l2); reused = (nnz-R)*n;
+//         stores = sum_g sum_sj trans(h_g w_sj); flops = 2 nnz n.
+//   csr   rowptr trans(m+1) + SC; B nnz*segs (D*segs first touches); stores m*segs.
+int gcoo_model_traffic_dev(int kind, int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, int64_t nnz,
+                           const int32_t* row_idx, const int32_t* col_idx, int64_t groups, const int64_t* g_idxes,
+                           const int64_t* nnz_per_group, int cache_mode, gcoo_traffic* rep,
+                           gcoo_traffic_detail* det, void* stream) {
+  return guarded([&] {
+    if (!is_pow2(p) || !is_pow2(b)) einval("ExecConfig: p and b must be powers of two");
+    if (m < 1 || k < 1 || n < 1) einval("traffic model: dimensions must be >= 1");
+    if (groups != ceil_div(m, p)) einval("traffic model: group arrays do not match ceil(m/p)");
+    if (kind != 0 && kind != 1) einval("traffic model: kind must be 0 (gcoo) or 1 (csr)");
+    if (!rep) einval("traffic model: report pointer is null");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DevBuf<unsigned long long> cnt(4, s);
+    DevBuf<unsigned char> flag(k, s);
+    DevBuf<int32_t> row_nnz(kind == 1 ? m : 0, s);
+    GCOO_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
+    GCOO_CUDA(cudaMemsetAsync(flag.get(), 0, flag.bytes(), s));
+    if (nnz > 0)
+      GCOO_LAUNCH(traffic_entries_kernel, grid_for(nnz, 256), 256, 0, s, nnz, p, b, groups, row_idx, col_idx,
+                  g_idxes, flag.get(), cnt.get());
+    GCOO_LAUNCH(count_flags_kernel, grid_for(k, 256), 256, 0, s, k, (const unsigned char*)flag.get(), cnt.get() + 1);
+    GCOO_LAUNCH(traffic_trans_sum_kernel<int64_t>, grid_for(groups, 256), 256, 0, s, groups, nnz_per_group,
+                (int64_t)3, cnt.get() + 2);
+    if (kind == 1) {
+      GCOO_CUDA(cudaMemsetAsync(row_nnz.get(), 0, row_nnz.bytes(), s));
+      if (nnz > 0) GCOO_LAUNCH(row_nnz_kernel, grid_for(nnz, 256), 256, 0, s, nnz, row_idx, row_nnz.get());
+      GCOO_LAUNCH(traffic_trans_sum_kernel<int32_t>, grid_for(m, 256), 256, 0, s, m,
+                  (const int32_t*)row_nnz.get(), (int64_t)2, cnt.get() + 3);
+    }
+    unsigned long long h[4] = {};
+    d2h(h, cnt.get(), 4, s);
+    GCOO_CUDA(cudaStreamSynchronize(s));
+    const uint64_t R = h[0], D = h[1], SP = h[2], SC = h[3], N = (uint64_t)nnz, un = (uint64_t)n;
+    auto tr = [](uint64_t e) { return (e + 31) / 32; };
+    gcoo_traffic r{};
+    gcoo_traffic_detail d{};
+    const bool inf = cache_mode != 0;
+    if (kind == 0) {
+      const uint64_t S = (uint64_t)ceil_div(n, b), wl = un - (S - 1) * (uint64_t)b;
+      const uint64_t T = (S - 1) * tr((uint64_t)b) + tr(wl);
+      const uint64_t G = (uint64_t)groups, hl = (uint64_t)m - (G - 1) * (uint64_t)p;
+      auto strip_stores = [&](uint64_t hh) { return (S - 1) * tr(hh * (uint64_t)b) + tr(hh * wl); };
+      r.n_shm = 2 * N * S;
+      d.staged_entries = N * S;
+      d.sparse_transactions = SP * S;
+      d.b_load_transactions = R * T;
+      d.b_element_loads = R * un;
+      d.b_element_reused = (N - R) * un;
+      r.tex_l1_trans = (N - R) * un;
+      d.store_transactions = (G - 1) * strip_stores((uint64_t)p) + strip_stores(hl);
+      if (inf) {
+        r.n_dm = SP + D * T + d.store_transactions;
+        r.n_l2 = SP * (S - 1) + (R - D) * T;
+      } else {
+        r.n_dm = SP * S + R * T + d.store_transactions;
+      }
+    } else {
+      const uint64_t segs = (uint64_t)ceil_div(n, 32), M = (uint64_t)m;
+      d.sparse_transactions = tr(M + 1) + SC;
+      d.b_element_loads = N * un;
+      d.b_load_transactions = N * segs;
+      d.store_transactions = M * segs;
+      r.n_dm = tr(M + 1) + SC + (inf ? D * segs : N * segs) + M * segs;
+      r.n_l2 = inf ? (N - D) * segs : 0;
+    }
+    r.flops = 2 * N * un;
+    *rep = r;
+    if (det) *det = d;
+  });
+}
+
 int gcoo_coo_to_gcoo_f32(int64_t m, int64_t k, int32_t p, int64_t nnz, const float* values, const int32_t* row_idx,
                          const int32_t* col_idx, float* out_values, int32_t* out_row_idx, int32_t* out_col_idx,
                          int64_t* g_idxes, int64_t* nnz_per_group) {

@@ -429,3 +429,62 @@ __global__ void row_balance_kernel(int64_t m, const int32_t* __restrict__ row_nn
 }
 
 }  // namespace gcoo_b200
+
+namespace gcoo_b200 {
+
+// ------------------------------------------------------- traffic model --
+// Device evaluation of the reference's analytical traffic model
+// (traffic.cpp:43-197).  Every counter of model_gcoo_traffic /
+// model_csr_traffic is a closed form of four pattern statistics, gathered
+// here in one pass over the GCOO arrays (capi.cu assembles the reports):
+//   cnt[0] runs R: entries that start a run inside a chunk of b entries of
+//          their group's (col,row)-sorted slice (traffic.cpp:81-91)
+//   cnt[1] distinct columns D (first touches of (col, strip) in infinite_l2)
+//   cnt[2] sum over non-empty groups of trans(3 * nnz_g)  (:101)
+//   cnt[3] sum over non-empty rows of trans(2 * nnz_r)    (:170)
+__global__ void traffic_entries_kernel(int64_t nnz, int32_t p, int32_t b, int64_t groups,
+                                       const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
+                                       const int64_t* __restrict__ gidx, unsigned char* __restrict__ col_flag,
+                                       unsigned long long* __restrict__ cnt) {
+  unsigned long long runs = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = (int64_t)rows[i] / p;
+    const int32_t c = cols[i];
+    col_flag[c] = 1;
+    if (g < 0 || g >= groups) continue;
+    const int64_t e = i - gidx[g];
+    if ((e & (b - 1)) == 0 || c != cols[i - 1]) ++runs;
+  }
+#pragma unroll
+  for (int d = 16; d; d >>= 1) runs += __shfl_xor_sync(0xffffffffu, runs, d);
+  if ((threadIdx.x & 31) == 0 && runs) atomicAdd(&cnt[0], runs);
+}
+
+// sum over i < count of [v_i > 0] * ceil(mult * v_i / 32) into *out
+template <typename V>
+__global__ void traffic_trans_sum_kernel(int64_t count, const V* __restrict__ v, int64_t mult,
+                                         unsigned long long* __restrict__ out) {
+  unsigned long long acc = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = (int64_t)v[i];
+    if (x > 0) acc += (unsigned long long)((mult * x + 31) / 32);
+  }
+#pragma unroll
+  for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+__global__ void count_flags_kernel(int64_t count, const unsigned char* __restrict__ flag,
+                                   unsigned long long* __restrict__ out) {
+  unsigned long long acc = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    acc += flag[i];
+#pragma unroll
+  for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+}  // namespace gcoo_b200

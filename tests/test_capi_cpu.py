@@ -106,3 +106,11 @@ def test_no_oracle_in_product():
                 txt = open(os.path.join(dirpath, f), errors="ignore").read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "gcoo_oracle" not in txt and "libgcoo_ref" not in txt, f
+
+
+def test_roofline_profiles(gcoo):
+    """RooflineModel profiles + helpers (traffic.cpp:201-233) with the measured b200 entry."""
+    rep = {"flops": 1000, "n_dm": 10}
+    assert gcoo.operational_intensity(rep, 128) == 1000 / 1280
+    assert gcoo.roofline_throughput(1.0, "P100") == 732e9  # bandwidth-bound (traffic.cpp:210-213)
+    assert gcoo.roofline_throughput(1e6, "b200") == gcoo.ROOFLINE_PROFILES["b200"][0]

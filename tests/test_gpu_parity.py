@@ -389,3 +389,48 @@ def test_heavy_rows_balanced_placement(gcoo, cuda, oracle, kernel):
             assert np.array_equal(c, c_ref), (kernel, p)
     finally:
         gcoo.force_kernel("auto")
+
+
+# ----------------------------------------------------------- traffic model --
+def _traffic_golden():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "traffic.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("n,s", [(512, 0.95), (8000, 0.99)])
+def test_traffic_model_device_equals_reference_golden(gcoo, cuda, oracle, n, s):
+    """gcoo_model_traffic_dev reproduces the reference's model_gcoo_traffic /
+    model_csr_traffic counters exactly on the benchmark patterns (fixtures
+    made by tests/golden/make_traffic_golden.py from oracle/_ref)."""
+    import torch
+    a = gcoo.generate_uniform_sparse(n, s, 1)
+    d = gcoo.dense_to_gcoo_dev(torch.from_numpy(a).cuda(), 4)
+    gold = _traffic_golden()[f"n{n}_s{s}"]
+    for kind in ("gcoo", "csr"):
+        for mode in ("cold", "infinite_l2"):
+            got = gcoo.model_traffic_dev(d, n, gcoo.ExecConfig(p=4, b=64), mode == "infinite_l2", kind == "csr")
+            assert got == gold[f"{kind}_{mode}"], (kind, mode)
+
+
+def test_traffic_model_device_random_shapes(gcoo, cuda, oracle):
+    """Ragged m, k, n; p and b from 1 to 128; empty groups and columns: the
+    device model equals the plain-Python restatement (pinned to the reference
+    in tests/test_oracle.py)."""
+    from oracle import model_traffic
+    rng = np.random.default_rng(23)
+    for m, k, n, p, b, dens in [(37, 29, 70, 4, 8, 0.2), (64, 64, 64, 1, 1, 0.1), (50, 80, 33, 8, 64, 0.3),
+                                (9, 9, 1, 2, 2, 0.5), (100, 7, 129, 64, 4, 0.05), (5, 300, 31, 2, 128, 0.0),
+                                (300, 200, 1000, 16, 32, 0.02)]:
+        a = rand_dense(rng, m, k, dens)
+        g = gcoo.dense_to_gcoo(a, p)
+        dg = gcoo.DeviceGcoo.from_host(g)
+        rows, cols = np.nonzero(a)
+        for inf in (False, True):
+            for csr in (False, True):
+                got = gcoo.model_traffic_dev(dg, n, gcoo.ExecConfig(p=p, b=b), inf, csr)
+                assert got == model_traffic(rows, cols, m, k, n, p, b, inf, csr), (m, k, n, p, b, inf, csr)
+    with pytest.raises(ValueError):
+        gcoo.model_traffic_dev(dg, 10, gcoo.ExecConfig(p=16, b=3))
+

@@ -207,3 +207,38 @@ def test_powerlaw_generator_shape(oracle):
     key = r.astype(np.int64) * 1024 + c
     assert np.all(np.diff(key) > 0)  # strictly row-major, no duplicates
     assert np.all((v > 0) & (v <= 1))
+
+
+# ----------------------------------------------------------- traffic model --
+def _traffic_golden():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "traffic.json")) as f:
+        return json.load(f)
+
+
+def test_traffic_restatement_matches_golden(oracle):
+    """oracle.model_traffic (plain-Python restatement of traffic.cpp:43-197)
+    against the reference's own counts on square_benchmark(512, 0.95)."""
+    from oracle import model_traffic
+    a = oracle.uniform_sparse(512, 0.95, 1)
+    rows, cols = np.nonzero(a)
+    gold = _traffic_golden()["n512_s0.95"]
+    for kind in ("gcoo", "csr"):
+        for mode in ("cold", "infinite_l2"):
+            got = model_traffic(rows, cols, 512, 512, 512, 4, 64, mode == "infinite_l2", kind == "csr")
+            assert got == gold[f"{kind}_{mode}"], (kind, mode)
+
+
+def test_traffic_restatement_vs_reference_random(reference):
+    """Ragged shapes, p and b extremes, empty groups: restatement == reference."""
+    from oracle import model_traffic
+    R, _ = reference
+    rng = np.random.default_rng(17)
+    for m, k, n, p, b, d in [(37, 29, 70, 4, 8, 0.2), (64, 64, 64, 1, 1, 0.1), (50, 80, 33, 8, 64, 0.3),
+                             (9, 9, 1, 2, 2, 0.5), (100, 7, 129, 64, 4, 0.05), (5, 300, 31, 2, 128, 0.0)]:
+        rows, cols = np.nonzero(rng.random((m, k)) < d)
+        for inf in (False, True):
+            for csr in (False, True):
+                assert model_traffic(rows, cols, m, k, n, p, b, inf, csr) == \
+                    R.model_traffic(rows, cols, m, k, n, p, b, inf, csr), (m, k, n, p, b, inf, csr)
