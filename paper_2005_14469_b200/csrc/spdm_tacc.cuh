@@ -396,11 +396,11 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
         if (row >= 0) {
           float* dst = C + row * ldc + j;
           if constexpr (V == 4) {
-            *reinterpret_cast<float4*>(dst) = make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+            __stcs(reinterpret_cast<float4*>(dst), make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]));
           } else if constexpr (V == 2) {
-            *reinterpret_cast<float2*>(dst) = make_float2(r[2 * k], r[2 * k + 1]);
+            __stcs(reinterpret_cast<float2*>(dst), make_float2(r[2 * k], r[2 * k + 1]));
           } else {
-            *dst = r[k];
+            __stcs(dst, r[k]);
           }
         }
       }

@@ -325,11 +325,11 @@ spdm_tile_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
       if (row < m) {
         float* dst = C + row * ldc + j;
         if constexpr (V == 4) {
-          *reinterpret_cast<float4*>(dst) = make_float4(acc[s][0], acc[s][1], acc[s][2], acc[s][3]);
+          __stcs(reinterpret_cast<float4*>(dst), make_float4(acc[s][0], acc[s][1], acc[s][2], acc[s][3]));
         } else if constexpr (V == 2) {
-          *reinterpret_cast<float2*>(dst) = make_float2(acc[s][0], acc[s][1]);
+          __stcs(reinterpret_cast<float2*>(dst), make_float2(acc[s][0], acc[s][1]));
         } else {
-          *dst = acc[s][0];
+          __stcs(dst, acc[s][0]);
         }
       }
     }
