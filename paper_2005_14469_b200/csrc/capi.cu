@@ -264,6 +264,7 @@ struct SpdmPlan {
   int nchunks = 0;
   // TMEM kernels: row placement (original row -> unit row, and back; -1 = padding)
   DevBuf<int32_t> unit_of, row_of;
+  DevBuf<int32_t> skewed;  // 1: heaviest rows in row block 0 (launched first)
 };
 
 template <class Cfg, bool TACC>
@@ -308,6 +309,7 @@ void build_plan(SpdmPlan& P, const DevGcoo<float>& a, cudaStream_t s, int64_t mi
   if (TACC) {
     P.unit_of = DevBuf<int32_t>(a.m, s);
     P.row_of = DevBuf<int32_t>(P.row_blocks * Cfg::RB, s);
+    P.skewed = DevBuf<int32_t>(1, s);
   }
   DevBuf<int64_t> seg_len(nseg, s), scan_tmp(scan_scratch(nseg), s);
   P.seg_off = DevBuf<int64_t>(nseg + 1, s);
@@ -328,7 +330,7 @@ void build_plan(SpdmPlan& P, const DevGcoo<float>& a, cudaStream_t s, int64_t mi
     GCOO_LAUNCH_PDL(row_balance_kernel, grid_for(a.m, 256), 256, 0, s, a.m, (const int32_t*)row_nnz.get(),
                     (const int32_t*)hist.get(), cursor.get(), (int32_t)Cfg::RB, (int32_t)Cfg::NW, (int32_t)Cfg::RW,
                     (int32_t)std::min<int64_t>(INT32_MAX, 4 * ceil_div(a.nnz, a.m) + 16), (int32_t)rpb,
-                    P.unit_of.get(), P.row_of.get());
+                    P.unit_of.get(), P.row_of.get(), P.skewed.get());
   }
   if (a.nnz > 0) {
     if constexpr (TACC)
@@ -370,7 +372,7 @@ void run_plan(const SpdmPlan& P, const DevGcoo<float>& a, int64_t n, const float
   if constexpr (TACC)
     GCOO_LAUNCH_PDL(spdm_tacc_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n,
                     (const unsigned char*)P.ent.get(), (const int64_t*)P.seg_off.get(), C, ldc, P.row_blocks,
-                    P.nchunks, (const int32_t*)P.row_of.get());
+                    P.nchunks, (const int32_t*)P.row_of.get(), (const int32_t*)P.skewed.get());
   else
     GCOO_LAUNCH_PDL(spdm_tile_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n,
                     (const unsigned char*)P.ent.get(), (const int64_t*)P.seg_off.get(), C, ldc, P.row_blocks,

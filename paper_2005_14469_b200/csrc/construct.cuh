@@ -369,7 +369,8 @@ __global__ void plan_init_kernel(uint32_t* __restrict__ cnt, int64_t cnt_n, int3
 // TMEM kernels: rows are ordered by log2(nnz) bucket, heaviest first (a
 // counting sort; order inside a bucket is arbitrary — C does not depend on
 // where a row is computed), then sorted position i goes to row block
-// i / RB, warp (i % RB) % NW, slot (i % RB) / NW.
+// i / rpb, warp (i % rpb) % NW, slot (i % rpb) / NW.  Row block 0 then holds
+// the heaviest rows; *skew_flag tells the multiply to launch its CTAs first.
 __device__ __forceinline__ int nnz_bucket(int32_t c) { return 31 - (c > 0 ? 31 - __clz(c) : -1) - 1; }
 
 // hist[1..32]: rows per bucket; hist[0]: the largest row.
@@ -395,7 +396,7 @@ __global__ void bucket_hist_kernel(int64_t m, const int32_t* __restrict__ row_nn
 __global__ void row_balance_kernel(int64_t m, const int32_t* __restrict__ row_nnz, const int32_t* __restrict__ hist,
                                    int32_t* __restrict__ cursor, int32_t rb_rows, int32_t nw, int32_t rw,
                                    int32_t skew, int32_t rpb, int32_t* __restrict__ unit_of,
-                                   int32_t* __restrict__ row_of) {
+                                   int32_t* __restrict__ row_of, int32_t* __restrict__ skew_flag) {
   griddep_wait();  // PDL: predecessor complete
   __shared__ int32_t off[33];
   if (threadIdx.x == 0) {
@@ -409,20 +410,22 @@ __global__ void row_balance_kernel(int64_t m, const int32_t* __restrict__ row_nn
   __syncthreads();
   const bool skewed = hist[0] > skew;
   if (!skewed && rpb == rb_rows) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *skew_flag = 0;
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
       unit_of[r] = (int32_t)r;
       row_of[r] = (int32_t)r;
     }
     return;
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *skew_flag = skewed ? 1 : 0;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = r;
     if (skewed) {
       const int b = nnz_bucket(row_nnz[r]) + 1;
       i = off[b] + atomicAdd(&cursor[b], 1);
     }
-    const int64_t j = i % rpb;
-    const int64_t u = (i / rpb) * rb_rows + (j % nw) * rw + j / nw;
+    const int64_t blk = i / rpb, j = i % rpb;
+    const int64_t u = blk * rb_rows + (j % nw) * rw + j / nw;
     unit_of[r] = (int32_t)u;
     row_of[u] = (int32_t)r;
   }

@@ -288,7 +288,7 @@ template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
 spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t n, const unsigned char* __restrict__ ent,
                  const int64_t* __restrict__ seg_off, float* __restrict__ C, int64_t ldc, int64_t row_blocks,
-                 int nchunks, const int32_t* __restrict__ row_of) {
+                 int nchunks, const int32_t* __restrict__ row_of, const int32_t* __restrict__ skewed) {
   constexpr int W = Cfg::W, NW = Cfg::NW, S = Cfg::STAGES, V = Cfg::V, RW = Cfg::RW;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * Cfg::STAGE_BYTES);
@@ -297,20 +297,7 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
   const uint32_t smem0 = smem_u32(smem_raw);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // Row block 0 holds the heaviest rows (row_balance_kernel): its CTAs go
-  // first, then row blocks vary fastest so co-resident CTAs share a B strip.
   const int64_t col_tiles = ceil_div_dev(n, W);
-  int64_t rb, ct;
-  if (row_blocks > 1 && (int64_t)blockIdx.x < col_tiles) {
-    rb = 0;
-    ct = blockIdx.x;
-  } else {
-    const int64_t x = row_blocks > 1 ? (int64_t)blockIdx.x - col_tiles : (int64_t)blockIdx.x;
-    const int64_t rest = row_blocks > 1 ? row_blocks - 1 : 1;
-    rb = (row_blocks > 1 ? 1 : 0) + x % rest;
-    ct = x / rest;
-  }
-  const int64_t* so = seg_off + rb * nchunks;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -325,6 +312,23 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
   tmem_fence_after();
   const uint32_t tbase = *tmem_slot;
   griddep_wait();  // PDL: the planner's record stream is complete
+  // CTA order.  Row blocks vary fastest, so the CTAs co-resident on the GPU
+  // share a few B strips and every B tile crosses HBM once.  A skewed matrix
+  // (*skewed, row_balance_kernel) has its heaviest rows in row block 0: those
+  // CTAs go first so they overlap everything else instead of forming a tail.
+  int64_t rb, ct;
+  if (*skewed && row_blocks > 1 && (int64_t)blockIdx.x < col_tiles) {
+    rb = 0;
+    ct = blockIdx.x;
+  } else if (*skewed && row_blocks > 1) {
+    const int64_t x = (int64_t)blockIdx.x - col_tiles;
+    rb = 1 + x % (row_blocks - 1);
+    ct = x / (row_blocks - 1);
+  } else {
+    rb = (int64_t)blockIdx.x % row_blocks;
+    ct = (int64_t)blockIdx.x / row_blocks;
+  }
+  const int64_t* so = seg_off + rb * nchunks;
 
   if (warp == NW) {
     // ------------- producer: B tile (TMA 2-D) + record segment (bulk 1-D)
