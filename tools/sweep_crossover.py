@@ -3,7 +3,10 @@
 the crossover against dense-equivalent FLOPs — the smallest sparsity at which
 the GCOO multiply beats a dense FP32 GEMM of the same shape
 (crossover_search, bench.hpp:272-299).  The dense yardstick is cuBLAS SGEMM
-with TF32 off (torch.mm): measurement only, never on the product path.
+with TF32 off (torch.mm); the paper's sparse yardstick is cuSPARSE CSR SpMM
+(torch.sparse.mm on a CSR tensor, the timed region includes copying its
+output into a preallocated C).  Both are measurement only, never on the
+product path.
 
     python tools/sweep_crossover.py > profiles/rNN_sweep_crossover.jsonl
 
@@ -73,6 +76,16 @@ def main():
             ms = timed(lambda: G.spdm_gcoo_dev(d, b, c, stream=st), args.reps, flush, st)
             k_ms, k_n = G.kernel_time()
             G.kernel_timing(False)
+            # the paper's comparison: cuSPARSE CSR SpMM (torch.sparse.mm on a CSR
+            # tensor) on the same operands — a yardstick, never the product path
+            csr = a.to_sparse_csr()
+            cc = torch.empty_like(c)
+            try:
+                cusparse_ms = timed(lambda: cc.copy_(torch.sparse.mm(csr, b)), args.reps, flush, st)
+                same = bool(torch.allclose(cc, c, rtol=1e-5, atol=1e-6))
+            except RuntimeError as e:  # noqa: F841
+                cusparse_ms, same = None, None
+            del csr, cc
             if dense_ms is None:  # the dense time does not depend on the values
                 cd = torch.empty_like(c)
                 dense_ms = timed(lambda: torch.mm(a, b, out=cd), args.reps, flush, st)
@@ -83,7 +96,10 @@ def main():
                    "kernel_ms": round(k_ms / max(k_n, 1), 4), "gflops": round(fl / ms / 1e6, 1),
                    "eo_ms": round(eo_ms, 4), "dense_sgemm_ms": round(dense_ms, 4),
                    "dense_sgemm_tflops": round(2.0 * n ** 3 / dense_ms / 1e9, 2),
-                   "speedup_vs_dense": round(dense_ms / ms, 3)}
+                   "speedup_vs_dense": round(dense_ms / ms, 3),
+                   "cusparse_csr_ms": None if cusparse_ms is None else round(cusparse_ms, 4),
+                   "speedup_vs_cusparse": None if cusparse_ms is None else round(cusparse_ms / ms, 3),
+                   "cusparse_matches_1e-5": same}
             print(json.dumps(row), flush=True)
             if cross is None and ms < dense_ms:
                 cross = s
