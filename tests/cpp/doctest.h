@@ -4,7 +4,7 @@
 // not vendor (proj/.gitignore excludes vendor/).  This shim implements the
 // subset those tests use — TEST_CASE, SUBCASE (run inline, in order), CHECK*,
 // REQUIRE, FAIL, doctest::Approx and DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN — so
-// the reference's test_matrix.cpp / test_kernels.cpp compile unmodified
+// the reference's test_{matrix,kernels,io,traffic,bench}.cpp compile unmodified
 // against the drop-in headers in include/gcoo (tests/cpp/Makefile).
 #pragma once
 
@@ -21,11 +21,16 @@ struct Approx {
   explicit Approx(double v) : value(v) {}
   double value;
   double eps = 1.1920928955078125e-07 * 100;  // doctest's default epsilon
+  Approx& epsilon(double e) {
+    eps = e;
+    return *this;
+  }
   friend bool operator==(double lhs, const Approx& a) {
     return std::fabs(lhs - a.value) < a.eps * (1.0 + std::max(std::fabs(lhs), std::fabs(a.value)));
   }
   friend bool operator==(const Approx& a, double rhs) { return rhs == a; }
   friend bool operator!=(double lhs, const Approx& a) { return !(lhs == a); }
+  friend bool operator!=(const Approx& a, double rhs) { return !(rhs == a); }
 };
 
 namespace detail {

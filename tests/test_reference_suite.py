@@ -1,6 +1,10 @@
-"""The reference's OWN unit tests (proj/tests/test_matrix.cpp and
-test_kernels.cpp, compiled unmodified against the drop-in C++ headers in
-include/gcoo by tests/cpp/Makefile) run on the B200 through libgcoo_cuda.so.
+"""The reference's OWN unit tests (proj/tests/test_{matrix,kernels,io,traffic,
+bench}.cpp, compiled unmodified against the drop-in C++ headers in
+include/gcoo, together with the reference's unchanged io.cpp / traffic.cpp /
+bench.cpp, by tests/cpp/Makefile) run on the B200 through libgcoo_cuda.so.
+test_io needs no GPU and also runs in the CPU suite.  mtx_spdm --selftest
+(this repository's) reads MatrixMarket files with the reference's reader and
+multiplies them on the GPU.
 
 They cover the GCOO goldens (test_matrix.cpp:49-68), the converters' error
 types (:70-102), round trips and cross-format agreement (:138-209), the
@@ -17,7 +21,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BUILD = os.path.join(ROOT, "tests", "cpp", "_build")
-SUITES = ["ref_test_matrix", "ref_test_kernels"]
+SUITES = ["ref_test_matrix", "ref_test_kernels", "ref_test_traffic", "ref_test_bench"]
 
 
 def test_drop_in_headers_compile():
@@ -43,3 +47,27 @@ def test_reference_unit_suite_on_b200(cuda, gcoo, suite):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "failed: 0 | assertions" in r.stdout and r.stdout.rstrip().endswith("failed: 0"), r.stdout
+
+
+def _run_suite(name):
+    exe = os.path.join(BUILD, name)
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (needs the reference sources: make -C tests/cpp)")
+    return subprocess.run([exe], capture_output=True, text=True, timeout=600)
+
+
+def test_reference_io_suite():
+    """MatrixMarket reader/writer, generators, sweep grid and manifest
+    (test_io.cpp) against the drop-in matrix.hpp — host code only."""
+    r = _run_suite("ref_test_io")
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.rstrip().endswith("failed: 0"), r.stdout
+
+
+@pytest.mark.gpu
+def test_matrix_market_into_gpu_path(cuda, gcoo):
+    exe = os.path.join(BUILD, "mtx_spdm")
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (needs the reference sources: make -C tests/cpp)")
+    r = subprocess.run([exe, "--selftest"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "mtx selftest: 0 failure(s)" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
