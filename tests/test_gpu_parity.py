@@ -185,6 +185,44 @@ def test_determinism(gcoo, cuda):
         assert np.array_equal(c0, gcoo.spdm_gcoo(g, bm))
 
 
+def test_concurrent_host_calls_are_independent(gcoo, cuda, oracle):
+    """The C ABI is re-entrant (per-thread stream, thread-local error string):
+    host threads calling spdm_gcoo / coo_to_gcoo at once (ctypes drops the GIL)
+    each get their own bit-exact result, including the pipelined size and an
+    error raised on one thread while the others compute."""
+    import threading
+    rng = np.random.default_rng(41)
+    cases = []
+    for i, (m, k, n, d) in enumerate([(700, 900, 320, 0.01), (2048, 2048, 2048, 0.004), (513, 129, 68, 0.2),
+                                      (1000, 3000, 512, 0.002), (4096, 4096, 2304, 0.002), (64, 64, 64, 0.5)]):
+        a = rand_dense(rng, m, k, d)
+        bm = rand_dense(rng, k, n, 1.0)
+        go = oracle.dense_to_gcoo(a, 4)
+        cases.append((a, bm, go, oracle.spdm(go, bm, 64, fma=True)[0]))
+    out, errs = [None] * len(cases), []
+
+    def work(i):
+        try:
+            a, bm, go, _ = cases[i]
+            for _ in range(3):
+                g = gcoo.dense_to_gcoo(a, 4)
+                out[i] = gcoo.spdm_gcoo(g, bm)
+            if i == 0:
+                with pytest.raises(ValueError):
+                    gcoo.spdm_gcoo(g, bm[:-1].copy())  # inner-dimension mismatch on this thread only
+        except Exception as e:  # noqa: BLE001
+            errs.append((i, repr(e)))
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(len(cases))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for (a, bm, go, c_ref), c in zip(cases, out):
+        assert np.array_equal(c, c_ref)
+
+
 def test_strided_column_shards_bitwise_equal(gcoo, cuda, oracle):
     """Column sharding (the multi-GPU decomposition) is bitwise invisible."""
     import torch
