@@ -223,6 +223,33 @@ def run_ours(args):
     flops_rank = 2.0 * nnz * n
     value = world * flops_rank / (ms_mean * 1e-3) / 1e9
 
+    # ---- plan reuse (extension): the same multiply, A's record stream built once
+    plan_reuse = None
+    try:
+        plan = G.SpdmPlan(dg, stream=stream)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                flush.zero_()
+                plan.run(dB, dC, stream=stream)
+            torch.cuda.synchronize()
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            torch.cuda._sleep(int(1e7))
+            for e0, e1 in evs:
+                flush.zero_()
+                e0.record(stream)
+                plan.run(dB, dC, stream=stream)
+                e1.record(stream)
+            torch.cuda.synchronize()
+        pms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / len(evs)
+        plan.close()
+        plan_reuse = {"ms_per_step": round(pms, 4), "value": round(world * 2.0 * nnz * n / (pms * 1e-3) / 1e9, 2),
+                      "unit": "GFLOPS", "note": "gcoo_plan_* (A's record stream built once, then one multiply "
+                                                "kernel per B); not the headline, which plans every call"}
+    except Exception as e:  # noqa: BLE001
+        plan_reuse = {"error": str(e)[:200]}
+
     # ---- end to end through the public host API ----------------------
     g_host = dg.to_host()
     b_pin = torch.empty((k, n), dtype=torch.float32, pin_memory=True)
@@ -240,11 +267,15 @@ def run_ours(args):
         G.spdm_gcoo(g_pin, b_pin.numpy(), cfg, out=c_pin.numpy())
     if world > 1:
         dist.barrier()
-    e2e_steps = max(3, min(args.steps, 10))
-    t0 = time.perf_counter()
+    # each call timed on its own (host clock around the whole API call: copies in,
+    # multiply, copy out, synchronised); the median is robust to host hiccups
+    e2e_steps = max(5, min(args.steps, 20))
+    e2e_times = []
     for _ in range(e2e_steps):
+        t0 = time.perf_counter()
         G.spdm_gcoo(g_pin, b_pin.numpy(), cfg, out=c_pin.numpy())
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = statistics.median(e2e_times)
     te = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -350,9 +381,11 @@ def run_ours(args):
                    "l2": "flushed (256 MiB write) before every timed launch; B+C = 512 MB > L2"},
         "e2e": {"value": round(e2e_value, 2), "unit": "GFLOPS", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_s * 1e3, 3),
+                "ms_per_step_mean": round(statistics.mean(e2e_times) * 1e3, 3), "calls": len(e2e_times),
                 "path": "paper_2005_14469_b200.spdm_gcoo -> gcoo_spdm_f32 (pinned host buffers)",
                 **pcie_roofline(h2d + d2h, e2e_s)},
         "gpu_launches": int(launches),
+        "plan_reuse": plan_reuse,
         "c_gather": gather,
         "roofline": {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved_gbs / hbm_peak, 4), "traffic": traffic,

@@ -111,6 +111,26 @@ int gcoo_spdm_f64_dev(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, int
                       const double* B, int64_t ldb, double* C, int64_t ldc, gcoo_stats* stats,
                       int flavor, void* stream);
 
+/*
+ * Plan / execute split (an extension; the reference recomputes nothing between
+ * calls because its kernel reads the GCOO arrays directly).  The B200 multiply
+ * runs from a record stream built from A by a ~35 us planner; a caller that
+ * multiplies the same A by many B builds it once here.  A's device arrays must
+ * stay alive and unchanged while the plan exists.  The plan's buffers are
+ * stream-ordered on `stream`: multiplies on other streams must be ordered
+ * after the create.  gcoo_plan_spdm_f32_dev is stream-ordered and returns the
+ * same bits as gcoo_spdm_f32_dev (any B/C layout; an unaligned one is planned
+ * per call).  gcoo_plan_destroy synchronises the device, then frees.
+ */
+typedef struct gcoo_plan gcoo_plan;
+int gcoo_plan_create_f32_dev(int64_t m, int64_t k, int32_t p, int64_t nnz, const float* values,
+                             const int32_t* row_idx, const int32_t* col_idx, int64_t groups,
+                             const int64_t* g_idxes, const int64_t* nnz_per_group, int flavor,
+                             gcoo_plan** plan, void* stream);
+int gcoo_plan_spdm_f32_dev(const gcoo_plan* plan, int64_t n, const float* B, int64_t ldb, float* C,
+                           int64_t ldc, void* stream);
+int gcoo_plan_destroy(gcoo_plan* plan);
+
 /* KernelStats only (K4 run counter; kernels.hpp:283-310) for a device GCOO. */
 int gcoo_stats_dev(int64_t m, int64_t n, int32_t p, int32_t b, int64_t nnz,
                    const int32_t* row_idx, const int32_t* col_idx, int64_t groups,

@@ -706,6 +706,20 @@ void spdm_dev(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, int64_t nnz
   if (stats) device_stats(nnz, n, p, b, groups, row_idx, col_idx, g_idxes, stats, s);
 }
 
+// ------------------------------------------------------ plan / execute -----
+// A's record stream (the planner's output) depends on A alone, so a caller
+// that multiplies the same A by many B builds it once (gcoo_plan_create_*)
+// and runs gcoo_plan_spdm_* per B: the step is then the multiply kernel only.
+}  // namespace gcoo_b200
+
+struct gcoo_plan {
+  gcoo_b200::DevGcoo<float> a;
+  int flavor = GCOO_FLAVOR_FMA;
+  gcoo_b200::SpdmPlan plan;
+};
+
+namespace gcoo_b200 {
+
 // ------------------------------------------------------- construction -----
 // coo_to_gcoo on device arrays: validate, offsets, log2(p) merge rounds.
 template <typename T>
@@ -1011,6 +1025,51 @@ int gcoo_spdm_f32_dev(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, int
   return guarded([&] {
     spdm_dev<float>(m, k, n, p, b, nnz, values, row_idx, col_idx, groups, g_idxes, nnz_per_group, B, ldb, C,
                     ldc, stats, flavor, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int gcoo_plan_create_f32_dev(int64_t m, int64_t k, int32_t p, int64_t nnz, const float* values,
+                             const int32_t* row_idx, const int32_t* col_idx, int64_t groups, const int64_t* g_idxes,
+                             const int64_t* nnz_per_group, int flavor, gcoo_plan** plan, void* stream) {
+  return guarded([&] {
+    if (!plan) einval("gcoo_plan_create: null plan pointer");
+    *plan = nullptr;
+    validate_spdm(m, k, 1, p, p, 1, k, nnz, groups, nullptr, 0);
+    std::unique_ptr<gcoo_plan> h(new gcoo_plan());
+    h->a = DevGcoo<float>{m, k, nnz, groups, p, values, row_idx, col_idx, g_idxes, nnz_per_group};
+    h->flavor = flavor;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (m > 0) {
+      // the kernel class for 16-byte aligned B/C with n % 4 == 0 (checked again per multiply)
+      static const float aligned[4] __attribute__((aligned(16))) = {};
+      make_plan<float>(h->plan, h->a, choose_kind<float>(h->a, 4, 4, 4, aligned, aligned, flavor), s);
+    }
+    *plan = h.release();
+  });
+}
+
+int gcoo_plan_spdm_f32_dev(const gcoo_plan* plan, int64_t n, const float* B, int64_t ldb, float* C, int64_t ldc,
+                           void* stream) {
+  return guarded([&] {
+    if (!plan) einval("gcoo_plan_spdm: null plan");
+    if (n < 0 || ldb < n || ldc < n) einval("spdm_gcoo: leading dimension smaller than n");
+    const DevGcoo<float>& a = plan->a;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (a.m == 0 || n == 0) return;
+    const int kind = choose_kind<float>(a, n, ldb, ldc, B, C, plan->flavor);
+    if (kind == plan->plan.kind) {
+      run_spdm<float>(plan->plan, a, n, B, ldb, C, ldc, plan->flavor, s);
+    } else {  // this B/C layout needs another kernel class: plan it for this call
+      launch_spdm<float>(a, n, B, ldb, C, ldc, plan->flavor, s);
+    }
+  });
+}
+
+int gcoo_plan_destroy(gcoo_plan* plan) {
+  return guarded([&] {
+    if (!plan) return;
+    GCOO_CUDA(cudaDeviceSynchronize());  // no multiply may still read the plan's buffers
+    delete plan;
   });
 }
 

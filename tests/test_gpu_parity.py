@@ -223,6 +223,30 @@ def test_concurrent_host_calls_are_independent(gcoo, cuda, oracle):
         assert np.array_equal(c, c_ref)
 
 
+def test_plan_execute_split_bit_exact(gcoo, cuda, oracle):
+    """gcoo_plan_*: one plan, many multiplies (different B widths, a strided
+    column shard, an unaligned shard that needs another kernel class) — every
+    result equals the one-shot device call bit for bit."""
+    import torch
+    rng = np.random.default_rng(43)
+    for m, k, d in [(3000, 2500, 0.01), (777, 1000, 0.05), (5000, 5000, 0.002)]:
+        a = rand_dense(rng, m, k, d)
+        dg = gcoo.DeviceGcoo.from_host(gcoo.dense_to_gcoo(a, 4))
+        plan = gcoo.SpdmPlan(dg)
+        bfull = torch.from_numpy(rand_dense(rng, k, 1030, 1.0)).cuda()
+        for n0, n1 in [(0, 512), (0, 1030), (128, 640), (3, 515)]:
+            b = bfull[:, n0:n1]
+            c1 = torch.empty((m, n1 - n0), device="cuda")
+            c2 = torch.empty_like(c1)
+            plan.run(b, c1)
+            gcoo.spdm_gcoo_dev(dg, b, c2)
+            torch.cuda.synchronize()
+            assert torch.equal(c1, c2), (m, k, n0, n1)
+        plan.close()
+    with pytest.raises(ValueError):
+        plan.run(bfull, torch.empty((5000, 1030), device="cuda"))
+
+
 def test_strided_column_shards_bitwise_equal(gcoo, cuda, oracle):
     """Column sharding (the multi-GPU decomposition) is bitwise invisible."""
     import torch
