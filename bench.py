@@ -76,6 +76,7 @@ class Clocks:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.first = ""
 
     def __enter__(self):
         try:
@@ -86,6 +87,14 @@ class Clocks:
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            # wait for the first sample: nvidia-smi's NVML start-up briefly stalls the
+            # GPU, and must not land inside the timed region
+            import threading
+            box = []
+            t = threading.Thread(target=lambda: box.append(self.proc.stdout.readline()), daemon=True)
+            t.start()
+            t.join(timeout=30)
+            self.first = box[0] if box else ""
         except Exception:
             self.proc = None
         return self
@@ -101,7 +110,8 @@ class Clocks:
 
     def summary(self):
         rows = []
-        for line in (self.out or "").strip().splitlines():
+        lines = (self.out or "").strip().splitlines() or [self.first]  # pre-region sample only if none inside
+        for line in lines:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) >= 7:
                 try:
