@@ -140,7 +140,8 @@ def set_device(device: int) -> None:
     _check(lib().gcoo_set_device(device))
 
 
-KERNELS = {"auto": -1, "rowtile": 0, "tile_v4": 5, "tacc_v4": 8, "tacc_v2": 9, "tacc_v4w": 10}
+KERNELS = {"auto": -1, "rowtile": 0, "tile_v4": 5, "tacc_v4": 8, "tacc_v2": 9, "tacc_v4w": 10, "tacc28_k192": 11, "tacc28_k160": 12,
+           "tacc28_k128": 13, "tacc28_k96": 14, "tacc28_k64": 15}
 
 
 def force_kernel(which: str = "auto") -> None:

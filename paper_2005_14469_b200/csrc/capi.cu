@@ -257,7 +257,7 @@ bool tile_fits(const DevGcoo<float>& a, int64_t n, int64_t ldb, int64_t ldc, con
 // serves any number of B/C column strips with the same layout class
 // (the host-pointer path pipelines strips through one plan).
 struct SpdmPlan {
-  int kind = 0;  // 0 row-tile, 5 tile_v4, 8 tacc_v4, 9 tacc_v2, 10 tacc_v4w
+  int kind = 0;  // 0 row-tile, 5 tile_v4, 8 tacc_v4, 9 tacc_v2, 10 tacc_v4w, 11-15 tacc28 (KC 192..64)
   DevBuf<int64_t> seg_off;
   DevBuf<unsigned char> ent;
   int64_t row_blocks = 0;
@@ -389,14 +389,26 @@ int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const 
   if constexpr (std::is_same<T, float>::value) {
     if (flavor == GCOO_FLAVOR_MUL_ADD || g_force_kernel == 0 || a.m == 0) return 0;
     const double density = (double)a.nnz / ((double)a.m * (double)a.k);
-    // measured crossovers at n=8000 (profiles/r01_kernel_sweep.jsonl): register tiles win at
-    // s <= 0.95, TMEM accumulators with 24 warps for 0.95 < s < 0.998, 16 warps beyond
-    const int pick = g_force_kernel > 0 ? g_force_kernel : density >= 0.035 ? 5 : density >= 0.002 ? 10 : 8;
+    // measured crossovers at n=8000 (profiles/r01_kernel_sweep_28w.jsonl): TMEM accumulators
+    // with 28 warps everywhere, the chunk depth shrinking as the density grows (the record
+    // stage must hold a chunk's records); 16 warps at the sparse end
+    const int pick = g_force_kernel > 0    ? g_force_kernel
+                     : density >= 0.16     ? 15
+                     : density >= 0.075    ? 14
+                     : density >= 0.035    ? 13
+                     : density >= 0.017    ? 12
+                     : density >= 0.0015   ? 11
+                                           : 8;
     switch (pick) {
       case 5: return tile_fits<TileV4>(a, n, ldb, ldc, B, C) ? 5 : 0;
       case 8: return tile_fits<TaccV4>(a, n, ldb, ldc, B, C) ? 8 : 0;
       case 9: return tile_fits<TaccV2>(a, n, ldb, ldc, B, C) ? 9 : 0;
       case 10: return tile_fits<TaccV4W>(a, n, ldb, ldc, B, C) ? 10 : 0;
+      case 11: return tile_fits<Tacc28K192>(a, n, ldb, ldc, B, C) ? 11 : 0;
+      case 12: return tile_fits<Tacc28K160>(a, n, ldb, ldc, B, C) ? 12 : 0;
+      case 13: return tile_fits<Tacc28K128>(a, n, ldb, ldc, B, C) ? 13 : 0;
+      case 14: return tile_fits<Tacc28K96>(a, n, ldb, ldc, B, C) ? 14 : 0;
+      case 15: return tile_fits<Tacc28K64>(a, n, ldb, ldc, B, C) ? 15 : 0;
       default: return 0;
     }
   }
@@ -414,6 +426,11 @@ void make_plan(SpdmPlan& P, const DevGcoo<T>& a, int kind, cudaStream_t s, int64
     if (kind == 8) build_plan<TaccV4, true>(P, a, s, wave, ceil_div(strip_n, TaccV4::W));
     if (kind == 9) build_plan<TaccV2, true>(P, a, s, wave, ceil_div(strip_n, TaccV2::W));
     if (kind == 10) build_plan<TaccV4W, true>(P, a, s, wave, ceil_div(strip_n, TaccV4W::W));
+    if (kind == 11) build_plan<Tacc28K192, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K192::W));
+    if (kind == 12) build_plan<Tacc28K160, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K160::W));
+    if (kind == 13) build_plan<Tacc28K128, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K128::W));
+    if (kind == 14) build_plan<Tacc28K96, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K96::W));
+    if (kind == 15) build_plan<Tacc28K64, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K64::W));
   }
 }
 
@@ -426,6 +443,11 @@ void run_spdm(const SpdmPlan& P, const DevGcoo<T>& a, int64_t n, const T* B, int
     if (P.kind == 8) return run_plan<TaccV4, true>(P, a, n, B, ldb, C, ldc, s);
     if (P.kind == 9) return run_plan<TaccV2, true>(P, a, n, B, ldb, C, ldc, s);
     if (P.kind == 10) return run_plan<TaccV4W, true>(P, a, n, B, ldb, C, ldc, s);
+    if (P.kind == 11) return run_plan<Tacc28K192, true>(P, a, n, B, ldb, C, ldc, s);
+    if (P.kind == 12) return run_plan<Tacc28K160, true>(P, a, n, B, ldb, C, ldc, s);
+    if (P.kind == 13) return run_plan<Tacc28K128, true>(P, a, n, B, ldb, C, ldc, s);
+    if (P.kind == 14) return run_plan<Tacc28K96, true>(P, a, n, B, ldb, C, ldc, s);
+    if (P.kind == 15) return run_plan<Tacc28K64, true>(P, a, n, B, ldb, C, ldc, s);
   }
   if (flavor != GCOO_FLAVOR_MUL_ADD) launch_rowtile_p<T, true>(a, n, B, ldb, C, ldc, s);
   else launch_rowtile_p<T, false>(a, n, B, ldb, C, ldc, s);

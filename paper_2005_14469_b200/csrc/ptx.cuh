@@ -141,6 +141,17 @@ __device__ __forceinline__ void tmem_st(uint32_t addr, const float (&r)[N]) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(addr), "f"(r[0]) : "memory");
   }
 }
+// 8 consecutive columns per thread (zero-fill / read-back)
+__device__ __forceinline__ void tmem_st8_zero(uint32_t addr) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(addr), "r"(0u)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t addr, float (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+               : "r"(addr)
+               : "memory");
+}
 // 16 consecutive columns per thread (zero-fill / read-back)
 __device__ __forceinline__ void tmem_st16_zero(uint32_t addr) {
   asm volatile(

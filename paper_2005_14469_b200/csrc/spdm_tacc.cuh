@@ -51,7 +51,7 @@ struct TaccCfg {
   static constexpr int V = V_;             // floats per lane
   static constexpr int W = 32 * V_;        // columns per CTA strip
   static constexpr int NW = NW_;           // consumer warps: NW/4 per TMEM lane quadrant
-  static constexpr int TCOLS = (512 / (NW_ / 4)) & ~15;  // TMEM columns per warp (128 for 16 warps)
+  static constexpr int TCOLS = (512 / (NW_ / 4)) & ~7;  // TMEM columns per warp (128 / 80 / 72 for 16 / 24 / 28 warps)
   static constexpr int RW = TCOLS / V_;    // rows (slots) per warp
   static constexpr int RB = NW * RW;       // rows per CTA
   static constexpr int KC = KC_;           // B rows per chunk
@@ -65,7 +65,7 @@ struct TaccCfg {
   static constexpr int TABLE = (4 * NW_ + 15) & ~15;  // per-segment warp offset table (NW x u32)
   static constexpr size_t SMEM = (size_t)STAGES_ * STAGE_BYTES + 2 * STAGES_ * 8 + 16;
   static_assert(KC_ <= 256, "TMA box rows");
-  static_assert(NW_ % 4 == 0 && NW_ <= 28 && TCOLS % (4 * V_) == 0, "warps tile the 4 TMEM lane quadrants");
+  static_assert(NW_ % 4 == 0 && NW_ <= 28 && TCOLS % 8 == 0 && 8 % V_ == 0, "warps tile the 4 TMEM lane quadrants");
   static_assert(BTILE < (1u << 24) && RW <= 256, "24-bit B offsets, 8-bit slots");
   static_assert(CAP_ % 16 == 0 && BTILE % 16 == 0, "16-byte stages");
   static_assert(SMEM <= 227 * 1024 && SMEM > 116 * 1024, "one CTA per SM (it owns all 512 TMEM columns)");
@@ -75,6 +75,15 @@ struct TaccCfg {
 using TaccV4 = TaccCfg<4, 192, 2, 16384>;   // W=128, RB=512 : density >~ 2%
 using TaccV2 = TaccCfg<2, 256, 2, 16384>;   // W=64,  RB=1024: density ~ 1%
 using TaccV4W = TaccCfg<4, 192, 2, 16384, 24>;  // W=128, RB=480, 24 consumer warps (more latency hiding)
+// 28 consumer warps (RB=504): the chunk depth KC trades run length (swaps per
+// entry) against the record-stage capacity, which must hold a row block's
+// records for one chunk (an oversize segment is read from global memory):
+// denser matrices take shallower chunks and bigger record stages.
+using Tacc28K192 = TaccCfg<4, 192, 2, 16384, 28>;  // density < 1.5 %
+using Tacc28K160 = TaccCfg<4, 160, 2, 32768, 28>;  //         < 3.5 %
+using Tacc28K128 = TaccCfg<4, 128, 2, 49152, 28>;  //         < 7 %
+using Tacc28K96 = TaccCfg<4, 96, 2, 65536, 28>;    //         < 12 %
+using Tacc28K64 = TaccCfg<4, 64, 2, 81920, 28>;    //         >= 12 %
 
 // ---------------------------------------------------------------- planner --
 // P1: per (unit u = row / RW, chunk, slot = row % RW) entry counts.
@@ -356,7 +365,7 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
   // my accumulators: TMEM lanes 32*(warp%4).., columns (warp/4)*TCOLS + slot*V + v
   const uint32_t tacc = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * Cfg::TCOLS);
 #pragma unroll
-  for (int c0 = 0; c0 < Cfg::TCOLS; c0 += 16) tmem_st16_zero(tacc + c0);
+  for (int c0 = 0; c0 < Cfg::TCOLS; c0 += 8) tmem_st8_zero(tacc + c0);
   tmem_wait_st();
 
   float acc[V];
@@ -389,13 +398,13 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
   const int64_t row0 = (rb * NW + warp) * (int64_t)RW;
   const int64_t j = ct * W + lane * V;
 #pragma unroll 1
-  for (int c0 = 0; c0 < Cfg::TCOLS; c0 += 16) {
-    float r[16];
-    tmem_ld16(tacc + c0, r);
+  for (int c0 = 0; c0 < Cfg::TCOLS; c0 += 8) {
+    float r[8];
+    tmem_ld8(tacc + c0, r);
     tmem_wait_ld();
     if (j < n) {
 #pragma unroll
-      for (int k = 0; k < 16 / V; ++k) {
+      for (int k = 0; k < 8 / V; ++k) {
         const int64_t row = row_of[row0 + c0 / V + k];  // -1: padding slot
         if (row >= 0) {
           float* dst = C + row * ldc + j;
