@@ -18,8 +18,8 @@ JSON line per sparsity with three predictions and the ncu measurement:
   loads (1 per record) + TMA tile writes (bytes / 128).
 * measured — ncu (profiles/r01_ncu_*.json, `--set full` of the same launch).
 
-    python tools/traffic_crosscheck.py profiles/r01_ncu_tile_s0.9.json \
-        profiles/r01_ncu_tacc_v4w_s0.99.json profiles/r01_ncu_tacc_v4w_s0.995.json
+    python tools/traffic_crosscheck.py profiles/r01_ncu_tacc28_s0.9.json \
+        profiles/r01_ncu_tacc28_s0.99.json profiles/r01_ncu_tacc28_s0.995.json
 """
 import json
 import os
@@ -31,8 +31,20 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2005_14469_b200 as G  # noqa: E402
 
 N = 8000
-# kernel tilings (csrc/spdm_tacc.cuh TaccV4W, csrc/spdm_tile.cuh TileV4)
-TILING = {"tacc": dict(RB=480, W=128, KC=192), "tile": dict(RB=240, W=128, KC=48)}
+
+
+def tiling(kernel_name):
+    """RB, W, KC of the profiled kernel from its template arguments
+    (TaccCfg<V, KC, STAGES, CAP, NW>: RB = NW * (512 / (NW/4) & ~7) / V; TileCfg: RB = 15 * 64 / V)."""
+    import re
+    m = re.search(r"TaccCfg<(\d+), (\d+), \d+, \d+(?:, (\d+))?>", kernel_name)
+    if m:
+        v, kc, nw = int(m.group(1)), int(m.group(2)), int(m.group(3) or 16)
+        tcols = (512 // (nw // 4)) & ~7
+        return dict(RB=nw * (tcols // v), W=32 * v, KC=kc)
+    m = re.search(r"TileCfg<(\d+), (\d+),", kernel_name)
+    v, kc = int(m.group(1)), int(m.group(2))
+    return dict(RB=15 * (64 // v), W=32 * v, KC=kc)
 
 
 def pow2_at_least(x):
@@ -47,19 +59,17 @@ def main():
     for path in sys.argv[1:]:
         with open(path) as f:
             m = json.load(f)
-        kname = "tacc" if "tacc" in m["kernel"] else "tile"
         s = float(path.rsplit("_s", 1)[1].rsplit(".json", 1)[0])
-        meas[s] = (kname, m, os.path.basename(path))
-    b_dev = None
+        meas[s] = (m["kernel"], m, os.path.basename(path))
     for s in sorted(meas):
         kname, m, src = meas[s]
-        t = TILING[kname]
+        t = tiling(kname)
         a = torch.from_numpy(G.generate_uniform_sparse(N, s, 1)).cuda()
         d = G.dense_to_gcoo_dev(a, 4)
         nnz = d.nnz()
         paper = G.model_traffic_dev(d, N, G.ExecConfig(p=4, b=64), infinite_l2=True)
         dp = G.dense_to_gcoo_dev(a, pow2_at_least(t["RB"]))
-        tiling = G.model_traffic_dev(dp, N, G.ExecConfig(p=dp.p, b=t["W"]), infinite_l2=True)
+        tmodel = G.model_traffic_dev(dp, N, G.ExecConfig(p=dp.p, b=t["W"]), infinite_l2=True)
         del a, dp
         # this kernel: records hold up to two entries of one row per chunk (count them exactly)
         rows = d.row_idx.long()
@@ -74,13 +84,13 @@ def main():
         compulsory = 12 * nnz + 16 * ((N + 3) // 4) + 4 * N * N + 4 * N * N
         wavefronts = nnz * col_tiles * 4 + records * col_tiles + (b_tiles + rec_bytes) / 128
         row = {
-            "n": N, "s": s, "nnz": nnz, "kernel": kname, "ncu": src,
+            "n": N, "s": s, "nnz": nnz, "kernel": kname[:60], "tiling": t, "ncu": src,
             "paper_model_p4_b64": {"dram_bytes": paper["n_dm"] * 128, "l2_to_sm_bytes": (paper["n_dm"] + paper["n_l2"]) * 128,
                                    "onchip_bytes": (paper["n_shm"] + paper["tex_l1_trans"]) * 4,
                                    "share": {k: round(paper[k] / max(1, sum(paper[x] for x in ("n_dm", "n_l2", "n_shm", "tex_l1_trans"))), 4)
                                              for k in ("n_dm", "n_l2", "n_shm", "tex_l1_trans")}},
-            "tiling_model": {"p": pow2_at_least(t["RB"]), "b": t["W"], "dram_bytes": tiling["n_dm"] * 128,
-                             "l2_to_sm_bytes": (tiling["n_dm"] + tiling["n_l2"]) * 128},
+            "tiling_model": {"p": pow2_at_least(t["RB"]), "b": t["W"], "dram_bytes": tmodel["n_dm"] * 128,
+                             "l2_to_sm_bytes": (tmodel["n_dm"] + tmodel["n_l2"]) * 128},
             "kernel_model": {"dram_bytes": compulsory, "l2_to_sm_bytes": b_tiles + rec_bytes,
                              "smem_wavefronts": int(wavefronts), "records": records},
             "measured": {"dram_bytes": m["dram_read_bytes"] + m["dram_write_bytes"],
