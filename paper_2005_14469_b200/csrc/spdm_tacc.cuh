@@ -225,6 +225,9 @@ struct RecSrc<true> {  // segment larger than a stage: read from global memory
 #define GCOO_ABL 0  // ablation builds (tools/ablate.sh, wrong results): 1 no TMEM swap, 2 no B loads, 3 both
 #endif
 
+// `cur` always names a slot whose TMEM copy the registers may overwrite: it
+// starts at slot 0 with zero accumulators (slot 0's TMEM is zero too), so the
+// first swap needs no "nothing held yet" test.
 template <class Cfg>
 __device__ __forceinline__ void tacc_switch(float (&acc)[Cfg::V], uint32_t& cur, uint32_t tacc, uint32_t s) {
   if ((GCOO_ABL & 1) && s != cur) {
@@ -232,7 +235,7 @@ __device__ __forceinline__ void tacc_switch(float (&acc)[Cfg::V], uint32_t& cur,
     return;
   }
   if (s != cur) {  // warp-uniform: swap the slot's accumulators through TMEM
-    if (cur != ~0u) tmem_st<Cfg::V>(tacc + cur * Cfg::V, acc);
+    tmem_st<Cfg::V>(tacc + cur * Cfg::V, acc);
     tmem_ld<Cfg::V>(tacc + s * Cfg::V, acc);
     tmem_wait_ld();
     cur = s;
@@ -245,9 +248,24 @@ __device__ __forceinline__ void tacc_fma(float (&acc)[V], float a, const float (
   for (int v = 0; v < V; ++v) acc[v] = __fmaf_rn(a, b[v], acc[v]);
 }
 
+// One record: its (up to) two entries of one row slot.
+template <class Cfg, bool GLOBAL>
+__device__ __forceinline__ void tacc_one(float (&acc)[Cfg::V], uint32_t& cur, uint32_t tacc, const uint4 q,
+                                         uint32_t bbase) {
+  constexpr int V = Cfg::V;
+  float b0[V], b1[V];
+  const bool two = q.w != ~0u;
+  lds_vec<V>(bbase + (q.z & 0xffffffu), b0);
+  if (two) lds_vec<V>(bbase + q.w, b1);
+  tacc_switch<Cfg>(acc, cur, tacc, q.z >> 24);
+  tacc_fma<V>(acc, __uint_as_float(q.x), b0);
+  if (two) tacc_fma<V>(acc, __uint_as_float(q.y), b1);
+}
+
 // One warp walks its records for one chunk, two records per step (both
-// records and their B rows are in flight before the first FMA).  `cur` (the
-// slot whose accumulators are in registers) persists across chunks.
+// records and their B rows are in flight before the first FMA), then the odd
+// record if any — the paired loop carries no "second record present" tests.
+// `cur` (the slot whose accumulators are in registers) persists across chunks.
 template <class Cfg, bool GLOBAL>
 __device__ __forceinline__ void tacc_consume(float (&acc)[Cfg::V], uint32_t& cur, uint32_t tacc,
                                              typename RecSrc<GLOBAL>::addr_t seg, int warp, uint32_t bbase) {
@@ -260,11 +278,9 @@ __device__ __forceinline__ void tacc_consume(float (&acc)[Cfg::V], uint32_t& cur
   const auto wseg = seg + woff;
   const uint32_t nrec = Src::ld32(wseg);
   auto rec = wseg + Cfg::HDR;
-  for (uint32_t r = 0; r < nrec; r += 2, rec += 2 * Cfg::REC) {
-    const bool hasB = r + 1 < nrec;
+  for (uint32_t r = 1; r < nrec; r += 2, rec += 2 * Cfg::REC) {
     const uint4 qa = Src::ld(rec);
-    uint4 qb = make_uint4(0u, 0u, 0u, ~0u);
-    if (hasB) qb = Src::ld(rec + Cfg::REC);
+    const uint4 qb = Src::ld(rec + Cfg::REC);
     float ba0[V], ba1[V], bb0[V], bb1[V];
     const bool a2 = qa.w != ~0u;
     const bool b2 = qb.w != ~0u;
@@ -279,18 +295,17 @@ __device__ __forceinline__ void tacc_consume(float (&acc)[Cfg::V], uint32_t& cur
     } else {
       lds_vec<V>(bbase + (qa.z & 0xffffffu), ba0);
       if (a2) lds_vec<V>(bbase + qa.w, ba1);
-      if (hasB) lds_vec<V>(bbase + (qb.z & 0xffffffu), bb0);
+      lds_vec<V>(bbase + (qb.z & 0xffffffu), bb0);
       if (b2) lds_vec<V>(bbase + qb.w, bb1);
     }
     tacc_switch<Cfg>(acc, cur, tacc, qa.z >> 24);
     tacc_fma<V>(acc, __uint_as_float(qa.x), ba0);
     if (a2) tacc_fma<V>(acc, __uint_as_float(qa.y), ba1);
-    if (hasB) {
-      tacc_switch<Cfg>(acc, cur, tacc, qb.z >> 24);
-      tacc_fma<V>(acc, __uint_as_float(qb.x), bb0);
-      if (b2) tacc_fma<V>(acc, __uint_as_float(qb.y), bb1);
-    }
+    tacc_switch<Cfg>(acc, cur, tacc, qb.z >> 24);
+    tacc_fma<V>(acc, __uint_as_float(qb.x), bb0);
+    if (b2) tacc_fma<V>(acc, __uint_as_float(qb.y), bb1);
   }
+  if (nrec & 1u) tacc_one<Cfg, GLOBAL>(acc, cur, tacc, Src::ld(rec), bbase);
 }
 
 template <class Cfg>
@@ -371,7 +386,7 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
   float acc[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) acc[v] = 0.f;
-  uint32_t cur = ~0u;
+  uint32_t cur = 0;  // slot 0, zero accumulators (see tacc_switch)
 
   int64_t lo = so[0], hi = so[1];
   for (int c = 0; c < nchunks; ++c) {
@@ -391,7 +406,7 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
     lo = hi;
     hi = hi_next;
   }
-  if (cur != ~0u) tmem_st<V>(tacc + cur * V, acc);
+  tmem_st<V>(tacc + cur * V, acc);
   tmem_wait_st();
 
   // read back and single write of the tile: slot s, value v at column s*V + v
