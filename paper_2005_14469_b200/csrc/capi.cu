@@ -317,6 +317,7 @@ void build_plan(SpdmPlan& P, const DevGcoo<float>& a, cudaStream_t s, int64_t mi
   const int64_t bound = nseg * (Cfg::TABLE + Cfg::NW * Cfg::HDR) + (int64_t)Cfg::REC * a.nnz + 16;
   P.ent = DevBuf<unsigned char>(bound, s);
   DevBuf<int64_t> slot_pos(nseg * Cfg::NW * Cfg::RW, s);
+  DevBuf<uint32_t> woff(TACC ? nseg * Cfg::NW : 0, s);  // warp segment offsets inside a segment
 
   const int64_t init_n = std::max<int64_t>((int64_t)cnt.count, TACC ? std::max<int64_t>(a.m, (int64_t)P.row_of.count) : 0);
   GCOO_LAUNCH_PDL(plan_init_kernel, grid_for(init_n, 256), 256, 0, s, cnt.get(), (int64_t)cnt.count,
@@ -342,14 +343,15 @@ void build_plan(SpdmPlan& P, const DevGcoo<float>& a, cudaStream_t s, int64_t mi
   }
   if constexpr (TACC)
     GCOO_LAUNCH_PDL(tacc_size_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, (const uint32_t*)cnt.get(), units,
-                    nchunks, nseg, seg_len.get());
+                    nchunks, nseg, seg_len.get(), woff.get());
   else
     GCOO_LAUNCH_PDL(tile_size_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, (const uint32_t*)cnt.get(), units,
                     nchunks, nseg, seg_len.get());
   exclusive_scan(seg_len.get(), P.seg_off.get(), nseg, s, scan_tmp.get());
   if constexpr (TACC) {
-    GCOO_LAUNCH_PDL(tacc_header_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, (const uint32_t*)cnt.get(), units,
-                    nchunks, nseg, (const int64_t*)P.seg_off.get(), P.ent.get(), slot_pos.get());
+    GCOO_LAUNCH_PDL(tacc_header_kernel<Cfg>, grid_for(nseg * Cfg::NW * Cfg::RW, 256), 256, 0, s,
+                    (const uint32_t*)cnt.get(), units, nchunks, nseg, (const int64_t*)P.seg_off.get(),
+                    (const uint32_t*)woff.get(), P.ent.get(), slot_pos.get());
     if (a.nnz > 0)
       GCOO_LAUNCH_PDL(tacc_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols,
                       a.gidx, nchunks, (const int64_t*)slot_pos.get(), P.ent.get(), (const int32_t*)P.unit_of.get());

@@ -112,62 +112,65 @@ __device__ __forceinline__ uint32_t tacc_warp_records(const uint32_t* __restrict
   return r;
 }
 
-// P2: one warp per (rb, c): segment length (table + warp segments).
+// P2: one warp per (rb, c): segment length (table + warp segments) and each
+// warp segment's offset inside the segment.
 template <class Cfg>
 __global__ void tacc_size_kernel(const uint32_t* __restrict__ cnt, int64_t units, int nchunks, int64_t nseg,
-                                 int64_t* __restrict__ seg_len) {
+                                 int64_t* __restrict__ seg_len, uint32_t* __restrict__ woff) {
   griddep_wait();  // PDL: predecessor complete
   const int lane = threadIdx.x & 31;
   for (int64_t x = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < nseg;
        x += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t rb = x / nchunks;
     const int c = (int)(x % nchunks);
-    uint32_t sz = lane < Cfg::NW
-                      ? Cfg::HDR + Cfg::REC * tacc_warp_records<Cfg>(cnt, units, nchunks, rb * Cfg::NW + lane, c)
-                      : 0u;
-#pragma unroll
-    for (int d = 16; d; d >>= 1) sz += __shfl_xor_sync(0xffffffffu, sz, d);
-    if (lane == 0) seg_len[x] = Cfg::TABLE + sz;
-  }
-}
-
-// P4: one warp per (rb, c): warp offset table, per-warp record counts, the
-// "absent second entry" marks, and the stream position of every (warp, slot)
-// record run for the scatter.
-template <class Cfg>
-__global__ void tacc_header_kernel(const uint32_t* __restrict__ cnt, int64_t units, int nchunks, int64_t nseg,
-                                   const int64_t* __restrict__ seg_off, unsigned char* __restrict__ ent,
-                                   int64_t* __restrict__ slot_pos) {
-  griddep_wait();  // PDL: predecessor complete
-  const int lane = threadIdx.x & 31;
-  for (int64_t x = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < nseg;
-       x += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t rb = x / nchunks;
-    const int c = (int)(x % nchunks);
-    const int64_t u = rb * Cfg::NW + lane;
-    const uint32_t nrec = lane < Cfg::NW ? tacc_warp_records<Cfg>(cnt, units, nchunks, u, c) : 0u;
-    const uint32_t sz = lane < Cfg::NW ? Cfg::HDR + Cfg::REC * nrec : 0u;
+    const uint32_t sz = lane < Cfg::NW
+                            ? Cfg::HDR + Cfg::REC * tacc_warp_records<Cfg>(cnt, units, nchunks, rb * Cfg::NW + lane, c)
+                            : 0u;
     uint32_t incl = sz;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
       if (lane >= d) incl += y;
     }
-    if (lane < Cfg::NW) {
-      const uint32_t woff = Cfg::TABLE + incl - sz;
+    if (lane < Cfg::NW) woff[x * Cfg::NW + lane] = Cfg::TABLE + incl - sz;
+    if (lane == 31) seg_len[x] = Cfg::TABLE + incl;
+  }
+}
+
+// P4: one thread per (segment, warp, slot): the stream position of the slot's
+// record run (for the scatter) and its "absent second entry" marks; the
+// slot-0 thread also writes the warp's offset-table entry and record count.
+template <class Cfg>
+__global__ void tacc_header_kernel(const uint32_t* __restrict__ cnt, int64_t units, int nchunks, int64_t nseg,
+                                   const int64_t* __restrict__ seg_off, const uint32_t* __restrict__ woff,
+                                   unsigned char* __restrict__ ent, int64_t* __restrict__ slot_pos) {
+  griddep_wait();  // PDL: predecessor complete
+  const int64_t total = nseg * Cfg::NW * Cfg::RW;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(t % Cfg::RW);
+    const int64_t xw = t / Cfg::RW;  // segment * NW + warp
+    const int w = (int)(xw % Cfg::NW);
+    const int64_t x = xw / Cfg::NW;
+    const int64_t rb = x / nchunks;
+    const int c = (int)(x % nchunks);
+    const int64_t u = rb * Cfg::NW + w;
+    const uint32_t* p = cnt + (u * nchunks + c) * Cfg::RW;
+    uint32_t before = 0;
+    if (u < units)
+      for (int q = 0; q < s; ++q) before += (p[q] + 1) >> 1;
+    const uint32_t ns = u < units ? (p[s] + 1) >> 1 : 0u;
+    const uint32_t wo = woff[xw];
+    const int64_t pos = seg_off[x] + wo + Cfg::HDR + (int64_t)Cfg::REC * before;
+    slot_pos[t] = pos;
+    uint32_t* rec = reinterpret_cast<uint32_t*>(ent + pos);
+    for (uint32_t j = 0; j < ns; ++j) rec[4 * j + 3] = ~0u;  // overwritten when the entry exists
+    if (s == 0) {
+      uint32_t nrec = 0;
+      if (u < units)
+        for (int q = 0; q < Cfg::RW; ++q) nrec += (p[q] + 1) >> 1;
       unsigned char* seg = ent + seg_off[x];
-      reinterpret_cast<uint32_t*>(seg)[lane] = woff;
-      *reinterpret_cast<uint4*>(seg + woff) = make_uint4(nrec, 0u, 0u, 0u);
-      int64_t pos = seg_off[x] + woff + Cfg::HDR;
-      int64_t* sp = slot_pos + (x * Cfg::NW + lane) * Cfg::RW;
-      const uint32_t* p = cnt + (u * nchunks + c) * Cfg::RW;
-      for (int s = 0; s < Cfg::RW; ++s) {
-        const uint32_t ns = u < units ? (p[s] + 1) >> 1 : 0u;
-        sp[s] = pos;
-        uint32_t* rec = reinterpret_cast<uint32_t*>(ent + pos);
-        for (uint32_t j = 0; j < ns; ++j) rec[4 * j + 3] = ~0u;  // overwritten when the entry exists
-        pos += (int64_t)Cfg::REC * ns;
-      }
+      reinterpret_cast<uint32_t*>(seg)[w] = wo;
+      *reinterpret_cast<uint4*>(seg + wo) = make_uint4(nrec, 0u, 0u, 0u);
     }
   }
 }
