@@ -399,7 +399,7 @@ int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const 
                      : density >= 0.075    ? 14
                      : density >= 0.035    ? 13
                      : density >= 0.017    ? 12
-                     : density >= 0.0015   ? 11
+                     : density >= 0.0025   ? 11
                                            : 8;
     switch (pick) {
       case 5: return tile_fits<TileV4>(a, n, ldb, ldc, B, C) ? 5 : 0;
