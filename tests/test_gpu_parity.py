@@ -431,6 +431,47 @@ def test_large_configs_sampled_rows_bit_exact(gcoo, cuda, oracle, case):
     assert np.array_equal(c_gpu, c_ref)
 
 
+@pytest.mark.slow
+def test_output_beyond_2g_elements_bit_exact(gcoo, cuda, oracle):
+    """C with more than 2^31 elements (70000 x 40000 fp32 = 11.2 GB): 64-bit
+    offsets in the planner, TMA coordinates and the epilogue; sampled rows
+    (first, last, random) x columns (incl. the last) equal the oracle bit for
+    bit, for the default kernel and a dense-regime configuration."""
+    import torch
+    m, k, n = 70000, 512, 40000
+    rng = np.random.default_rng(77)
+    nnz = 700000
+    flat = np.unique(rng.integers(0, m * k, size=nnz * 2, dtype=np.int64))[:nnz]
+    rng.shuffle(flat)
+    flat = np.sort(flat)
+    r = (flat // k).astype(np.int32)
+    c = (flat % k).astype(np.int32)
+    v = (1.0 - rng.random(r.size)).astype(np.float32)
+    dg = gcoo.coo_to_gcoo_dev(m, k, torch.from_numpy(v).cuda(), torch.from_numpy(r).cuda(), torch.from_numpy(c).cuda(), 4)
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    dB = 1.0 - torch.rand((k, n), device="cuda", dtype=torch.float32, generator=gen)
+    dC = torch.empty((m, n), device="cuda", dtype=torch.float32)
+    rows = np.unique(np.concatenate([[0, m - 1], rng.choice(m, 30, replace=False)]))
+    cols = np.unique(np.concatenate([[0, n - 1], rng.choice(n, 100, replace=False)]))
+    sel = np.isin(r, rows)
+    remap = {int(x): i for i, x in enumerate(rows)}
+    a_sub = np.zeros((len(rows), k), np.float32)
+    a_sub[[remap[int(x)] for x in r[sel]], c[sel]] = v[sel]
+    b_sub = np.ascontiguousarray(dB[:, torch.from_numpy(cols).cuda()].cpu().numpy())
+    c_ref, _ = oracle.spdm(oracle.dense_to_gcoo(a_sub, 4), b_sub, 64, fma=True)
+    for kern in ("auto", "tacc28_k64"):
+        gcoo.force_kernel(kern)
+        try:
+            dC.fill_(float("nan"))
+            gcoo.spdm_gcoo_dev(dg, dB, dC)
+            torch.cuda.synchronize()
+        finally:
+            gcoo.force_kernel("auto")
+        c_gpu = dC[torch.from_numpy(rows).cuda()][:, torch.from_numpy(cols).cuda()].cpu().numpy()
+        assert np.array_equal(c_gpu, c_ref), kern
+    del dC
+
+
 @pytest.mark.parametrize("kernel", ["tacc_v4", "tacc_v4w", "tacc_v2", "tacc28_k192", "tacc28_k64"])
 def test_heavy_rows_balanced_placement(gcoo, cuda, oracle, kernel):
     """The TMEM kernels place rows heaviest-first across warps (a permutation
