@@ -14,10 +14,10 @@
 //     chunk and all its RB rows' nonzeros in the chunk read it, so the L2->SM
 //     bytes per FMA are 4 / (RB * density): RB must be large.  Register-held
 //     accumulators cap RB*W at ~30K; here they live in TMEM (128 lanes x 512
-//     columns = 64K fp32 per SM), so RB doubles: 16 consumer warps, warp w
-//     owns TMEM lane quadrant w%4 and 128 columns = RW = 128/V rows x V
-//     columns per lane.  V=4: W=128, RB=512; V=2: W=64, RB=1024; V=1: W=32,
-//     RB=2048.
+//     columns = 64K fp32 per SM), so RB doubles: NW consumer warps (16, 24 or
+//     28), warp w owns TMEM lane quadrant w%4 and TCOLS = 512/(NW/4) columns
+//     = RW = TCOLS/V rows x V columns per lane.  V=4, 28 warps: W=128, RB=504
+//     (the default); 16 warps: RB=512; V=2: W=64, RB=1024.
 //   * A warp walks its chunk's records in one flat loop: a record carries up
 //     to two entries of one row slot {v0, v1, off0 | slot << 24, off1}.  The
 //     slot's V accumulators are pulled into registers from TMEM
@@ -27,7 +27,9 @@
 //     accumulator arrays.
 //   * Producer warp: per chunk one 2-D TMA of the B tile and one 1-D bulk copy
 //     of the CTA's record segment into a STAGES-deep ring (mbarrier
-//     complete_tx); consumers release a stage with one arrive per warp.
+//     complete_tx); consumers release a stage with one arrive per warp.  The
+//     chunk depth KC is matched to the density so that a chunk's records fit
+//     the stage (choose_kind in capi.cu).
 //
 // Per C element the FMAs run over the row's nonzeros in ascending column
 // order (chunks in order, a (row, chunk)'s entries in column order), one
@@ -72,18 +74,18 @@ struct TaccCfg {
 };
 
 //                      V  KC   S  CAP
-using TaccV4 = TaccCfg<4, 192, 2, 16384>;   // W=128, RB=512 : density >~ 2%
-using TaccV2 = TaccCfg<2, 256, 2, 16384>;   // W=64,  RB=1024: density ~ 1%
-using TaccV4W = TaccCfg<4, 192, 2, 16384, 24>;  // W=128, RB=480, 24 consumer warps (more latency hiding)
+using TaccV4 = TaccCfg<4, 192, 2, 16384>;   // W=128, RB=512, 16 warps: the sparse end (density < 0.25 %)
+using TaccV2 = TaccCfg<2, 256, 2, 16384>;   // W=64,  RB=1024 (tests / measurements only)
+using TaccV4W = TaccCfg<4, 192, 2, 16384, 24>;  // W=128, RB=480, 24 warps (previous default; tests / measurements)
 // 28 consumer warps (RB=504): the chunk depth KC trades run length (swaps per
 // entry) against the record-stage capacity, which must hold a row block's
 // records for one chunk (an oversize segment is read from global memory):
 // denser matrices take shallower chunks and bigger record stages.
-using Tacc28K192 = TaccCfg<4, 192, 2, 16384, 28>;  // density < 1.5 %
-using Tacc28K160 = TaccCfg<4, 160, 2, 32768, 28>;  //         < 3.5 %
-using Tacc28K128 = TaccCfg<4, 128, 2, 49152, 28>;  //         < 7 %
-using Tacc28K96 = TaccCfg<4, 96, 2, 65536, 28>;    //         < 12 %
-using Tacc28K64 = TaccCfg<4, 64, 2, 81920, 28>;    //         >= 12 %
+using Tacc28K192 = TaccCfg<4, 192, 2, 16384, 28>;  // density 0.25 % .. 1.7 %
+using Tacc28K160 = TaccCfg<4, 160, 2, 32768, 28>;  //         .. 3.5 %
+using Tacc28K128 = TaccCfg<4, 128, 2, 49152, 28>;  //         .. 7.5 %
+using Tacc28K96 = TaccCfg<4, 96, 2, 65536, 28>;    //         .. 16 %
+using Tacc28K64 = TaccCfg<4, 64, 2, 81920, 28>;    //         >= 16 %
 
 // ---------------------------------------------------------------- planner --
 // P1: per (unit u = row / RW, chunk, slot = row % RW) entry counts.
