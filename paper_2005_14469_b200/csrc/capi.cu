@@ -162,8 +162,8 @@ void exclusive_scan(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s, 
   if (tiles > 1) {
     exclusive_scan(sums, sums_scan, tiles, s, scratch + 2 * tiles + 1);
     GCOO_LAUNCH_PDL(add_tile_offsets_kernel, (unsigned)ceil_div(n, 256), 256, 0, s, out, n, (const int64_t*)sums_scan);
+    GCOO_LAUNCH_PDL(write_total_kernel, 1, 1, 0, s, in, out, n);
   }
-  GCOO_LAUNCH_PDL(write_total_kernel, 1, 1, 0, s, in, out, n);
 }
 
 void exclusive_scan(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s) {

@@ -73,7 +73,10 @@ scan_tiles_kernel(const int64_t* __restrict__ in, int64_t* __restrict__ out, int
     if (base + i < n) out[base + i] = run;
     run += v[i];
   }
-  if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+  if (threadIdx.x == 0) {
+    tile_sums[blockIdx.x] = total;
+    if (gridDim.x == 1) out[n] = total;  // single tile: the total is final (no write_total launch)
+  }
 }
 
 __global__ void add_tile_offsets_kernel(int64_t* __restrict__ out, int64_t n,
