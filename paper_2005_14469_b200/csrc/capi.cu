@@ -629,16 +629,21 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
   const bool perm = tile_order ? tile_order_is_permutation(tile_order, tile_count) : true;
   cudaStream_t s = thread_stream();
   const int64_t W = perm ? pipeline_strip(m, k, n) : 0;
-  // pipelined path: strip buffers first, so B strip 0 can start crossing PCIe
-  // while A is uploaded and planned on the compute stream
+  // pipelined path: every buffer first; then A crosses PCIe ahead of B strip 0
+  // on the H2D stream (the planner and strip 0's multiply need it first), so
+  // the D2H direction can start as early as possible
   const int nb = W ? NBUF : 0;
   std::vector<DevBuf<T>> dBv, dCv;
   for (int b = 0; b < nb; ++b) {
     dBv.emplace_back(k * W, s);
     dCv.emplace_back(m * W, s);
   }
-  // events: 0 buffers ready, then per ring slot b: in_done 1+b, cmp_done 1+NBUF+b, out_done 1+2*NBUF+b
-  Events ev(W ? 1 + 3 * NBUF : 0);
+  DevBuf<T> d_vals(nnz, s);
+  DevBuf<int32_t> d_rows(nnz, s), d_cols(nnz, s);
+  DevBuf<int64_t> d_gidx(groups, s), d_gnnz(groups, s);
+  // events: 0 buffers ready, then per ring slot b: in_done 1+b, cmp_done 1+NBUF+b,
+  // out_done 1+2*NBUF+b; 1+3*NBUF: A uploaded
+  Events ev(W ? 2 + 3 * NBUF : 0);
   auto in_done = [&](int b) { return ev[1 + b]; };
   auto cmp_done = [&](int b) { return ev[1 + NBUF + b]; };
   auto out_done = [&](int b) { return ev[1 + 2 * NBUF + b]; };
@@ -662,15 +667,17 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
     GCOO_CUDA(cudaEventRecord(in_done(b), s_in));
     if (trace) trace->mark(s_in, 2, j);
   };
-  if (W) h2d_strip(0);
-  DevBuf<T> d_vals(nnz, s);
-  DevBuf<int32_t> d_rows(nnz, s), d_cols(nnz, s);
-  DevBuf<int64_t> d_gidx(groups, s), d_gnnz(groups, s);
-  h2d(d_vals.get(), values, nnz, s);
-  h2d(d_rows.get(), row_idx, nnz, s);
-  h2d(d_cols.get(), col_idx, nnz, s);
-  h2d(d_gidx.get(), g_idxes, groups, s);
-  h2d(d_gnnz.get(), gnnz, groups, s);
+  cudaStream_t s_a = W ? s_in : s;
+  h2d(d_vals.get(), values, nnz, s_a);
+  h2d(d_rows.get(), row_idx, nnz, s_a);
+  h2d(d_cols.get(), col_idx, nnz, s_a);
+  h2d(d_gidx.get(), g_idxes, groups, s_a);
+  h2d(d_gnnz.get(), gnnz, groups, s_a);
+  if (W) {
+    GCOO_CUDA(cudaEventRecord(ev[1 + 3 * NBUF], s_in));
+    GCOO_CUDA(cudaStreamWaitEvent(s, ev[1 + 3 * NBUF], 0));
+    h2d_strip(0);
+  }
   DevGcoo<T> a{m, k, nnz, groups, a_p, d_vals.get(), d_rows.get(), d_cols.get(), d_gidx.get(), d_gnnz.get()};
   if (W == 0) {
     DevBuf<T> d_B(k * n, s), d_C(m * n, s);
