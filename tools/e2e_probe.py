@@ -29,10 +29,12 @@ gp = G.GcooMatrix(g.rows_dim, g.cols_dim, g.p, pin(g.values), pin(g.row_idx), pi
                   pin(g.nnz_per_group))
 bp = pin(b)
 cp = pin(np.empty((n, n), np.float32))
-for strips in (1, 8, 16, 32, 64):
+for strips in (1, 8, 12, 16, 24, 32, 64):
     G.lib().gcoo_debug_pipeline_strips(strips)
     G.spdm_gcoo(gp, bp, out=cp)
-    t = time.perf_counter()
-    for _ in range(5):
+    ts = []
+    for _ in range(7):
+        t = time.perf_counter()
         G.spdm_gcoo(gp, bp, out=cp)
-    print("strips", strips, "ms", round((time.perf_counter() - t) / 5 * 1e3, 3))
+        ts.append(time.perf_counter() - t)
+    print("strips", strips, "median ms", round(sorted(ts)[3] * 1e3, 3))
