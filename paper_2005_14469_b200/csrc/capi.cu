@@ -390,6 +390,9 @@ template <typename T>
 int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const T* B, const T* C, int flavor) {
   if constexpr (std::is_same<T, float>::value) {
     if (flavor == GCOO_FLAVOR_MUL_ADD || g_force_kernel == 0 || a.m == 0) return 0;
+    // small products: the planner (~35 us) costs more than it saves, the
+    // row-tile kernel needs none (profiles/r01_small_n.jsonl: n <= 2000)
+    if (g_force_kernel < 0 && 2.0 * (double)a.nnz * (double)n < 4e8) return 0;
     const double density = (double)a.nnz / ((double)a.m * (double)a.k);
     // measured crossovers at n=8000 (profiles/r01_kernel_sweep_28w.jsonl): TMEM accumulators
     // with 28 warps everywhere, the chunk depth shrinking as the density grows (the record
@@ -417,8 +420,9 @@ int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const 
   return 0;
 }
 
-// strip_n > 0: the plan will serve column strips of that width (host pipeline)
-// — TMEM kernels then spread rows over enough blocks for one full wave.
+// strip_n > 0: the plan will serve B/C of that width (a direct call, or the
+// column strips of the host pipeline) — when that grid is smaller than one
+// wave, TMEM kernels spread A's rows over enough row blocks to fill the GPU.
 template <typename T>
 void make_plan(SpdmPlan& P, const DevGcoo<T>& a, int kind, cudaStream_t s, int64_t strip_n = 0) {
   P.kind = kind;
@@ -460,7 +464,8 @@ void launch_spdm(const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C, 
                  cudaStream_t s) {
   if (a.m == 0 || n == 0) return;
   SpdmPlan P;
-  make_plan<T>(P, a, choose_kind<T>(a, n, ldb, ldc, B, C, flavor), s);
+  // strip_n = n: a grid smaller than one wave spreads A's rows over more row blocks
+  make_plan<T>(P, a, choose_kind<T>(a, n, ldb, ldc, B, C, flavor), s, n);
   run_spdm<T>(P, a, n, B, ldb, C, ldc, flavor, s);
 }
 
