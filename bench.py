@@ -324,6 +324,20 @@ def run_ours(args):
                 traffic = tr.get("dram_bytes_per_launch")
         except Exception:
             pass
+    # the paper's argument, measured: where the multiply's bytes move (ncu --set full
+    # of the same launch, profiles/r01_ncu_tacc28_s0.99.json)
+    traffic_split = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_tacc28_s0.99.json")) as f:
+            nc = json.load(f)
+        if n == 8000 and s == 0.99:
+            dram = nc["dram_read_bytes"] + nc["dram_write_bytes"]
+            traffic_split = {"dram_bytes": int(dram), "l2_to_sm_bytes": int(nc["l2_read_bytes_from_sm"]),
+                             "shared_memory_bytes": int(nc["smem_wavefronts"] * 128),
+                             "shared_memory_busy_frac": round(nc["smem_wavefront_pct"] / 100, 3),
+                             "source": "ncu --set full, profiles/r01_ncu_tacc28_s0.99.json (LSU wavefronts x 128 B)"}
+    except Exception:  # noqa: BLE001
+        pass
     fp_peak, fp_src = fp32_peak_tflops()
     tflops = flops_rank / (kernel_ms * 1e-3) / 1e12
 
@@ -402,6 +416,7 @@ def run_ours(args):
                      "peak_source": hbm_src, "algorithmic_bytes_per_launch": int(cb),
                      "kernel_ms": round(kernel_ms, 4), "kernel_share_of_step": round(kernel_ms / ms_mean, 3),
                      "bytes_formula": "12*nnz + 16*ceil(m/p) + 4*k_nz*N + 4*m*N (SURVEY 8d)"},
+        "traffic_split": traffic_split,
         "roofline_fp32": {"achieved": round(tflops, 3), "peak": round(fp_peak, 2), "unit": "TFLOP/s",
                           "frac": round(tflops / fp_peak, 4), "peak_source": fp_src,
                           "note": "the path is an FP32 FFMA gather: this, not HBM, is its binding roofline"},
