@@ -851,13 +851,14 @@ void csr_to_gcoo_host(int64_t m, int64_t k, int32_t p, int64_t nnz, const T* val
   {
     DevBuf<unsigned long long> bad(1, s);
     GCOO_CUDA(cudaMemsetAsync(bad.get(), 0xff, sizeof(unsigned long long), s));
-    GCOO_LAUNCH(validate_csr_kernel, grid_for(m, 256), 256, 0, s, m, k, drp.get(), dc.get(), bad.get());
+    GCOO_LAUNCH(validate_csr_kernel, grid_for(m, 256), 256, 0, s, m, k, nnz, drp.get(), dc.get(), bad.get());
     unsigned long long h = 0;
     d2h(&h, bad.get(), 1, s);
     GCOO_CUDA(cudaStreamSynchronize(s));
-    if (h != ~0ull) {
-      if ((h & 1ull) == 0) einval("CsrMatrix: row_ptr not monotone");
-      einval("CsrMatrix: columns not strictly increasing (or out of range) in row " + std::to_string(h >> 1));
+    if (h != ~0ull) {  // the reference's messages (matrix.hpp:154-162)
+      if ((h & 3ull) == 0) einval("CsrMatrix: row_ptr not monotone");
+      if ((h & 3ull) == 1) einval("CsrMatrix: column out of range");
+      einval("CsrMatrix: columns not strictly increasing in row " + std::to_string(h >> 2));
     }
   }
   if (!is_pow2(p)) einval("csr_to_gcoo: p must be a power of two");

@@ -166,20 +166,24 @@ __global__ void merge_round_kernel(int64_t nnz, int64_t m, int t, const int64_t*
 
 // --------------------------------------------------------------- K5 -------
 // CsrMatrix::validate (matrix.hpp:122-165) after the host-side size checks:
-// first bad row (2*r: row_ptr not monotone, 2*r+1: column out of range or not
-// strictly increasing).
-__global__ void validate_csr_kernel(int64_t m, int64_t k, const int64_t* __restrict__ rp,
+// first bad row r and its first error, code 4r + kind (0: row_ptr not
+// monotone, 1: column out of range, 2: columns not strictly increasing),
+// checked in the reference's order.  A row whose range leaves [0, nnz) is
+// reported as non-monotone (row_ptr starts at 0 and ends at nnz, so some
+// offset decreases) and its columns are never read.
+__global__ void validate_csr_kernel(int64_t m, int64_t k, int64_t nnz, const int64_t* __restrict__ rp,
                                     const int32_t* __restrict__ cols, unsigned long long* first_bad) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t a = rp[r], b = rp[r + 1];
     unsigned long long code = ~0ull;
-    if (a > b) {
-      code = 2ull * (unsigned long long)r;
+    if (a > b || a < 0 || b > nnz) {
+      code = 4ull * (unsigned long long)r;
     } else {
       for (int64_t e = a; e < b; ++e) {
         const int32_t c = cols[e];
-        if (c < 0 || c >= k || (e > a && cols[e - 1] >= c)) { code = 2ull * (unsigned long long)r + 1ull; break; }
+        if (c < 0 || c >= k) { code = 4ull * (unsigned long long)r + 1ull; break; }
+        if (e > a && cols[e - 1] >= c) { code = 4ull * (unsigned long long)r + 2ull; break; }
       }
     }
     if (code != ~0ull) atomicMin(first_bad, code);

@@ -297,8 +297,15 @@ def test_coo_validation_errors(gcoo, cuda):
         gcoo.coo_to_gcoo(2, 2, np.ones(2, np.float32), np.array([1, 0]), np.array([0, 0]), 2)
     with pytest.raises(ValueError):
         gcoo.coo_to_gcoo(2, 2, np.ones(1, np.float32), np.array([0]), np.array([0]), 3)
-    with pytest.raises(ValueError):  # CSR non-monotone row_ptr (test_matrix.cpp:99-101)
+    with pytest.raises(ValueError, match="not monotone"):  # CSR non-monotone row_ptr (test_matrix.cpp:99-101)
         gcoo.csr_to_gcoo(2, 2, np.ones(1, np.float32), np.array([0]), np.array([0, 2, 1]), 2)
+    # the reference's CsrMatrix::validate messages and order (matrix.hpp:154-162)
+    with pytest.raises(ValueError, match="column out of range"):
+        gcoo.csr_to_gcoo(2, 3, np.ones(3, np.float32), np.array([0, 2, 7]), np.array([0, 1, 3]), 2)
+    with pytest.raises(ValueError, match="not strictly increasing in row 1"):
+        gcoo.csr_to_gcoo(3, 3, np.ones(4, np.float32), np.array([0, 2, 2, 1]), np.array([0, 1, 3, 4]), 2)
+    with pytest.raises(ValueError, match="not strictly increasing in row 0"):  # first bad element wins
+        gcoo.csr_to_gcoo(1, 3, np.ones(3, np.float32), np.array([2, 1, 9]), np.array([0, 3]), 2)
 
 
 def test_powerlaw_construction_and_multiply(gcoo, cuda, oracle):
