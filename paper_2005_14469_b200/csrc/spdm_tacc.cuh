@@ -48,7 +48,7 @@ namespace gcoo_b200 {
 
 __device__ __forceinline__ int64_t ceil_div_dev(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-template <int V_, int KC_, int STAGES_, int CAP_, int NW_ = 16>
+template <int V_, int KC_, int STAGES_, int CAP_, int NW_ = 16, int EPR_ = 2>
 struct TaccCfg {
   static constexpr int V = V_;             // floats per lane
   static constexpr int W = 32 * V_;        // columns per CTA strip
@@ -64,6 +64,10 @@ struct TaccCfg {
   static constexpr uint32_t STAGE_BYTES = BTILE + CAP_;
   static constexpr int HDR = 16;           // per-warp header: record count
   static constexpr int REC = 16;           // bytes per record
+  // entries per record: 2 = {v0, v1, off0 | slot<<24, off1} (byte offsets, ~0 = absent);
+  // 3 = {v0, v1, v2, r0 | r1<<8 | r2<<16 | slot<<24} (B row indices in the chunk, 0xFF = absent)
+  static constexpr int EPR = EPR_;
+  static_assert(EPR_ == 2 || (EPR_ == 3 && KC_ < 255), "record format");
   static constexpr int TABLE = (4 * NW_ + 15) & ~15;  // per-segment warp offset table (NW x u32)
   static constexpr size_t SMEM = (size_t)STAGES_ * STAGE_BYTES + 2 * STAGES_ * 8 + 16;
   static_assert(KC_ <= 256, "TMA box rows");
@@ -83,9 +87,12 @@ using TaccV4W = TaccCfg<4, 192, 2, 16384, 24>;  // W=128, RB=480, 24 warps (prev
 // denser matrices take shallower chunks and bigger record stages.
 using Tacc28K192 = TaccCfg<4, 192, 2, 16384, 28>;  // density 0.25 % .. 1.7 %
 using Tacc28K160 = TaccCfg<4, 160, 2, 32768, 28>;  //         .. 3.5 %
-using Tacc28K128 = TaccCfg<4, 128, 2, 49152, 28>;  //         .. 7.5 %
-using Tacc28K96 = TaccCfg<4, 96, 2, 65536, 28>;    //         .. 16 %
-using Tacc28K64 = TaccCfg<4, 64, 2, 81920, 28>;    //         >= 16 %
+// the dense-regime configurations pack three entries per record (long runs
+// fill them; -4..5 % at s <= 0.95), the sparse ones two (pairs of records in
+// flight matter more there)
+using Tacc28K128 = TaccCfg<4, 128, 2, 49152, 28, 3>;  //      .. 7.5 %
+using Tacc28K96 = TaccCfg<4, 96, 2, 65536, 28, 3>;    //      .. 16 %
+using Tacc28K64 = TaccCfg<4, 64, 2, 81920, 28, 3>;    //      >= 16 %
 
 // ---------------------------------------------------------------- planner --
 // P1: per (unit u = row / RW, chunk, slot = row % RW) entry counts.
@@ -110,7 +117,7 @@ __device__ __forceinline__ uint32_t tacc_warp_records(const uint32_t* __restrict
   const uint32_t* p = cnt + (u * nchunks + c) * Cfg::RW;
   uint32_t r = 0;
 #pragma unroll 8
-  for (int s = 0; s < Cfg::RW; ++s) r += (p[s] + 1) >> 1;
+  for (int s = 0; s < Cfg::RW; ++s) r += (p[s] + Cfg::EPR - 1) / Cfg::EPR;
   return r;
 }
 
@@ -159,17 +166,19 @@ __global__ void tacc_header_kernel(const uint32_t* __restrict__ cnt, int64_t uni
     const uint32_t* p = cnt + (u * nchunks + c) * Cfg::RW;
     uint32_t before = 0;
     if (u < units)
-      for (int q = 0; q < s; ++q) before += (p[q] + 1) >> 1;
-    const uint32_t ns = u < units ? (p[s] + 1) >> 1 : 0u;
+      for (int q = 0; q < s; ++q) before += (p[q] + Cfg::EPR - 1) / Cfg::EPR;
+    const uint32_t ns = u < units ? (p[s] + Cfg::EPR - 1) / Cfg::EPR : 0u;
     const uint32_t wo = woff[xw];
     const int64_t pos = seg_off[x] + wo + Cfg::HDR + (int64_t)Cfg::REC * before;
     slot_pos[t] = pos;
     uint32_t* rec = reinterpret_cast<uint32_t*>(ent + pos);
-    for (uint32_t j = 0; j < ns; ++j) rec[4 * j + 3] = ~0u;  // overwritten when the entry exists
+    // absent-entry marks, overwritten by the entries that exist
+    const uint32_t mark = Cfg::EPR == 3 ? 0x00FFFFFFu | ((uint32_t)s << 24) : ~0u;
+    for (uint32_t j = 0; j < ns; ++j) rec[4 * j + 3] = mark;
     if (s == 0) {
       uint32_t nrec = 0;
       if (u < units)
-        for (int q = 0; q < Cfg::RW; ++q) nrec += (p[q] + 1) >> 1;
+        for (int q = 0; q < Cfg::RW; ++q) nrec += (p[q] + Cfg::EPR - 1) / Cfg::EPR;
       unsigned char* seg = ent + seg_off[x];
       reinterpret_cast<uint32_t*>(seg)[w] = wo;
       *reinterpret_cast<uint4*>(seg + wo) = make_uint4(nrec, 0u, 0u, 0u);
@@ -203,10 +212,16 @@ __global__ void tacc_fill_kernel(int64_t nnz, int32_t p, const float* __restrict
     const int w = (int)(u % Cfg::NW);
     const uint32_t slot = (uint32_t)(ur % Cfg::RW);
     const int64_t base = slot_pos[((rb * nchunks + c) * Cfg::NW + w) * Cfg::RW + slot];
-    uint32_t* word = reinterpret_cast<uint32_t*>(ent + base + (int64_t)Cfg::REC * (rank >> 1));
-    const uint32_t off = (uint32_t)(col - lo_col) * (uint32_t)(Cfg::W * 4);
-    word[rank & 1] = __float_as_uint(vals[e]);
-    word[2 + (rank & 1)] = (rank & 1) ? off : (off | (slot << 24));
+    if constexpr (Cfg::EPR == 3) {
+      uint32_t* word = reinterpret_cast<uint32_t*>(ent + base + (int64_t)Cfg::REC * (rank / 3));
+      word[rank % 3] = __float_as_uint(vals[e]);
+      reinterpret_cast<unsigned char*>(word + 3)[rank % 3] = (unsigned char)(col - lo_col);  // slot byte: header
+    } else {
+      uint32_t* word = reinterpret_cast<uint32_t*>(ent + base + (int64_t)Cfg::REC * (rank >> 1));
+      const uint32_t off = (uint32_t)(col - lo_col) * (uint32_t)(Cfg::W * 4);
+      word[rank & 1] = __float_as_uint(vals[e]);
+      word[2 + (rank & 1)] = (rank & 1) ? off : (off | (slot << 24));
+    }
   }
 }
 
@@ -265,6 +280,34 @@ __device__ __forceinline__ void tacc_one(float (&acc)[Cfg::V], uint32_t& cur, ui
   tacc_switch<Cfg>(acc, cur, tacc, q.z >> 24);
   tacc_fma<V>(acc, __uint_as_float(q.x), b0);
   if (two) tacc_fma<V>(acc, __uint_as_float(q.y), b1);
+}
+
+// Three-entry records (dense regime: long runs fill them): B row r of the
+// staged tile sits at r * W * 4 bytes; one record per step.
+template <class Cfg, bool GLOBAL>
+__device__ __forceinline__ void tacc_consume3(float (&acc)[Cfg::V], uint32_t& cur, uint32_t tacc,
+                                             typename RecSrc<GLOBAL>::addr_t seg, int warp, uint32_t bbase) {
+  using Src = RecSrc<GLOBAL>;
+  constexpr int V = Cfg::V;
+  constexpr uint32_t ROWB = Cfg::W * 4;
+  asm volatile("mov.b32 %0, %0;" : "+r"(bbase));
+  const uint32_t woff = Src::ld32(seg + 4 * warp);
+  const auto wseg = seg + woff;
+  const uint32_t nrec = Src::ld32(wseg);
+  auto rec = wseg + Cfg::HDR;
+  for (uint32_t r = 0; r < nrec; ++r, rec += Cfg::REC) {
+    const uint4 q = Src::ld(rec);
+    const uint32_t r0 = q.w & 0xffu, r1 = (q.w >> 8) & 0xffu, r2 = (q.w >> 16) & 0xffu;
+    const bool h1 = r1 != 0xffu, h2 = r2 != 0xffu;
+    float b0[V], b1[V], b2[V];
+    lds_vec<V>(bbase + r0 * ROWB, b0);
+    if (h1) lds_vec<V>(bbase + r1 * ROWB, b1);
+    if (h2) lds_vec<V>(bbase + r2 * ROWB, b2);
+    tacc_switch<Cfg>(acc, cur, tacc, q.w >> 24);
+    tacc_fma<V>(acc, __uint_as_float(q.x), b0);
+    if (h1) tacc_fma<V>(acc, __uint_as_float(q.y), b1);
+    if (h2) tacc_fma<V>(acc, __uint_as_float(q.z), b2);
+  }
 }
 
 // One warp walks its records for one chunk, two records per step (both
@@ -402,9 +445,15 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
     const uint32_t stage = smem0 + (uint32_t)s_idx * Cfg::STAGE_BYTES;
     const uint32_t bbase = stage + (uint32_t)(lane * V * 4);
     if (hi - lo <= (int64_t)Cfg::CAP) {
-      tacc_consume<Cfg, false>(acc, cur, tacc, stage + Cfg::BTILE, warp, bbase);
+      if constexpr (Cfg::EPR == 3)
+        tacc_consume3<Cfg, false>(acc, cur, tacc, stage + Cfg::BTILE, warp, bbase);
+      else
+        tacc_consume<Cfg, false>(acc, cur, tacc, stage + Cfg::BTILE, warp, bbase);
     } else {
-      tacc_consume<Cfg, true>(acc, cur, tacc, ent + lo, warp, bbase);
+      if constexpr (Cfg::EPR == 3)
+        tacc_consume3<Cfg, true>(acc, cur, tacc, ent + lo, warp, bbase);
+      else
+        tacc_consume<Cfg, true>(acc, cur, tacc, ent + lo, warp, bbase);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s_idx]);
