@@ -398,9 +398,9 @@ int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const 
     // with 28 warps everywhere, the chunk depth shrinking as the density grows (the record
     // stage must hold a chunk's records); 16 warps at the sparse end
     const int pick = g_force_kernel > 0    ? g_force_kernel
-                     : density >= 0.16     ? 15
-                     : density >= 0.075    ? 14
-                     : density >= 0.035    ? 13
+                     : density >= 0.3      ? 15
+                     : density >= 0.12     ? 14
+                     : density >= 0.06     ? 13
                      : density >= 0.017    ? 12
                      : density >= 0.0025   ? 11
                                            : 8;

@@ -85,14 +85,14 @@ using TaccV4W = TaccCfg<4, 192, 2, 16384, 24>;  // W=128, RB=480, 24 warps (prev
 // entry) against the record-stage capacity, which must hold a row block's
 // records for one chunk (an oversize segment is read from global memory):
 // denser matrices take shallower chunks and bigger record stages.
-using Tacc28K192 = TaccCfg<4, 192, 2, 16384, 28>;  // density 0.25 % .. 1.7 %
-using Tacc28K160 = TaccCfg<4, 160, 2, 32768, 28>;  //         .. 3.5 %
-// the dense-regime configurations pack three entries per record (long runs
-// fill them; -4..5 % at s <= 0.95), the sparse ones two (pairs of records in
-// flight matter more there)
-using Tacc28K128 = TaccCfg<4, 128, 2, 49152, 28, 3>;  //      .. 7.5 %
-using Tacc28K96 = TaccCfg<4, 96, 2, 65536, 28, 3>;    //      .. 16 %
-using Tacc28K64 = TaccCfg<4, 64, 2, 81920, 28, 3>;    //      >= 16 %
+using Tacc28K192 = TaccCfg<4, 192, 2, 16384, 28>;     // density 0.25 % .. 1.7 %
+// the denser configurations pack three entries per record (long runs fill
+// them; 3-10 % faster), the sparsest two (pairs of records in flight matter
+// more there)
+using Tacc28K160 = TaccCfg<4, 160, 2, 32768, 28, 3>;  //         .. 6 %
+using Tacc28K128 = TaccCfg<4, 128, 2, 49152, 28, 3>;  //         .. 12 %
+using Tacc28K96 = TaccCfg<4, 96, 2, 65536, 28, 3>;    //         .. 30 %
+using Tacc28K64 = TaccCfg<4, 64, 2, 81920, 28, 3>;    //      >= 30 %
 
 // ---------------------------------------------------------------- planner --
 // P1: per (unit u = row / RW, chunk, slot = row % RW) entry counts.
