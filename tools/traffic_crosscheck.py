@@ -37,14 +37,14 @@ def tiling(kernel_name):
     """RB, W, KC of the profiled kernel from its template arguments
     (TaccCfg<V, KC, STAGES, CAP, NW>: RB = NW * (512 / (NW/4) & ~7) / V; TileCfg: RB = 15 * 64 / V)."""
     import re
-    m = re.search(r"TaccCfg<(\d+), (\d+), \d+, \d+(?:, (\d+))?>", kernel_name)
+    m = re.search(r"TaccCfg<(\d+), (\d+), \d+, \d+(?:, (\d+))?(?:, (\d+))?>", kernel_name)
     if m:
-        v, kc, nw = int(m.group(1)), int(m.group(2)), int(m.group(3) or 16)
+        v, kc, nw, epr = int(m.group(1)), int(m.group(2)), int(m.group(3) or 16), int(m.group(4) or 2)
         tcols = (512 // (nw // 4)) & ~7
-        return dict(RB=nw * (tcols // v), W=32 * v, KC=kc)
+        return dict(RB=nw * (tcols // v), W=32 * v, KC=kc, EPR=epr)
     m = re.search(r"TileCfg<(\d+), (\d+),", kernel_name)
     v, kc = int(m.group(1)), int(m.group(2))
-    return dict(RB=15 * (64 // v), W=32 * v, KC=kc)
+    return dict(RB=15 * (64 // v), W=32 * v, KC=kc, EPR=2)
 
 
 def pow2_at_least(x):
@@ -71,12 +71,12 @@ def main():
         dp = G.dense_to_gcoo_dev(a, pow2_at_least(t["RB"]))
         tmodel = G.model_traffic_dev(dp, N, G.ExecConfig(p=dp.p, b=t["W"]), infinite_l2=True)
         del a, dp
-        # this kernel: records hold up to two entries of one row per chunk (count them exactly)
+        # this kernel: records hold up to EPR entries of one row per chunk (count them exactly)
         rows = d.row_idx.long()
         cols = d.col_idx.long()
         key = rows * ((N + t["KC"] - 1) // t["KC"]) + cols // t["KC"]
         per_run = torch.bincount(key)
-        records = int(((per_run + 1) // 2).sum())
+        records = int(((per_run + t["EPR"] - 1) // t["EPR"]).sum())
         col_tiles = (N + t["W"] - 1) // t["W"]
         row_blocks = (N + t["RB"] - 1) // t["RB"]
         b_tiles = row_blocks * col_tiles * N * t["W"] * 4
