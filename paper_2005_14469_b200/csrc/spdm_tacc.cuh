@@ -69,7 +69,8 @@ struct TaccCfg {
   static constexpr int EPR = EPR_;
   static_assert(EPR_ == 2 || (EPR_ == 3 && KC_ < 255), "record format");
   static constexpr int TABLE = (4 * NW_ + 15) & ~15;  // per-segment warp offset table (NW x u32)
-  static constexpr size_t SMEM = (size_t)STAGES_ * STAGE_BYTES + 2 * STAGES_ * 8 + 16;
+  // stages + full/empty barriers + TMEM address slot + per-stage segment offsets (int64) and lengths
+  static constexpr size_t SMEM = (size_t)STAGES_ * STAGE_BYTES + 2 * STAGES_ * 8 + 16 + STAGES_ * 16;
   static_assert(KC_ <= 256, "TMA box rows");
   static_assert(NW_ % 4 == 0 && NW_ <= 28 && TCOLS % 8 == 0 && 8 % V_ == 0, "warps tile the 4 TMEM lane quadrants");
   static_assert(BTILE < (1u << 24) && RW <= 256, "24-bit B offsets, 8-bit slots");
@@ -366,6 +367,10 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * Cfg::STAGE_BYTES);
   uint64_t* empty = full + S;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + S);
+  // the producer publishes each stage's record-segment offset and length here
+  // (ordered by the full barrier), so consumers never read seg_off
+  int64_t* stage_lo = reinterpret_cast<int64_t*>(tmem_slot + 4);
+  uint32_t* stage_len = reinterpret_cast<uint32_t*>(stage_lo + S);
   const uint32_t smem0 = smem_u32(smem_raw);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -414,6 +419,8 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
         const uint32_t bytes = len <= Cfg::CAP ? len : 0u;  // oversize: consumers read global memory
         if (c >= S) mbar_wait(&empty[s], (uint32_t)((c / S) - 1) & 1u);
         unsigned char* stage = smem_raw + (size_t)s * Cfg::STAGE_BYTES;
+        stage_lo[s] = lo;
+        stage_len[s] = len;
         mbar_arrive_expect_tx(&full[s], Cfg::BTILE + bytes);
         tma_load_2d(stage, &tmap_b, x, c * Cfg::KC, &full[s]);
         if (bytes) bulk_g2s(smem_u32(stage + Cfg::BTILE), ent + lo, bytes, &full[s]);
@@ -436,15 +443,14 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
   for (int v = 0; v < V; ++v) acc[v] = 0.f;
   uint32_t cur = 0;  // slot 0, zero accumulators (see tacc_switch)
 
-  int64_t lo = so[0], hi = so[1];
   for (int c = 0; c < nchunks; ++c) {
     const int s_idx = c % S;
-    const int64_t hi_next = so[c + 2 <= nchunks ? c + 2 : nchunks];  // prefetch
     mbar_wait(&full[s_idx], (uint32_t)(c / S) & 1u);
     tmem_wait_st();  // slots pushed during earlier chunks are complete before they are pulled again
     const uint32_t stage = smem0 + (uint32_t)s_idx * Cfg::STAGE_BYTES;
     const uint32_t bbase = stage + (uint32_t)(lane * V * 4);
-    if (hi - lo <= (int64_t)Cfg::CAP) {
+    const int64_t lo = stage_lo[s_idx];
+    if (stage_len[s_idx] <= Cfg::CAP) {
       if constexpr (Cfg::EPR == 3)
         tacc_consume3<Cfg, false>(acc, cur, tacc, stage + Cfg::BTILE, warp, bbase);
       else
@@ -457,8 +463,6 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s_idx]);
-    lo = hi;
-    hi = hi_next;
   }
   tmem_st<V>(tacc + cur * V, acc);
   tmem_wait_st();
