@@ -230,25 +230,30 @@ EncodeTiledFn encode_tiled() {
   return fn;
 }
 
-// B (k x n, leading dimension ldb) as a 2-D fp32 tensor; box = W columns x KC rows.
-CUtensorMap make_b_map(const float* B, int64_t k, int64_t n, int64_t ldb, int box_w, int box_k) {
+// B (k x n, leading dimension ldb) as a 2-D fp32/fp64 tensor; box = W columns x KC rows.
+template <typename T>
+CUtensorMap make_b_map(const T* B, int64_t k, int64_t n, int64_t ldb, int box_w, int box_k) {
   CUtensorMap map;
   const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)k};
-  const cuuint64_t strides[1] = {(cuuint64_t)ldb * sizeof(float)};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldb * sizeof(T)};
   const cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)box_k};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(B), dims, strides,
-                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+  const CUtensorMapDataType dt = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const CUresult r = encode_tiled()(&map, dt, 2, const_cast<T*>(B), dims, strides, box, estr,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(GCOO_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return map;
 }
 
 // ------------------------------------------------------- tile path ------
-template <class Cfg>
-bool tile_fits(const DevGcoo<float>& a, int64_t n, int64_t ldb, int64_t ldc, const float* B, const float* C) {
-  return ldb % 4 == 0 && ldc % Cfg::V == 0 && n % Cfg::V == 0 && (reinterpret_cast<uintptr_t>(B) % 16) == 0 &&
-         (reinterpret_cast<uintptr_t>(C) % (4 * Cfg::V)) == 0 && a.k <= (int64_t)INT32_MAX - Cfg::KC &&
+// The TMA/record kernels need 16-byte aligned B rows and C vectors.
+template <class Cfg, typename T>
+bool tile_fits(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const T* B, const T* C) {
+  constexpr int VE = Cfg::W / 32;  // elements per lane
+  constexpr int ALIGN_E = 16 / (int)sizeof(T);
+  return ldb % ALIGN_E == 0 && ldc % VE == 0 && n % VE == 0 && (reinterpret_cast<uintptr_t>(B) % 16) == 0 &&
+         (reinterpret_cast<uintptr_t>(C) % (sizeof(T) * VE)) == 0 && a.k <= (int64_t)INT32_MAX - Cfg::KC &&
          n <= INT32_MAX && a.m <= (int64_t)INT32_MAX;
 }
 
@@ -286,8 +291,8 @@ void set_smem_attr() {
 // `min_ctas` (TMEM kernels): spread rows over enough row blocks that a launch
 // over `col_tiles` column tiles has at least that many CTAs (narrow strips of
 // the host pipeline); 0 = full row blocks.
-template <class Cfg, bool TACC>
-void build_plan(SpdmPlan& P, const DevGcoo<float>& a, cudaStream_t s, int64_t min_ctas = 0, int64_t col_tiles = 1) {
+template <class Cfg, bool TACC, typename T>
+void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ctas = 0, int64_t col_tiles = 1) {
   set_smem_attr<Cfg, TACC>();
   P.row_blocks = ceil_div(a.m, Cfg::RB);
   int64_t rpb = Cfg::RB;
@@ -364,8 +369,8 @@ void build_plan(SpdmPlan& P, const DevGcoo<float>& a, cudaStream_t s, int64_t mi
   }
 }
 
-template <class Cfg, bool TACC>
-void run_plan(const SpdmPlan& P, const DevGcoo<float>& a, int64_t n, const float* B, int64_t ldb, float* C,
+template <class Cfg, bool TACC, typename T>
+void run_plan(const SpdmPlan& P, const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C,
               int64_t ldc, cudaStream_t s) {
   const CUtensorMap map = make_b_map(B, a.k, n, ldb, Cfg::W, Cfg::KC);
   const int64_t grid = P.row_blocks * ceil_div(n, Cfg::W);
@@ -416,6 +421,17 @@ int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const 
       case 15: return tile_fits<Tacc28K64>(a, n, ldb, ldc, B, C) ? 15 : 0;
       default: return 0;
     }
+  } else {  // fp64: TMEM kernels with one-entry records
+    if (flavor == GCOO_FLAVOR_MUL_ADD || g_force_kernel == 0 || a.m == 0) return 0;
+    if (g_force_kernel < 0 && 2.0 * (double)a.nnz * (double)n < 4e8) return 0;
+    const double density = (double)a.nnz / ((double)a.m * (double)a.k);
+    const int pick = g_force_kernel > 0 ? g_force_kernel : density >= 0.07 ? 22 : density >= 0.025 ? 21 : 20;
+    switch (pick) {
+      case 20: return tile_fits<Tacc28F64K160>(a, n, ldb, ldc, B, C) ? 20 : 0;
+      case 21: return tile_fits<Tacc28F64K96>(a, n, ldb, ldc, B, C) ? 21 : 0;
+      case 22: return tile_fits<Tacc28F64K64>(a, n, ldb, ldc, B, C) ? 22 : 0;
+      default: return 0;
+    }
   }
   return 0;
 }
@@ -437,6 +453,10 @@ void make_plan(SpdmPlan& P, const DevGcoo<T>& a, int kind, cudaStream_t s, int64
     if (kind == 13) build_plan<Tacc28K128, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K128::W));
     if (kind == 14) build_plan<Tacc28K96, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K96::W));
     if (kind == 15) build_plan<Tacc28K64, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K64::W));
+  } else {
+    if (kind == 20) build_plan<Tacc28F64K160, true>(P, a, s, wave, ceil_div(strip_n, Tacc28F64K160::W));
+    if (kind == 21) build_plan<Tacc28F64K96, true>(P, a, s, wave, ceil_div(strip_n, Tacc28F64K96::W));
+    if (kind == 22) build_plan<Tacc28F64K64, true>(P, a, s, wave, ceil_div(strip_n, Tacc28F64K64::W));
   }
 }
 
@@ -454,6 +474,10 @@ void run_spdm(const SpdmPlan& P, const DevGcoo<T>& a, int64_t n, const T* B, int
     if (P.kind == 13) return run_plan<Tacc28K128, true>(P, a, n, B, ldb, C, ldc, s);
     if (P.kind == 14) return run_plan<Tacc28K96, true>(P, a, n, B, ldb, C, ldc, s);
     if (P.kind == 15) return run_plan<Tacc28K64, true>(P, a, n, B, ldb, C, ldc, s);
+  } else {
+    if (P.kind == 20) return run_plan<Tacc28F64K160, true>(P, a, n, B, ldb, C, ldc, s);
+    if (P.kind == 21) return run_plan<Tacc28F64K96, true>(P, a, n, B, ldb, C, ldc, s);
+    if (P.kind == 22) return run_plan<Tacc28F64K64, true>(P, a, n, B, ldb, C, ldc, s);
   }
   if (flavor != GCOO_FLAVOR_MUL_ADD) launch_rowtile_p<T, true>(a, n, B, ldb, C, ldc, s);
   else launch_rowtile_p<T, false>(a, n, B, ldb, C, ldc, s);

@@ -48,10 +48,12 @@ namespace gcoo_b200 {
 
 __device__ __forceinline__ int64_t ceil_div_dev(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-template <int V_, int KC_, int STAGES_, int CAP_, int NW_ = 16, int EPR_ = 2>
+template <int V_, int KC_, int STAGES_, int CAP_, int NW_ = 16, int EPR_ = 2, class E_ = float>
 struct TaccCfg {
-  static constexpr int V = V_;             // floats per lane
-  static constexpr int W = 32 * V_;        // columns per CTA strip
+  using E = E_;                            // element type (float; double: two 32-bit cells)
+  static constexpr int V = V_;             // 32-bit cells per lane (= floats per lane)
+  static constexpr int VE = V_ * 4 / (int)sizeof(E_);  // elements per lane
+  static constexpr int W = 32 * VE;        // columns (elements) per CTA strip
   static constexpr int NW = NW_;           // consumer warps: NW/4 per TMEM lane quadrant
   static constexpr int TCOLS = (512 / (NW_ / 4)) & ~7;  // TMEM columns per warp (128 / 80 / 72 for 16 / 24 / 28 warps)
   static constexpr int RW = TCOLS / V_;    // rows (slots) per warp
@@ -59,15 +61,18 @@ struct TaccCfg {
   static constexpr int KC = KC_;           // B rows per chunk
   static constexpr int STAGES = STAGES_;
   static constexpr int THREADS = (NW + 1) * 32;
-  static constexpr uint32_t BTILE = (uint32_t)KC_ * W * 4;
+  static constexpr uint32_t ROWB = (uint32_t)W * sizeof(E_);  // bytes of one staged B row
+  static constexpr uint32_t BTILE = (uint32_t)KC_ * ROWB;
   static constexpr uint32_t CAP = CAP_;    // record-segment bytes per stage
   static constexpr uint32_t STAGE_BYTES = BTILE + CAP_;
   static constexpr int HDR = 16;           // per-warp header: record count
   static constexpr int REC = 16;           // bytes per record
   // entries per record: 2 = {v0, v1, off0 | slot<<24, off1} (byte offsets, ~0 = absent);
-  // 3 = {v0, v1, v2, r0 | r1<<8 | r2<<16 | slot<<24} (B row indices in the chunk, 0xFF = absent)
+  // 3 = {v0, v1, v2, r0 | r1<<8 | r2<<16 | slot<<24} (B row indices in the chunk, 0xFF = absent);
+  // 1 (double) = {lo(v), hi(v), off | slot<<24, 0}
   static constexpr int EPR = EPR_;
-  static_assert(EPR_ == 2 || (EPR_ == 3 && KC_ < 255), "record format");
+  static_assert((sizeof(E_) == 4 && (EPR_ == 2 || (EPR_ == 3 && KC_ < 255))) || (sizeof(E_) == 8 && EPR_ == 1),
+                "record format");
   static constexpr int TABLE = (4 * NW_ + 15) & ~15;  // per-segment warp offset table (NW x u32)
   // stages + full/empty barriers + TMEM address slot + per-stage segment offsets (int64) and lengths
   static constexpr size_t SMEM = (size_t)STAGES_ * STAGE_BYTES + 2 * STAGES_ * 8 + 16 + STAGES_ * 16;
@@ -94,6 +99,11 @@ using Tacc28K160 = TaccCfg<4, 160, 2, 32768, 28, 3>;  //         .. 6 %
 using Tacc28K128 = TaccCfg<4, 128, 2, 49152, 28, 3>;  //         .. 12 %
 using Tacc28K96 = TaccCfg<4, 96, 2, 65536, 28, 3>;    //         .. 30 %
 using Tacc28K64 = TaccCfg<4, 64, 2, 81920, 28, 3>;    //      >= 30 %
+// fp64 (the reference's GCOO_SCALAR_F64 build): 64 doubles per CTA strip,
+// 504 rows, one entry per 16-byte record
+using Tacc28F64K160 = TaccCfg<4, 160, 2, 32768, 28, 1, double>;  // density < 2.5 %
+using Tacc28F64K96 = TaccCfg<4, 96, 2, 65536, 28, 1, double>;    //         < 7 %
+using Tacc28F64K64 = TaccCfg<4, 64, 2, 81920, 28, 1, double>;    //         >= 7 %
 
 // ---------------------------------------------------------------- planner --
 // P1: per (unit u = row / RW, chunk, slot = row % RW) entry counts.
@@ -174,7 +184,7 @@ __global__ void tacc_header_kernel(const uint32_t* __restrict__ cnt, int64_t uni
     slot_pos[t] = pos;
     uint32_t* rec = reinterpret_cast<uint32_t*>(ent + pos);
     // absent-entry marks, overwritten by the entries that exist
-    const uint32_t mark = Cfg::EPR == 3 ? 0x00FFFFFFu | ((uint32_t)s << 24) : ~0u;
+    const uint32_t mark = Cfg::EPR == 3 ? 0x00FFFFFFu | ((uint32_t)s << 24) : Cfg::EPR == 1 ? 0u : ~0u;
     for (uint32_t j = 0; j < ns; ++j) rec[4 * j + 3] = mark;
     if (s == 0) {
       uint32_t nrec = 0;
@@ -191,7 +201,7 @@ __global__ void tacc_header_kernel(const uint32_t* __restrict__ cnt, int64_t uni
 // in the same chunk comes from the (col,row)-sorted group slice: the entries
 // of the chunk are contiguous there, so count same-row ones before it.
 template <class Cfg>
-__global__ void tacc_fill_kernel(int64_t nnz, int32_t p, const float* __restrict__ vals,
+__global__ void tacc_fill_kernel(int64_t nnz, int32_t p, const typename Cfg::E* __restrict__ vals,
                                  const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
                                  const int64_t* __restrict__ gidx, int nchunks,
                                  const int64_t* __restrict__ slot_pos, unsigned char* __restrict__ ent,
@@ -213,14 +223,20 @@ __global__ void tacc_fill_kernel(int64_t nnz, int32_t p, const float* __restrict
     const int w = (int)(u % Cfg::NW);
     const uint32_t slot = (uint32_t)(ur % Cfg::RW);
     const int64_t base = slot_pos[((rb * nchunks + c) * Cfg::NW + w) * Cfg::RW + slot];
-    if constexpr (Cfg::EPR == 3) {
+    if constexpr (Cfg::EPR == 1) {
+      uint32_t* word = reinterpret_cast<uint32_t*>(ent + base + (int64_t)Cfg::REC * rank);
+      const double v = (double)vals[e];
+      word[0] = (uint32_t)__double2loint(v);
+      word[1] = (uint32_t)__double2hiint(v);
+      word[2] = ((uint32_t)(col - lo_col) * Cfg::ROWB) | (slot << 24);
+    } else if constexpr (Cfg::EPR == 3) {
       uint32_t* word = reinterpret_cast<uint32_t*>(ent + base + (int64_t)Cfg::REC * (rank / 3));
-      word[rank % 3] = __float_as_uint(vals[e]);
+      word[rank % 3] = __float_as_uint((float)vals[e]);
       reinterpret_cast<unsigned char*>(word + 3)[rank % 3] = (unsigned char)(col - lo_col);  // slot byte: header
     } else {
       uint32_t* word = reinterpret_cast<uint32_t*>(ent + base + (int64_t)Cfg::REC * (rank >> 1));
-      const uint32_t off = (uint32_t)(col - lo_col) * (uint32_t)(Cfg::W * 4);
-      word[rank & 1] = __float_as_uint(vals[e]);
+      const uint32_t off = (uint32_t)(col - lo_col) * Cfg::ROWB;
+      word[rank & 1] = __float_as_uint((float)vals[e]);
       word[2 + (rank & 1)] = (rank & 1) ? off : (off | (slot << 24));
     }
   }
@@ -290,7 +306,7 @@ __device__ __forceinline__ void tacc_consume3(float (&acc)[Cfg::V], uint32_t& cu
                                              typename RecSrc<GLOBAL>::addr_t seg, int warp, uint32_t bbase) {
   using Src = RecSrc<GLOBAL>;
   constexpr int V = Cfg::V;
-  constexpr uint32_t ROWB = Cfg::W * 4;
+  constexpr uint32_t ROWB = Cfg::ROWB;
   asm volatile("mov.b32 %0, %0;" : "+r"(bbase));
   const uint32_t woff = Src::ld32(seg + 4 * warp);
   const auto wseg = seg + woff;
@@ -308,6 +324,48 @@ __device__ __forceinline__ void tacc_consume3(float (&acc)[Cfg::V], uint32_t& cu
     tacc_fma<V>(acc, __uint_as_float(q.x), b0);
     if (h1) tacc_fma<V>(acc, __uint_as_float(q.y), b1);
     if (h2) tacc_fma<V>(acc, __uint_as_float(q.z), b2);
+  }
+}
+
+// fp64 (one entry per record; a lane's two doubles are four TMEM/shared
+// cells): two records per step, DFMA on the reinterpreted cells.
+__device__ __forceinline__ void tacc_dfma(float (&acc)[4], double a, const float (&b)[4]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const double bv = __hiloint2double(__float_as_int(b[2 * h + 1]), __float_as_int(b[2 * h]));
+    const double av = __hiloint2double(__float_as_int(acc[2 * h + 1]), __float_as_int(acc[2 * h]));
+    const double r = __fma_rn(a, bv, av);
+    acc[2 * h] = __int_as_float(__double2loint(r));
+    acc[2 * h + 1] = __int_as_float(__double2hiint(r));
+  }
+}
+
+template <class Cfg, bool GLOBAL>
+__device__ __forceinline__ void tacc_consume1(float (&acc)[Cfg::V], uint32_t& cur, uint32_t tacc,
+                                              typename RecSrc<GLOBAL>::addr_t seg, int warp, uint32_t bbase) {
+  using Src = RecSrc<GLOBAL>;
+  static_assert(Cfg::V == 4, "two doubles per lane");
+  asm volatile("mov.b32 %0, %0;" : "+r"(bbase));
+  const uint32_t woff = Src::ld32(seg + 4 * warp);
+  const auto wseg = seg + woff;
+  const uint32_t nrec = Src::ld32(wseg);
+  auto rec = wseg + Cfg::HDR;
+  for (uint32_t r = 1; r < nrec; r += 2, rec += 2 * Cfg::REC) {
+    const uint4 qa = Src::ld(rec), qb = Src::ld(rec + Cfg::REC);
+    float ba[4], bb[4];
+    lds_vec<4>(bbase + (qa.z & 0xffffffu), ba);
+    lds_vec<4>(bbase + (qb.z & 0xffffffu), bb);
+    tacc_switch<Cfg>(acc, cur, tacc, qa.z >> 24);
+    tacc_dfma(acc, __hiloint2double((int)qa.y, (int)qa.x), ba);
+    tacc_switch<Cfg>(acc, cur, tacc, qb.z >> 24);
+    tacc_dfma(acc, __hiloint2double((int)qb.y, (int)qb.x), bb);
+  }
+  if (nrec & 1u) {
+    const uint4 q = Src::ld(rec);
+    float b[4];
+    lds_vec<4>(bbase + (q.z & 0xffffffu), b);
+    tacc_switch<Cfg>(acc, cur, tacc, q.z >> 24);
+    tacc_dfma(acc, __hiloint2double((int)q.y, (int)q.x), b);
   }
 }
 
@@ -360,7 +418,7 @@ __device__ __forceinline__ void tacc_consume(float (&acc)[Cfg::V], uint32_t& cur
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
 spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t n, const unsigned char* __restrict__ ent,
-                 const int64_t* __restrict__ seg_off, float* __restrict__ C, int64_t ldc, int64_t row_blocks,
+                 const int64_t* __restrict__ seg_off, typename Cfg::E* __restrict__ C, int64_t ldc, int64_t row_blocks,
                  int nchunks, const int32_t* __restrict__ row_of, const int32_t* __restrict__ skewed) {
   constexpr int W = Cfg::W, NW = Cfg::NW, S = Cfg::STAGES, V = Cfg::V, RW = Cfg::RW;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -451,12 +509,16 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
     const uint32_t bbase = stage + (uint32_t)(lane * V * 4);
     const int64_t lo = stage_lo[s_idx];
     if (stage_len[s_idx] <= Cfg::CAP) {
-      if constexpr (Cfg::EPR == 3)
+      if constexpr (Cfg::EPR == 1)
+        tacc_consume1<Cfg, false>(acc, cur, tacc, stage + Cfg::BTILE, warp, bbase);
+      else if constexpr (Cfg::EPR == 3)
         tacc_consume3<Cfg, false>(acc, cur, tacc, stage + Cfg::BTILE, warp, bbase);
       else
         tacc_consume<Cfg, false>(acc, cur, tacc, stage + Cfg::BTILE, warp, bbase);
     } else {
-      if constexpr (Cfg::EPR == 3)
+      if constexpr (Cfg::EPR == 1)
+        tacc_consume1<Cfg, true>(acc, cur, tacc, ent + lo, warp, bbase);
+      else if constexpr (Cfg::EPR == 3)
         tacc_consume3<Cfg, true>(acc, cur, tacc, ent + lo, warp, bbase);
       else
         tacc_consume<Cfg, true>(acc, cur, tacc, ent + lo, warp, bbase);
@@ -469,7 +531,7 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
 
   // read back and single write of the tile: slot s, value v at column s*V + v
   const int64_t row0 = (rb * NW + warp) * (int64_t)RW;
-  const int64_t j = ct * W + lane * V;
+  const int64_t j = ct * W + lane * Cfg::VE;  // first element (column) of this lane
 #pragma unroll 1
   for (int c0 = 0; c0 < Cfg::TCOLS; c0 += 8) {
     float r[8];
@@ -480,8 +542,8 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
       for (int k = 0; k < 8 / V; ++k) {
         const int64_t row = row_of[row0 + c0 / V + k];  // -1: padding slot
         if (row >= 0) {
-          float* dst = C + row * ldc + j;
-          if constexpr (V == 4) {
+          typename Cfg::E* dst = C + row * ldc + j;
+          if constexpr (V == 4) {  // 16 bytes: four floats or two doubles
             __stcs(reinterpret_cast<float4*>(dst), make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]));
           } else if constexpr (V == 2) {
             __stcs(reinterpret_cast<float2*>(dst), make_float2(r[2 * k], r[2 * k + 1]));

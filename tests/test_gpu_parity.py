@@ -138,6 +138,29 @@ def test_f64(gcoo, cuda, oracle):
         assert max_rel(c, exact) <= 1e-12
 
 
+@pytest.mark.parametrize("kernel", ["tacc28_f64_k160", "tacc28_f64_k96", "tacc28_f64_k64", "auto"])
+def test_f64_tmem_kernels_bit_exact(gcoo, cuda, oracle, kernel):
+    """fp64 through the TMEM kernels (two 32-bit cells per double, one entry
+    per record): edge shapes and p values, bit-exact against the oracle's
+    double FMA chain; "auto" on a product large enough to take them."""
+    rng = np.random.default_rng(53)
+    gcoo.force_kernel(kernel)
+    try:
+        shapes = [(1, 1, 2, 1, 1.0), (300, 200, 132, 4, 0.02), (777, 1000, 256, 1, 0.01), (513, 129, 68, 16, 0.2),
+                  (64, 4000, 512, 2, 0.003), (100, 100, 1024, 4, 0.0)]
+        if kernel == "auto":
+            shapes = [(3000, 2000, 512, 4, 0.05), (2000, 3000, 640, 8, 0.005)]
+        for m, k, n, p, dens in shapes:
+            a = rand_dense(rng, m, k, dens, np.float64)
+            bm = rand_dense(rng, k, n, 1.0, np.float64)
+            go = oracle.dense_to_gcoo(a, p)
+            c_ref, _ = oracle.spdm(go, bm, 64, fma=True)
+            c = gcoo.spdm_gcoo(to_prod(gcoo, go), bm, gcoo.ExecConfig(p=p))
+            assert np.array_equal(c, c_ref), (kernel, m, k, n, p)
+    finally:
+        gcoo.force_kernel("auto")
+
+
 def test_empty_and_full_operands(gcoo, cuda, oracle):
     # test_kernels.cpp:254-264
     ones = np.ones((16, 16), np.float32)
