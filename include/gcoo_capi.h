@@ -118,8 +118,8 @@ int gcoo_spdm_f64_dev(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, int
  * multiplies the same A by many B builds it once here.  A's device arrays must
  * stay alive and unchanged while the plan exists.  The plan's buffers are
  * stream-ordered on `stream`: multiplies on other streams must be ordered
- * after the create.  gcoo_plan_spdm_f32_dev is stream-ordered and returns the
- * same bits as gcoo_spdm_f32_dev (any B/C layout; an unaligned one is planned
+ * after the create.  gcoo_plan_spdm_*_dev is stream-ordered and returns the
+ * same bits as gcoo_spdm_*_dev (any B/C layout; an unaligned one is planned
  * per call).  gcoo_plan_destroy synchronises the device, then frees.
  */
 typedef struct gcoo_plan gcoo_plan;
@@ -128,6 +128,13 @@ int gcoo_plan_create_f32_dev(int64_t m, int64_t k, int32_t p, int64_t nnz, const
                              const int64_t* g_idxes, const int64_t* nnz_per_group, int flavor,
                              gcoo_plan** plan, void* stream);
 int gcoo_plan_spdm_f32_dev(const gcoo_plan* plan, int64_t n, const float* B, int64_t ldb, float* C,
+                           int64_t ldc, void* stream);
+/* fp64 twins (a plan serves only the element type it was built for). */
+int gcoo_plan_create_f64_dev(int64_t m, int64_t k, int32_t p, int64_t nnz, const double* values,
+                             const int32_t* row_idx, const int32_t* col_idx, int64_t groups,
+                             const int64_t* g_idxes, const int64_t* nnz_per_group, int flavor,
+                             gcoo_plan** plan, void* stream);
+int gcoo_plan_spdm_f64_dev(const gcoo_plan* plan, int64_t n, const double* B, int64_t ldb, double* C,
                            int64_t ldc, void* stream);
 int gcoo_plan_destroy(gcoo_plan* plan);
 

@@ -103,6 +103,9 @@ def lib():
     _sig(L, "gcoo_plan_create_f32_dev", _int, [_i64, _i64, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _int,
                                                 C.POINTER(_vp), _vp])
     _sig(L, "gcoo_plan_spdm_f32_dev", _int, [_vp, _i64, _vp, _i64, _vp, _i64, _vp])
+    _sig(L, "gcoo_plan_create_f64_dev", _int, [_i64, _i64, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _int,
+                                                C.POINTER(_vp), _vp])
+    _sig(L, "gcoo_plan_spdm_f64_dev", _int, [_vp, _i64, _vp, _i64, _vp, _i64, _vp])
     _sig(L, "gcoo_plan_destroy", _int, [_vp])
     _sig(L, "gcoo_debug_kernel_timing", _int, [_int])
     _sig(L, "gcoo_debug_pipeline_strips", _int, [_int])
@@ -524,26 +527,31 @@ def spdm_gcoo_dev(a: DeviceGcoo, b, c, cfg: Optional[ExecConfig] = None, flavor:
 
 class SpdmPlan:
     """Plan / execute split (C ABI gcoo_plan_*): the multiply's record stream
-    built once from a DeviceGcoo (fp32), then `run(b, c)` per dense operand —
+    built once from a DeviceGcoo (fp32 or fp64), then `run(b, c)` per dense operand —
     the same bits as spdm_gcoo_dev without the ~35 us planner per call.  Keeps
     a reference to A's tensors; close() (or garbage collection) frees it."""
 
     def __init__(self, a: "DeviceGcoo", flavor: int = FLAVOR_FMA, stream=None):
+        import torch
         self.a = a
         self._h = _vp()
-        _check(lib().gcoo_plan_create_f32_dev(a.rows_dim, a.cols_dim, a.p, a.nnz(), _p(a.values), _p(a.row_idx),
-                                              _p(a.col_idx), a.groups(), _p(a.g_idxes), _p(a.nnz_per_group),
-                                              flavor, C.byref(self._h), _stream_ptr(stream)))
+        self._f64 = a.values.dtype == torch.float64
+        create = lib().gcoo_plan_create_f64_dev if self._f64 else lib().gcoo_plan_create_f32_dev
+        _check(create(a.rows_dim, a.cols_dim, a.p, a.nnz(), _p(a.values), _p(a.row_idx), _p(a.col_idx), a.groups(),
+                      _p(a.g_idxes), _p(a.nnz_per_group), flavor, C.byref(self._h), _stream_ptr(stream)))
 
     def run(self, b, c, stream=None) -> None:
+        import torch
         if b.stride(1) != 1 or c.stride(1) != 1:
             raise ValueError("spdm_gcoo_dev: B and C need unit column stride")
         if b.shape[0] != self.a.cols_dim or c.shape[0] != self.a.rows_dim or c.shape[1] != b.shape[1]:
             raise ValueError("spdm_gcoo: operand shapes do not match the plan's A")
         if self._h is None:
             raise ValueError("SpdmPlan: closed")
-        _check(lib().gcoo_plan_spdm_f32_dev(self._h, b.shape[1], _p(b), b.stride(0), _p(c), c.stride(0),
-                                            _stream_ptr(stream)))
+        if (b.dtype == torch.float64) != self._f64 or c.dtype != b.dtype:
+            raise ValueError("SpdmPlan: operand dtype differs from the plan's")
+        run = lib().gcoo_plan_spdm_f64_dev if self._f64 else lib().gcoo_plan_spdm_f32_dev
+        _check(run(self._h, b.shape[1], _p(b), b.stride(0), _p(c), c.stride(0), _stream_ptr(stream)))
 
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and _lib is not None:

@@ -773,10 +773,60 @@ void spdm_dev(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, int64_t nnz
 }  // namespace gcoo_b200
 
 struct gcoo_plan {
+  int elem_bytes = 4;  // 4: fp32 plan, 8: fp64 plan
   gcoo_b200::DevGcoo<float> a;
+  gcoo_b200::DevGcoo<double> a64;
   int flavor = GCOO_FLAVOR_FMA;
   gcoo_b200::SpdmPlan plan;
 };
+
+namespace gcoo_b200 {
+template <typename T>
+DevGcoo<T>& plan_a(gcoo_plan* h) {
+  if constexpr (sizeof(T) == 8) return h->a64; else return h->a;
+}
+template <typename T>
+const DevGcoo<T>& plan_a(const gcoo_plan* h) {
+  if constexpr (sizeof(T) == 8) return h->a64; else return h->a;
+}
+
+template <typename T>
+void plan_create(int64_t m, int64_t k, int32_t p, int64_t nnz, const T* values, const int32_t* row_idx,
+                 const int32_t* col_idx, int64_t groups, const int64_t* g_idxes, const int64_t* nnz_per_group,
+                 int flavor, gcoo_plan** plan, void* stream) {
+  if (!plan) einval("gcoo_plan_create: null plan pointer");
+  *plan = nullptr;
+  validate_spdm(m, k, 1, p, p, 1, k, nnz, groups, nullptr, 0);
+  std::unique_ptr<gcoo_plan> h(new gcoo_plan());
+  h->elem_bytes = (int)sizeof(T);
+  plan_a<T>(h.get()) = DevGcoo<T>{m, k, nnz, groups, p, values, row_idx, col_idx, g_idxes, nnz_per_group};
+  h->flavor = flavor;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (m > 0) {
+    // the kernel class for 16-byte aligned B/C with n % 4 == 0 (checked again per multiply)
+    static const double aligned[2] __attribute__((aligned(16))) = {};
+    const T* al = reinterpret_cast<const T*>(aligned);
+    make_plan<T>(h->plan, plan_a<T>(h.get()), choose_kind<T>(plan_a<T>(h.get()), 4, 4, 4, al, al, flavor), s);
+  }
+  *plan = h.release();
+}
+
+template <typename T>
+void plan_spdm(const gcoo_plan* plan, int64_t n, const T* B, int64_t ldb, T* C, int64_t ldc, void* stream) {
+  if (!plan) einval("gcoo_plan_spdm: null plan");
+  if (plan->elem_bytes != (int)sizeof(T)) einval("gcoo_plan_spdm: plan built for another element type");
+  if (n < 0 || ldb < n || ldc < n) einval("spdm_gcoo: leading dimension smaller than n");
+  const DevGcoo<T>& a = plan_a<T>(plan);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (a.m == 0 || n == 0) return;
+  const int kind = choose_kind<T>(a, n, ldb, ldc, B, C, plan->flavor);
+  if (kind == plan->plan.kind) {
+    run_spdm<T>(plan->plan, a, n, B, ldb, C, ldc, plan->flavor, s);
+  } else {  // this B/C layout needs another kernel class: plan it for this call
+    launch_spdm<T>(a, n, B, ldb, C, ldc, plan->flavor, s);
+  }
+}
+}  // namespace gcoo_b200
 
 namespace gcoo_b200 {
 
@@ -1093,37 +1143,26 @@ int gcoo_plan_create_f32_dev(int64_t m, int64_t k, int32_t p, int64_t nnz, const
                              const int32_t* row_idx, const int32_t* col_idx, int64_t groups, const int64_t* g_idxes,
                              const int64_t* nnz_per_group, int flavor, gcoo_plan** plan, void* stream) {
   return guarded([&] {
-    if (!plan) einval("gcoo_plan_create: null plan pointer");
-    *plan = nullptr;
-    validate_spdm(m, k, 1, p, p, 1, k, nnz, groups, nullptr, 0);
-    std::unique_ptr<gcoo_plan> h(new gcoo_plan());
-    h->a = DevGcoo<float>{m, k, nnz, groups, p, values, row_idx, col_idx, g_idxes, nnz_per_group};
-    h->flavor = flavor;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (m > 0) {
-      // the kernel class for 16-byte aligned B/C with n % 4 == 0 (checked again per multiply)
-      static const float aligned[4] __attribute__((aligned(16))) = {};
-      make_plan<float>(h->plan, h->a, choose_kind<float>(h->a, 4, 4, 4, aligned, aligned, flavor), s);
-    }
-    *plan = h.release();
+    plan_create<float>(m, k, p, nnz, values, row_idx, col_idx, groups, g_idxes, nnz_per_group, flavor, plan, stream);
+  });
+}
+
+int gcoo_plan_create_f64_dev(int64_t m, int64_t k, int32_t p, int64_t nnz, const double* values,
+                             const int32_t* row_idx, const int32_t* col_idx, int64_t groups, const int64_t* g_idxes,
+                             const int64_t* nnz_per_group, int flavor, gcoo_plan** plan, void* stream) {
+  return guarded([&] {
+    plan_create<double>(m, k, p, nnz, values, row_idx, col_idx, groups, g_idxes, nnz_per_group, flavor, plan, stream);
   });
 }
 
 int gcoo_plan_spdm_f32_dev(const gcoo_plan* plan, int64_t n, const float* B, int64_t ldb, float* C, int64_t ldc,
                            void* stream) {
-  return guarded([&] {
-    if (!plan) einval("gcoo_plan_spdm: null plan");
-    if (n < 0 || ldb < n || ldc < n) einval("spdm_gcoo: leading dimension smaller than n");
-    const DevGcoo<float>& a = plan->a;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (a.m == 0 || n == 0) return;
-    const int kind = choose_kind<float>(a, n, ldb, ldc, B, C, plan->flavor);
-    if (kind == plan->plan.kind) {
-      run_spdm<float>(plan->plan, a, n, B, ldb, C, ldc, plan->flavor, s);
-    } else {  // this B/C layout needs another kernel class: plan it for this call
-      launch_spdm<float>(a, n, B, ldb, C, ldc, plan->flavor, s);
-    }
-  });
+  return guarded([&] { plan_spdm<float>(plan, n, B, ldb, C, ldc, stream); });
+}
+
+int gcoo_plan_spdm_f64_dev(const gcoo_plan* plan, int64_t n, const double* B, int64_t ldb, double* C, int64_t ldc,
+                           void* stream) {
+  return guarded([&] { plan_spdm<double>(plan, n, B, ldb, C, ldc, stream); });
 }
 
 int gcoo_plan_destroy(gcoo_plan* plan) {

@@ -269,6 +269,20 @@ def test_plan_execute_split_bit_exact(gcoo, cuda, oracle):
         plan.close()
     with pytest.raises(ValueError):
         plan.run(bfull, torch.empty((5000, 1030), device="cuda"))
+    # fp64 plans
+    a = rand_dense(rng, 2000, 1500, 0.02, np.float64)
+    dg = gcoo.DeviceGcoo.from_host(gcoo.dense_to_gcoo(a, 4))
+    plan = gcoo.SpdmPlan(dg)
+    b = torch.from_numpy(rand_dense(rng, 1500, 640, 1.0, np.float64)).cuda()
+    c1 = torch.empty((2000, 640), device="cuda", dtype=torch.float64)
+    c2 = torch.empty_like(c1)
+    plan.run(b, c1)
+    gcoo.spdm_gcoo_dev(dg, b, c2)
+    torch.cuda.synchronize()
+    assert torch.equal(c1, c2)
+    with pytest.raises(ValueError):
+        plan.run(b.float(), c1.float())
+    plan.close()
 
 
 def test_strided_column_shards_bitwise_equal(gcoo, cuda, oracle):
