@@ -469,13 +469,14 @@ def cpu_baseline(g_host, b_host, n):
         from oracle import Gcoo, Reference, have_reference
     except Exception as e:  # noqa: BLE001
         return {"error": f"oracle unavailable: {e}"}
-    cores = os.cpu_count() or 1
+    cores = len(os.sched_getaffinity(0)) or os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     g = Gcoo(g_host.rows_dim, g_host.cols_dim, g_host.p, g_host.values, g_host.row_idx, g_host.col_idx,
              g_host.g_idxes, g_host.nnz_per_group)
     if have_reference():
         R = Reference(False)
-        r = R.time_spdm(g, b_host, b=BW, workers=0, warmup=1, reps=3)
+        # every host core, explicitly (torchrun exports OMP_NUM_THREADS=1)
+        r = R.time_spdm(g, b_host, b=BW, workers=cores, warmup=1, reps=3)
         kc = r["kc_s"]
         return {"value": round(2.0 * g.nnz * n / kc / 1e9, 3), "unit": "GFLOPS", "cores": int(r["workers"]),
                 "kind": "reference",
@@ -494,13 +495,14 @@ def run_reference(args):
     if not have_reference():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (reference sources absent)"}))
         return
-    cores = os.cpu_count() or 1
+    cores = len(os.sched_getaffinity(0)) or os.cpu_count() or 1
     R = Reference(False)
     n, s = args.n, args.sparsity
     a = R.uniform_sparse(n, s, SEED)
     b = R.uniform_sparse(n, 0.0, R.derive_seed(SEED, n, 0xB))
     g = R.dense_to_gcoo(a, P)
-    r = R.time_spdm(g, b, b=BW, workers=0, warmup=max(0, min(args.warmup, 2)), reps=max(1, args.steps))
+    # every host core, explicitly: torchrun exports OMP_NUM_THREADS=1 to its ranks
+    r = R.time_spdm(g, b, b=BW, workers=cores, warmup=max(0, min(args.warmup, 2)), reps=max(1, args.steps))
     kc = r["kc_s"]
     v = 2.0 * g.nnz * n / kc / 1e9
     line = {
