@@ -583,9 +583,23 @@ bool tile_order_is_permutation(const int64_t* order, int64_t count) {
 int g_pipeline_strips = 32;  // tuning hook (gcoo_debug_pipeline_strips)
 constexpr int NBUF = 3;
 
-int64_t pipeline_strip(int64_t m, int64_t k, int64_t n) {
-  if (g_pipeline_strips <= 1 || n < 2048 || (m + k) * n < (int64_t)32 << 20) return 0;  // small: one shot
-  int64_t w = ceil_div(ceil_div(n, g_pipeline_strips), 128) * 128;
+// Pageable (not page-locked) host memory crosses PCIe through the driver's
+// staging buffers at ~12 GB/s, and strided 2-D copies from it get slower the
+// narrower the strip: few wide strips then beat many narrow ones (n=8000:
+// 4 strips 43 ms, 32 strips 66 ms; pinned: 32 strips 5.8 ms).
+bool host_pageable(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeUnregistered;
+}
+
+int64_t pipeline_strip(int64_t m, int64_t k, int64_t n, bool pageable) {
+  const int strips = pageable ? std::min(g_pipeline_strips, 4) : g_pipeline_strips;
+  if (strips <= 1 || n < 2048 || (m + k) * n < (int64_t)32 << 20) return 0;  // small: one shot
+  int64_t w = ceil_div(ceil_div(n, strips), 128) * 128;
   return std::max<int64_t>(w, 256);
 }
 
@@ -657,7 +671,7 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
   validate_spdm(m, k, n, a_p, cfg_p, cfg_b, b_rows, nnz, groups, tile_order, tile_count);
   const bool perm = tile_order ? tile_order_is_permutation(tile_order, tile_count) : true;
   cudaStream_t s = thread_stream();
-  const int64_t W = perm ? pipeline_strip(m, k, n) : 0;
+  const int64_t W = perm ? pipeline_strip(m, k, n, host_pageable(B) || host_pageable(C)) : 0;
   // pipelined path: every buffer first; then A crosses PCIe ahead of B strip 0
   // on the H2D stream (the planner and strip 0's multiply need it first), so
   // the D2H direction can start as early as possible
