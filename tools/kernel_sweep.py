@@ -22,7 +22,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=8000)
     ap.add_argument("--s", type=float, nargs="+", default=[0.9, 0.99, 0.995])
-    ap.add_argument("--kernels", nargs="+", default=["auto", "tile_v4", "tacc_v4", "tacc_v2", "rowtile"])
+    ap.add_argument("--kernels", nargs="+", default=["auto", "tacc28_k192", "tacc28_k160", "tacc28_k128", "tacc_v4", "rowtile"])
     ap.add_argument("--reps", type=int, default=5)
     args = ap.parse_args()
     n = args.n
