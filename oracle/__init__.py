@@ -235,6 +235,46 @@ class Reference:
                                         1 if infinite_l2 else 0, out.ctypes.data))
         return dict(zip(self.TRAFFIC_FIELDS, (int(x) for x in out)))
 
+    def read_mtx(self, path: str, dtype=np.float32):
+        """read_matrix_market<T> (io.hpp:66-85).  Returns ("dense", array) or
+        ("coo", rows_dim, cols_dim, values, row_idx, col_idx); a ParseError comes
+        back as ("error", line, message), other failures raise."""
+        t = "f32" if np.dtype(dtype) == np.float32 else "f64"
+        rd, fe = getattr(self.lib, f"ref_mtx_read_{t}"), getattr(self.lib, f"ref_mtx_fetch_{t}")
+        rd.restype, rd.argtypes = C.c_int, [C.c_char_p, _vp]
+        fe.restype, fe.argtypes = None, [_vp, _vp, _vp]
+        info = np.zeros(5, np.int64)
+        rc = rd(os.fsencode(path), info.ctypes.data)
+        if rc == 3:
+            return ("error", int(info[4]), self.lib.ref_last_error().decode())
+        self._check(rc)
+        dense, m, k, cnt = (int(x) for x in info[:4])
+        if dense:
+            out = np.empty((m, k), dtype=dtype)
+            fe(out.ctypes.data, None, None)
+            return ("dense", out)
+        v, r, c = np.empty(cnt, dtype=dtype), np.empty(cnt, np.int32), np.empty(cnt, np.int32)
+        fe(v.ctypes.data, r.ctypes.data, c.ctypes.data)
+        return ("coo", m, k, v, r, c)
+
+    def write_mtx(self, path: str, a=None, coo=None):
+        """write_matrix_market (io.hpp:87-109): dense `a`, or coo=(m, k, values, row_idx, col_idx)."""
+        if a is not None:
+            a = np.ascontiguousarray(a)
+            t = "f32" if a.dtype == np.float32 else "f64"
+            f = getattr(self.lib, f"ref_mtx_write_dense_{t}")
+            f.restype, f.argtypes = C.c_int, [C.c_char_p, _i64, _i64, _vp]
+            self._check(f(os.fsencode(path), a.shape[0], a.shape[1], a.ctypes.data))
+            return
+        m, k, v, r, c = coo
+        v = np.ascontiguousarray(v)
+        r = np.ascontiguousarray(r, dtype=np.int32)
+        c = np.ascontiguousarray(c, dtype=np.int32)
+        t = "f32" if v.dtype == np.float32 else "f64"
+        f = getattr(self.lib, f"ref_mtx_write_coo_{t}")
+        f.restype, f.argtypes = C.c_int, [C.c_char_p, _i64, _i64, _i64, _vp, _vp, _vp]
+        self._check(f(os.fsencode(path), m, k, v.size, v.ctypes.data, r.ctypes.data, c.ctypes.data))
+
     def _check(self, rc: int):
         if rc == 1:
             raise ValueError(self.lib.ref_last_error().decode())

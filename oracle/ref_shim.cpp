@@ -15,6 +15,7 @@
 #include <exception>
 #include <stdexcept>
 #include <string>
+#include <variant>
 #include <vector>
 
 #include "gcoo/bench.hpp"
@@ -264,4 +265,99 @@ int ref_model_traffic(int csr, int64_t nnz, const int32_t* rows, const int32_t* 
   });
 }
 
+}  // extern "C"
+
+// MatrixMarket I/O (io.cpp:57-205 through io.hpp:66-109).  ref_mtx_read_*
+// parses into a thread-local cache and reports info = {dense, rows, cols,
+// count, error_line}; ref_mtx_fetch_* copies the cached arrays out (COO:
+// vals/rows/cols of `count` entries; dense: rows*cols row-major values).
+namespace {
+template <typename T>
+struct MtxCache {
+  bool dense = false;
+  DenseMatrix<T> d;
+  CooMatrix<T> c;
+};
+template <typename T>
+MtxCache<T>& mtx_cache() {
+  static thread_local MtxCache<T> m;
+  return m;
+}
+template <typename T>
+int mtx_read(const char* path, int64_t* info) {
+  info[4] = 0;
+  try {
+    auto got = read_matrix_market<T>(path);
+    auto& m = mtx_cache<T>();
+    if (std::holds_alternative<DenseMatrix<T>>(got)) {
+      m.dense = true;
+      m.d = std::move(std::get<DenseMatrix<T>>(got));
+      info[0] = 1, info[1] = m.d.rows, info[2] = m.d.cols, info[3] = m.d.rows * m.d.cols;
+    } else {
+      m.dense = false;
+      m.c = std::move(std::get<CooMatrix<T>>(got));
+      info[0] = 0, info[1] = m.c.rows_dim, info[2] = m.c.cols_dim, info[3] = m.c.nnz();
+    }
+    return 0;
+  } catch (const ParseError& e) {
+    g_err = e.what();
+    info[4] = e.line;
+    return 3;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+template <typename T>
+void mtx_fetch(T* vals, int32_t* rows, int32_t* cols) {
+  auto& m = mtx_cache<T>();
+  if (m.dense) {
+    std::memcpy(vals, m.d.data.data(), sizeof(T) * m.d.data.size());
+    return;
+  }
+  std::memcpy(vals, m.c.values.data(), sizeof(T) * m.c.values.size());
+  std::memcpy(rows, m.c.row_idx.data(), sizeof(int32_t) * m.c.row_idx.size());
+  std::memcpy(cols, m.c.col_idx.data(), sizeof(int32_t) * m.c.col_idx.size());
+}
+template <typename T>
+int mtx_write_coo(const char* path, int64_t m, int64_t k, int64_t nnz, const T* vals, const int32_t* rows,
+                  const int32_t* cols) {
+  return guarded([&] {
+    CooMatrix<T> c;
+    c.rows_dim = m;
+    c.cols_dim = k;
+    c.values.assign(vals, vals + nnz);
+    c.row_idx.assign(rows, rows + nnz);
+    c.col_idx.assign(cols, cols + nnz);
+    write_matrix_market(c, path);
+  });
+}
+template <typename T>
+int mtx_write_dense(const char* path, int64_t m, int64_t k, const T* data) {
+  return guarded([&] { write_matrix_market(make_dense<T>(m, k, data), path); });
+}
+}  // namespace
+
+extern "C" {
+int ref_mtx_read_f32(const char* path, int64_t* info) { return mtx_read<float>(path, info); }
+int ref_mtx_read_f64(const char* path, int64_t* info) { return mtx_read<double>(path, info); }
+void ref_mtx_fetch_f32(float* v, int32_t* r, int32_t* c) { mtx_fetch<float>(v, r, c); }
+void ref_mtx_fetch_f64(double* v, int32_t* r, int32_t* c) { mtx_fetch<double>(v, r, c); }
+int ref_mtx_write_coo_f32(const char* path, int64_t m, int64_t k, int64_t nnz, const float* v, const int32_t* r,
+                          const int32_t* c) {
+  return mtx_write_coo<float>(path, m, k, nnz, v, r, c);
+}
+int ref_mtx_write_coo_f64(const char* path, int64_t m, int64_t k, int64_t nnz, const double* v, const int32_t* r,
+                          const int32_t* c) {
+  return mtx_write_coo<double>(path, m, k, nnz, v, r, c);
+}
+int ref_mtx_write_dense_f32(const char* path, int64_t m, int64_t k, const float* d) {
+  return mtx_write_dense<float>(path, m, k, d);
+}
+int ref_mtx_write_dense_f64(const char* path, int64_t m, int64_t k, const double* d) {
+  return mtx_write_dense<double>(path, m, k, d);
+}
 }  // extern "C"
