@@ -251,6 +251,27 @@ int gcoo_generate_powerlaw_coo_f32(int64_t n, double s, double alpha, uint64_t s
                                    int64_t capacity, float* values, int32_t* row_idx,
                                    int32_t* col_idx, int64_t* nnz);
 
+/* ------------------------------------------------ MatrixMarket ---------- */
+/*
+ * Entry section of a MatrixMarket file — the text after the size line — parsed
+ * on the host's threads (threads <= 0: up to one per MiB of text and core;
+ * threads > 0: exactly that many newline-aligned chunks).  The tokenising
+ * half of read_matrix_market_raw (io.cpp:109-158): blank and '%' lines are
+ * skipped; every other line must hold exactly ncol tokens (3 coordinate
+ * real/integer, 2 pattern, 1 array), the first two of a coordinate line
+ * integers (1-based, written to idx[2*i], idx[2*i+1]), the last of a
+ * real/integer/array line a finite decimal (vals[i], via strtod: bit-identical
+ * to the reference's num_get<double>).  line_of[i] = 0-based line index of
+ * data line i within `text`.  At most `cap` rows are written; any pointer may
+ * be NULL.  Returns the number of data lines, or GCOO_MTX_IRREGULAR when some
+ * data line breaks the rules above (the caller re-reads that file line by
+ * line for the reference's exact ParseError).  No range, symmetry, order or
+ * duplicate checks here.
+ */
+#define GCOO_MTX_IRREGULAR (-1)
+int64_t gcoo_mtx_parse_entries(const char* text, int64_t len, int32_t ncol, int64_t cap, int64_t* idx,
+                               double* vals, int64_t* line_of, int32_t threads);
+
 #ifdef __cplusplus
 }
 #endif

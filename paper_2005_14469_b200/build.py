@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libgcoo_cuda.so")
-SOURCES = ["capi.cu", "host_gen.cpp"]
+SOURCES = ["capi.cu", "host_gen.cpp", "host_mtx.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -26,7 +26,6 @@ from __future__ import annotations
 
 import os
 import re
-import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -189,69 +188,26 @@ def _header(data: bytes):
     return fmt, field, sym, rows, cols, declared, pos, ln
 
 
-_LUT_WS = np.zeros(256, bool)
-_LUT_WS[list(_WS)] = True
-_LUT_OK = _LUT_WS.copy()
-_LUT_OK[list(b"\n+-0123456789.eE")] = True
+def _parse_entries(body: bytes, ln0: int, ncol: int, cap: int):
+    """The entry section through the native multi-threaded tokenizer
+    (gcoo_mtx_parse_entries, csrc/host_mtx.cpp).  Returns (line_numbers,
+    indices (n, 2) int64, values float64) for up to `cap` data lines plus the
+    total data-line count, or None when some data line is irregular — the
+    caller then re-reads line by line to report the reference's exact error."""
+    import ctypes as C
 
-
-def _scan(body: bytes, ln0: int, int_cols: int):
-    """Vectorised tokenisation of the entry section.
-
-    Returns (line_numbers, token_counts, numbers) for the data lines (blank and
-    comment lines dropped), where `numbers` is every token parsed as a double
-    in file order, or None when some data byte is outside [0-9+-.eE] or
-    whitespace, a token of the first `int_cols` columns is not a plain
-    integer, or a token does not parse — the caller then re-parses line by
-    line to report the reference's exact error."""
-    buf = np.frombuffer(body, np.uint8)
-    nl = np.flatnonzero(buf == 10)
-    starts = np.concatenate(([0], nl + 1))
-    ends = np.concatenate((nl, [buf.size]))
-    if body.endswith(b"\n") or not body:
-        starts, ends = starts[:-1], ends[:-1]
-    ws = _LUT_WS[buf] | (buf == 10)
-    solid = np.flatnonzero(~ws)
-    first = np.searchsorted(solid, starts)
-    has = first < solid.size
-    has[has] = solid[first[has]] < ends[has]
-    is_data = has.copy()
-    is_data[has] = buf[solid[first[has]]] != ord("%")
-    tok = solid[np.concatenate(([True], np.diff(solid) > 1)) | ws[np.maximum(solid - 1, 0)] | (solid == 0)] \
-        if solid.size else solid
-    tok_line = np.searchsorted(starts, tok, side="right") - 1
-    counts = np.bincount(tok_line, minlength=starts.size)
-    data_lines = np.flatnonzero(is_data)
-    numbers = None
-    skip = np.flatnonzero(~is_data & has)                    # comment lines: blank them out
-    if skip.size:
-        mark = np.zeros(buf.size + 1, np.int32)
-        np.add.at(mark, starts[skip], 1)
-        np.add.at(mark, ends[skip], -1)
-        work = buf.copy()
-        work[np.cumsum(mark[:-1]) > 0] = 32
-    else:
-        work = buf
-    if _LUT_OK[work].all():
-        ok = True
-        if int_cols:
-            odd = np.flatnonzero((work == ord(".")) | (work == ord("e")) | (work == ord("E")))
-            if odd.size:
-                t = np.searchsorted(tok, odd, side="right") - 1
-                col = t - np.searchsorted(tok_line, tok_line[t])       # rank of the token in its line
-                ok = not (col < int_cols).any()
-        if ok and not counts[data_lines].any():
-            numbers = np.zeros(0)
-        elif ok:
-            try:
-                with warnings.catch_warnings():
-                    warnings.simplefilter("error")
-                    numbers = np.fromstring(work.tobytes(), dtype=np.float64, sep=" ")
-            except (ValueError, DeprecationWarning):
-                numbers = None
-            if numbers is not None and (numbers.size != int(counts[data_lines].sum()) or not np.isfinite(numbers).all()):
-                numbers = None
-    return data_lines + ln0 + 1, counts[data_lines], numbers
+    from . import lib
+    f = lib().gcoo_mtx_parse_entries
+    f.restype = C.c_int64
+    f.argtypes = [C.c_char_p, C.c_int64, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]
+    idx = np.empty((cap, 2), np.int64)
+    vals = np.empty(cap, np.float64)
+    line = np.empty(cap, np.int64)
+    n = f(body, len(body), ncol, cap, idx.ctypes.data, vals.ctypes.data, line.ctypes.data, 0)
+    if n < 0:
+        return None
+    k = min(n, cap)
+    return line[:k] + ln0 + 1, idx[:k], vals[:k], n
 
 
 def _coord_slow(lines, ln0, field, sym, rows, cols, declared):
@@ -284,33 +240,38 @@ def _coord_slow(lines, ln0, field, sym, rows, cols, declared):
 
 def _read_coordinate(body, ln0, field, sym, rows, cols, declared, dtype):
     ncol = 2 if field == "pattern" else 3
-    line_no, counts, nums = _scan(body, ln0, 2)
-    fast = nums is not None and line_no.size == declared and bool((counts == ncol).all())
+    got = _parse_entries(body, ln0, ncol, declared + 1)
+    fast = got is not None and got[3] == declared
     if fast:
-        nums = nums.reshape(declared, ncol)
-        r = nums[:, 0].astype(np.int64)
-        c = nums[:, 1].astype(np.int64)
-        v = nums[:, 2].copy() if ncol == 3 else np.ones(declared, np.float64)
+        line_no, ij, v = got[0], got[1], got[2]
+        r, c = ij[:, 0].copy(), ij[:, 1].copy()
+        if ncol == 2:
+            v = np.ones(declared, np.float64)
         bad = (r < 1) | (r > rows) | (c < 1) | (c > cols)
         if sym == "symmetric":
             bad |= c > r
         fast = not bad.any()
     if not fast:
         _coord_slow(_lines(body), ln0, field, sym, rows, cols, declared)
-        raise AssertionError("vectorised MatrixMarket checks rejected a file the line parser accepts")
+        raise AssertionError("native MatrixMarket checks rejected a file the line parser accepts")
     r, c = r - 1, c - 1
     if sym == "symmetric":
         off = r != c
         r, c = np.concatenate([r, c[off]]), np.concatenate([c, r[off]])
         v = np.concatenate([v, v[off]])
         line_no = np.concatenate([line_no, line_no[off]])
-    order = np.lexsort((line_no, c, r))
-    r, c, v, line_no = r[order], c[order], v[order], line_no[order]
-    if r.size > 1:
-        dup = np.flatnonzero((r[1:] == r[:-1]) & (c[1:] == c[:-1]))
+    # io.cpp:122-132: sort by (row, col, line), a repeated coordinate is an error
+    key = r * cols + c
+    if key.size > 1 and not (key[1:] > key[:-1]).all():       # files written row-major skip the sort
+        order = np.argsort(key, kind="stable")
+        key = key[order]
+        dup = np.flatnonzero(key[1:] == key[:-1])
         if dup.size:
-            j = int(dup[0]) + 1
+            order = np.lexsort((line_no, c, r))
+            r, c, line_no = r[order], c[order], line_no[order]
+            j = int(np.flatnonzero((r[1:] == r[:-1]) & (c[1:] == c[:-1]))[0]) + 1
             raise ParseError(f"duplicate entry at ({int(r[j]) + 1}, {int(c[j]) + 1})", int(line_no[j]))
+        r, c, v = r[order], c[order], v[order]
     with np.errstate(over="ignore"):                 # static_cast<float>(1e308) = inf, as in C++
         v = v.astype(dtype)
     out = CooMatrix(int(rows), int(cols), v, r.astype(np.int32), c.astype(np.int32))
@@ -321,27 +282,28 @@ def _read_coordinate(body, ln0, field, sym, rows, cols, declared, dtype):
 def _read_array(body, ln0, sym, rows, cols, dtype):
     """io.cpp:138-158: column-major values, lower triangle when symmetric."""
     need = rows * cols if sym == "general" else rows * (rows + 1) // 2
-    line_no, counts, nums = _scan(body, ln0, 0)
-    if nums is None or line_no.size < need or not (counts[:need] == 1).all():
+    got = _parse_entries(body, ln0, 1, need + 1)
+    if got is None or got[3] < need:
         lines = _lines(body)
-        got = 0
-        for i, line in enumerate(lines):
-            if got == need:
-                break
-            if not _is_data(line):
-                continue
-            st = _Stream(line)
-            if st.dbl() is None:
-                raise ParseError("malformed array value", ln0 + i + 1)
-            _consumed(st, ln0 + i + 1)
-            got += 1
-        if got < need:
-            raise ParseError(f"file ends after {got} array values", ln0 + len(lines))
-        if line_no.size <= need:     # every value line is fine, so only a surplus line can have failed
-            raise AssertionError("vectorised MatrixMarket checks rejected a file the line parser accepts")
-    if line_no.size > need:
+        n, i = 0, 0
+        while n < need and i < len(lines):
+            if _is_data(lines[i]):
+                st = _Stream(lines[i])
+                if st.dbl() is None:
+                    raise ParseError("malformed array value", ln0 + i + 1)
+                _consumed(st, ln0 + i + 1)
+                n += 1
+            i += 1
+        if n < need:
+            raise ParseError(f"file ends after {n} array values", ln0 + len(lines))
+        for j in range(i, len(lines)):
+            if _is_data(lines[j]):
+                raise ParseError("more array values than the shape holds", ln0 + j + 1)
+        raise AssertionError("native MatrixMarket checks rejected a file the line parser accepts")
+    line_no, vals = got[0], got[2]
+    if got[3] > need:
         raise ParseError("more array values than the shape holds", int(line_no[need]))
-    vals = nums[:need]
+    vals = vals[:need]
     out = np.zeros((rows, cols), np.float64)
     if sym == "general":
         out[:] = vals.reshape(cols, rows).T

@@ -303,3 +303,43 @@ def test_mtx_to_gcoo_dev_matches_reference(tmp_path, cuda, gcoo, oracle, p):
     got = mmio.read_matrix_market_gcoo_dev(f, p).to_host()
     for name in ("values", "row_idx", "col_idx", "g_idxes", "nnz_per_group"):
         assert np.array_equal(np.asarray(getattr(got, name)), np.asarray(getattr(want, name))), name
+
+
+def test_native_tokenizer_chunking(gcoo):
+    """gcoo_mtx_parse_entries gives the same rows for 1..13 newline-aligned
+    chunks (chunk edges inside comments, blank lines, CRLF and a missing final
+    newline), and flags an irregular line in any chunk."""
+    import ctypes as C
+    f = gcoo.lib().gcoo_mtx_parse_entries
+    f.restype = C.c_int64
+    f.argtypes = [C.c_char_p, C.c_int64, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]
+    rnd = random.Random(5)
+    lines = []
+    for i in range(400):
+        t = rnd.random()
+        if t < 0.1:
+            lines.append("% comment " + str(i))
+        elif t < 0.15:
+            lines.append(rnd.choice(["", "  ", "\t\r"]))
+        else:
+            lines.append(f" {rnd.randrange(1, 99)}\t{rnd.randrange(1, 99)} {rnd.uniform(-1e3, 1e3)!r}" +
+                         ("\r" if rnd.random() < 0.2 else ""))
+    body = "\n".join(lines).encode()
+
+    def run(text, threads, cap=500):
+        idx, vals, line = np.zeros((cap, 2), np.int64), np.zeros(cap), np.zeros(cap, np.int64)
+        n = f(text, len(text), 3, cap, idx.ctypes.data, vals.ctypes.data, line.ctypes.data, threads)
+        return n, idx[:max(n, 0)], vals[:max(n, 0)], line[:max(n, 0)]
+
+    n1, i1, v1, l1 = run(body, 1)
+    want = [j for j, s in enumerate(lines) if s.strip() and not s.lstrip().startswith("%")]
+    assert n1 == len(want) and l1.tolist() == want
+    assert v1.tolist() == [float(lines[j].split()[2]) for j in want]
+    for t in range(2, 14):
+        n, i, v, l = run(body, t)
+        assert n == n1 and np.array_equal(i, i1) and v.tobytes() == v1.tobytes() and np.array_equal(l, l1)
+    bad = lines.copy()
+    bad[want[-1]] += " extra"
+    for t in (1, 3, 8):
+        assert run("\n".join(bad).encode(), t)[0] == -1
+    assert run(b"", 4)[0] == 0
