@@ -343,3 +343,34 @@ def test_native_tokenizer_chunking(gcoo):
     for t in (1, 3, 8):
         assert run("\n".join(bad).encode(), t)[0] == -1
     assert run(b"", 4)[0] == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("header", ["pattern symmetric", "real symmetric", "integer general"])
+def test_mtx_file_to_spdm_on_gpu_bit_exact(tmp_path, cuda, gcoo, oracle, header):
+    """A SuiteSparse-style file (symmetric / pattern / integer, scrambled entry
+    order, comments) -> read_matrix_market_gcoo_dev -> spdm_gcoo_dev: C
+    bit-identical to the oracle's FMA chain on the reference reader's COO."""
+    import torch
+    field, sym = header.split()
+    rng = np.random.default_rng(len(header))
+    n = 700
+    a = (rng.random((n, n)) < 0.01) * rng.integers(1, 9, (n, n)).astype(np.float64)
+    if sym == "symmetric":
+        a = np.tril(a) + np.tril(a, -1).T
+        rr, cc = np.nonzero(np.tril(a))
+    else:
+        rr, cc = np.nonzero(a)
+    lines = [f"%%MatrixMarket matrix coordinate {field} {sym}", "% generated", f"{n} {n} {rr.size}"]
+    for j in rng.permutation(rr.size):
+        v = "" if field == "pattern" else f" {int(a[rr[j], cc[j]])}"
+        lines.append(f"{rr[j] + 1} {cc[j] + 1}{v}")
+    f = _w(tmp_path, "\n".join(lines) + "\n")
+    if field == "pattern":
+        a = (a != 0).astype(np.float64)
+    d = mmio.read_matrix_market_gcoo_dev(f, 4)
+    B = rng.random((n, 384)).astype(np.float32)
+    Cd = torch.empty((n, 384), dtype=torch.float32, device="cuda")
+    gcoo.spdm_gcoo_dev(d, torch.from_numpy(B).cuda(), Cd)
+    want, _ = oracle.spdm(oracle.dense_to_gcoo(a.astype(np.float32), 4), B, fma=True)
+    assert Cd.cpu().numpy().tobytes() == want.tobytes()
