@@ -24,16 +24,27 @@ def main():
     ap.add_argument("--s", type=float, nargs="+", default=[0.9, 0.99, 0.995])
     ap.add_argument("--kernels", nargs="+", default=["auto", "tacc28_k192", "tacc28_k160", "tacc28_k128", "tacc_v4", "rowtile"])
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--powerlaw", action="store_true", help="BASELINE configs[3]: power-law A (n=16384 default)")
     args = ap.parse_args()
+    if args.powerlaw and args.n == 8000:
+        args.n = 16384
     n = args.n
     dev = torch.device("cuda")
-    b = torch.from_numpy(G.generate_uniform_sparse(n, 0.0, G.derive_seed(1, n, 0xB))).to(dev)
+    if args.powerlaw:
+        b = 1.0 - torch.rand((n, n), device=dev, dtype=torch.float32, generator=torch.Generator(device=dev).manual_seed(1))
+    else:
+        b = torch.from_numpy(G.generate_uniform_sparse(n, 0.0, G.derive_seed(1, n, 0xB))).to(dev)
     c = torch.empty((n, n), dtype=torch.float32, device=dev)
     torch.cuda.synchronize()
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
     st = torch.cuda.Stream()
     for s in args.s:
-        d = G.dense_to_gcoo_dev(torch.from_numpy(G.generate_uniform_sparse(n, s, 1)).to(dev), 4)
+        if args.powerlaw:
+            v, r, cc = G.generate_powerlaw_coo(n, s, 1.0, 1)
+            d = G.coo_to_gcoo_dev(n, n, torch.from_numpy(v).to(dev), torch.from_numpy(r).to(dev),
+                                  torch.from_numpy(cc).to(dev), 4)
+        else:
+            d = G.dense_to_gcoo_dev(torch.from_numpy(G.generate_uniform_sparse(n, s, 1)).to(dev), 4)
         torch.cuda.synchronize()
         ref = None
         for kname in args.kernels:

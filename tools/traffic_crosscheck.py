@@ -37,7 +37,7 @@ def tiling(kernel_name):
     """RB, W, KC of the profiled kernel from its template arguments
     (TaccCfg<V, KC, STAGES, CAP, NW>: RB = NW * (512 / (NW/4) & ~7) / V; TileCfg: RB = 15 * 64 / V)."""
     import re
-    m = re.search(r"TaccCfg<(\d+), (\d+), \d+, \d+(?:, (\d+))?(?:, (\d+))?>", kernel_name)
+    m = re.search(r"TaccCfg<(\d+), (\d+), \d+, \d+(?:, (\d+))?(?:, (\d+))?(?:, \w+)?>", kernel_name)
     if m:
         v, kc, nw, epr = int(m.group(1)), int(m.group(2)), int(m.group(3) or 16), int(m.group(4) or 2)
         tcols = (512 // (nw // 4)) & ~7
