@@ -649,4 +649,8 @@ __all__ = [
     "csr_to_gcoo", "spdm_gcoo", "spdm_gcoo_auto", "spdm_gcoo_dev", "coo_to_gcoo_dev", "dense_to_gcoo_dev",
     "derive_seed", "generate_uniform_sparse", "generate_uniform_sparse_coo", "generate_powerlaw_coo",
     "device_count", "set_device", "launch_count", "lib", "FLAVOR_FMA", "FLAVOR_MUL_ADD",
+    "read_matrix_market", "write_matrix_market", "read_matrix_market_gcoo_dev", "CooMatrix", "ParseError",
 ]
+
+# MatrixMarket I/O (io.hpp:21-109), as in the reference's gcoo namespace
+from .mmio import CooMatrix, ParseError, read_matrix_market, read_matrix_market_gcoo_dev, write_matrix_market  # noqa: E402
