@@ -402,13 +402,18 @@ int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const 
     // measured crossovers at n=8000 (profiles/r01_kernel_sweep_28w.jsonl): TMEM accumulators
     // with 28 warps everywhere, the chunk depth shrinking as the density grows (the record
     // stage must hold a chunk's records); 16 warps at the sparse end
+    // (profiles/r01_kernel_sweep_kc.jsonl: a deeper chunk with a smaller record stage where
+    // the stage still holds a chunk's records — KC 200 / 12 KB at 0.35-1.1 %, 16 warps with
+    // KC 216 / 4 KB below 0.2 %)
     const int pick = g_force_kernel > 0    ? g_force_kernel
                      : density >= 0.3      ? 15
                      : density >= 0.12     ? 14
                      : density >= 0.06     ? 13
                      : density >= 0.017    ? 12
-                     : density >= 0.0025   ? 11
-                                           : 8;
+                     : density >= 0.011    ? 11
+                     : density >= 0.0035   ? 16
+                     : density >= 0.002    ? 8
+                                           : 17;
     switch (pick) {
       case 5: return tile_fits<TileV4>(a, n, ldb, ldc, B, C) ? 5 : 0;
       case 8: return tile_fits<TaccV4>(a, n, ldb, ldc, B, C) ? 8 : 0;
@@ -419,6 +424,8 @@ int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const 
       case 13: return tile_fits<Tacc28K128>(a, n, ldb, ldc, B, C) ? 13 : 0;
       case 14: return tile_fits<Tacc28K96>(a, n, ldb, ldc, B, C) ? 14 : 0;
       case 15: return tile_fits<Tacc28K64>(a, n, ldb, ldc, B, C) ? 15 : 0;
+      case 16: return tile_fits<Tacc28K200>(a, n, ldb, ldc, B, C) ? 16 : 0;
+      case 17: return tile_fits<TaccV4K216>(a, n, ldb, ldc, B, C) ? 17 : 0;
       default: return 0;
     }
   } else {  // fp64: TMEM kernels with one-entry records
@@ -453,6 +460,8 @@ void make_plan(SpdmPlan& P, const DevGcoo<T>& a, int kind, cudaStream_t s, int64
     if (kind == 13) build_plan<Tacc28K128, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K128::W));
     if (kind == 14) build_plan<Tacc28K96, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K96::W));
     if (kind == 15) build_plan<Tacc28K64, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K64::W));
+    if (kind == 16) build_plan<Tacc28K200, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K200::W));
+    if (kind == 17) build_plan<TaccV4K216, true>(P, a, s, wave, ceil_div(strip_n, TaccV4K216::W));
   } else {
     if (kind == 20) build_plan<Tacc28F64K160, true>(P, a, s, wave, ceil_div(strip_n, Tacc28F64K160::W));
     if (kind == 21) build_plan<Tacc28F64K96, true>(P, a, s, wave, ceil_div(strip_n, Tacc28F64K96::W));
@@ -474,6 +483,8 @@ void run_spdm(const SpdmPlan& P, const DevGcoo<T>& a, int64_t n, const T* B, int
     if (P.kind == 13) return run_plan<Tacc28K128, true>(P, a, n, B, ldb, C, ldc, s);
     if (P.kind == 14) return run_plan<Tacc28K96, true>(P, a, n, B, ldb, C, ldc, s);
     if (P.kind == 15) return run_plan<Tacc28K64, true>(P, a, n, B, ldb, C, ldc, s);
+    if (P.kind == 16) return run_plan<Tacc28K200, true>(P, a, n, B, ldb, C, ldc, s);
+    if (P.kind == 17) return run_plan<TaccV4K216, true>(P, a, n, B, ldb, C, ldc, s);
   } else {
     if (P.kind == 20) return run_plan<Tacc28F64K160, true>(P, a, n, B, ldb, C, ldc, s);
     if (P.kind == 21) return run_plan<Tacc28F64K96, true>(P, a, n, B, ldb, C, ldc, s);
