@@ -26,6 +26,7 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <type_traits>
 
 namespace gcoo_b200 {
 
@@ -66,6 +67,25 @@ __device__ __forceinline__ void load_b(const T* __restrict__ B, int64_t ldb, int
   }
 }
 
+// One accumulator row += a * B row, element-wise in column order.  fp32 FMA
+// flavour: packed f32x2 FMAs (FFMA2: two independent round-to-nearest FMAs,
+// the same bits) to halve the FMA issue slots.
+template <typename T, int V, bool FMA>
+__device__ __forceinline__ void mac_row(T (&acc)[V], T a, const T (&bv)[V]) {
+  if constexpr (std::is_same<T, float>::value && FMA && V % 2 == 0) {
+    const float2 a2 = make_float2(a, a);
+#pragma unroll
+    for (int v = 0; v < V; v += 2) {
+      const float2 r = __ffma2_rn(a2, make_float2(bv[v], bv[v + 1]), make_float2(acc[v], acc[v + 1]));
+      acc[v] = r.x;
+      acc[v + 1] = r.y;
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = mac<T, FMA>(acc[v], a, bv[v]);
+  }
+}
+
 template <typename T, int PMAX, int V, bool FMA>
 __device__ __forceinline__ void accumulate(T (&acc)[PMAX][V], int slot, T a, const T (&bv)[V]) {
   // Warp-uniform switch: slot is the same in every lane, so this is one
@@ -73,7 +93,7 @@ __device__ __forceinline__ void accumulate(T (&acc)[PMAX][V], int slot, T a, con
 #define GCOO_CASE(s)                                                        \
   case s:                                                                   \
     if constexpr ((s) < PMAX) {                                             \
-      _Pragma("unroll") for (int v = 0; v < V; ++v) acc[s][v] = mac<T, FMA>(acc[s][v], a, bv[v]); \
+      mac_row<T, V, FMA>(acc[s], a, bv);                                     \
     }                                                                       \
     break;
   switch (slot) {
