@@ -415,6 +415,32 @@ def test_full_size_n8000_matches_reference_hashes(gcoo, cuda, oracle, golden_has
     assert [st2.flops, st2.b_loads_total, st2.b_loads_reused, st2.staging_fills] == ent["stats_p4_b64"]
 
 
+@pytest.mark.parametrize("s", [0.999, 0.9975, 0.993, 0.985, 0.96, 0.85, 0.7])
+def test_auto_choice_each_density_band_n8000_bit_exact(gcoo, cuda, oracle, s):
+    """The kernel `choose_kind` picks at every density band (16 warps KC 216 /
+    KC 192; 28 warps KC 200 / 192 / 160 / 128 / 96 / 64) on the full-size
+    reference inputs, against the oracle's FMA chain bit for bit (sampled rows
+    for the dense bands to keep the CPU check short)."""
+    import torch
+    n = 8000
+    a = gcoo.generate_uniform_sparse(n, s, 1)
+    bm = gcoo.generate_uniform_sparse(n, 0.0, gcoo.derive_seed(1, n, 0xB))
+    d = gcoo.dense_to_gcoo_dev(torch.from_numpy(a).cuda(), 4)
+    ct = torch.empty((n, n), dtype=torch.float32, device="cuda")
+    gcoo.spdm_gcoo_dev(d, torch.from_numpy(bm).cuda(), ct)
+    torch.cuda.synchronize()
+    c = ct.cpu().numpy()
+    g = oracle.dense_to_gcoo(a, 4)
+    if s >= 0.99:
+        want, _ = oracle.spdm(g, bm, fma=True)
+        assert c.tobytes() == want.tobytes()
+    else:
+        rng = np.random.default_rng(int(s * 1000))
+        for r0 in sorted(rng.choice(n // 8, 6, replace=False) * 8):
+            want = oracle.spdm_rows(g, bm, int(r0), int(r0) + 8, fma=True)[r0:r0 + 8]
+            assert c[r0:r0 + 8].tobytes() == want.tobytes(), r0
+
+
 @pytest.mark.parametrize("n", [2048, 2304, 2050, 3001])
 def test_host_pipeline_strips_bitwise_equal(gcoo, cuda, oracle, n):
     """The host-pointer path splits B/C into column strips on three streams
