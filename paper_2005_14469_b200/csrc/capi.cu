@@ -404,7 +404,7 @@ int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const 
     // stage must hold a chunk's records); 16 warps at the sparse end
     // (profiles/r01_kernel_sweep_kc.jsonl: a deeper chunk with a smaller record stage where
     // the stage still holds a chunk's records — KC 200 / 12 KB at 0.35-1.1 %, 16 warps with
-    // KC 216 / 4 KB below 0.2 %)
+    // KC 216 / 4 KB up to 0.22 %)
     const int pick = g_force_kernel > 0    ? g_force_kernel
                      : density >= 0.3      ? 15
                      : density >= 0.12     ? 14
@@ -412,7 +412,7 @@ int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const 
                      : density >= 0.017    ? 12
                      : density >= 0.011    ? 11
                      : density >= 0.0035   ? 16
-                     : density >= 0.002    ? 8
+                     : density >= 0.0022   ? 8
                                            : 17;
     switch (pick) {
       case 5: return tile_fits<TileV4>(a, n, ldb, ldc, B, C) ? 5 : 0;

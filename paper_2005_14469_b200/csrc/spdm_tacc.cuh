@@ -84,7 +84,7 @@ struct TaccCfg {
 };
 
 //                      V  KC   S  CAP
-using TaccV4 = TaccCfg<4, 192, 2, 16384>;   // W=128, RB=512, 16 warps: density 0.2 % .. 0.35 %
+using TaccV4 = TaccCfg<4, 192, 2, 16384>;   // W=128, RB=512, 16 warps: density 0.22 % .. 0.35 %
 using TaccV2 = TaccCfg<2, 256, 2, 16384>;   // W=64,  RB=1024 (tests / measurements only)
 using TaccV4W = TaccCfg<4, 192, 2, 16384, 24>;  // W=128, RB=480, 24 warps (previous default; tests / measurements)
 // 28 consumer warps (RB=504): the chunk depth KC trades run length (swaps per
@@ -100,7 +100,7 @@ using Tacc28K128 = TaccCfg<4, 128, 2, 49152, 28, 3>;  //         .. 12 %
 using Tacc28K96 = TaccCfg<4, 96, 2, 65536, 28, 3>;    //         .. 30 %
 using Tacc28K64 = TaccCfg<4, 64, 2, 81920, 28, 3>;    //      >= 30 %
 // Deeper chunks (fewer TMEM swaps per entry) where a smaller record stage still
-// holds a chunk's records: density 0.35 % .. 1.1 % (28 warps) and < 0.2 % (16 warps)
+// holds a chunk's records: density 0.35 % .. 1.1 % (28 warps) and < 0.22 % (16 warps)
 using Tacc28K200 = TaccCfg<4, 200, 2, 12288, 28>;
 using TaccV4K216 = TaccCfg<4, 216, 2, 4096>;
 // fp64 (the reference's GCOO_SCALAR_F64 build): 64 doubles per CTA strip,
