@@ -29,7 +29,7 @@ gp = G.GcooMatrix(g.rows_dim, g.cols_dim, g.p, pin(g.values), pin(g.row_idx), pi
                   pin(g.nnz_per_group))
 bp = pin(b)
 cp = pin(np.empty((n, n), np.float32))
-for strips in (1, 8, 12, 16, 24, 32, 64):
+for strips in [int(x) for x in os.environ.get("STRIPS", "1 8 12 16 24 32 64").split()]:
     G.lib().gcoo_debug_pipeline_strips(strips)
     G.spdm_gcoo(gp, bp, out=cp)
     ts = []
