@@ -409,7 +409,8 @@ int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const 
                      : density >= 0.3      ? 15
                      : density >= 0.12     ? 14
                      : density >= 0.06     ? 13
-                     : density >= 0.017    ? 12
+                     : density >= 0.035    ? 12
+                     : density >= 0.017    ? 18
                      : density >= 0.011    ? 11
                      : density >= 0.0035   ? 16
                      : density >= 0.0022   ? 8
@@ -426,6 +427,7 @@ int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const 
       case 15: return tile_fits<Tacc28K64>(a, n, ldb, ldc, B, C) ? 15 : 0;
       case 16: return tile_fits<Tacc28K200>(a, n, ldb, ldc, B, C) ? 16 : 0;
       case 17: return tile_fits<TaccV4K216>(a, n, ldb, ldc, B, C) ? 17 : 0;
+      case 18: return tile_fits<Tacc28K176>(a, n, ldb, ldc, B, C) ? 18 : 0;
       default: return 0;
     }
   } else {  // fp64: TMEM kernels with one-entry records
@@ -462,6 +464,7 @@ void make_plan(SpdmPlan& P, const DevGcoo<T>& a, int kind, cudaStream_t s, int64
     if (kind == 15) build_plan<Tacc28K64, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K64::W));
     if (kind == 16) build_plan<Tacc28K200, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K200::W));
     if (kind == 17) build_plan<TaccV4K216, true>(P, a, s, wave, ceil_div(strip_n, TaccV4K216::W));
+    if (kind == 18) build_plan<Tacc28K176, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K176::W));
   } else {
     if (kind == 20) build_plan<Tacc28F64K160, true>(P, a, s, wave, ceil_div(strip_n, Tacc28F64K160::W));
     if (kind == 21) build_plan<Tacc28F64K96, true>(P, a, s, wave, ceil_div(strip_n, Tacc28F64K96::W));
@@ -485,6 +488,7 @@ void run_spdm(const SpdmPlan& P, const DevGcoo<T>& a, int64_t n, const T* B, int
     if (P.kind == 15) return run_plan<Tacc28K64, true>(P, a, n, B, ldb, C, ldc, s);
     if (P.kind == 16) return run_plan<Tacc28K200, true>(P, a, n, B, ldb, C, ldc, s);
     if (P.kind == 17) return run_plan<TaccV4K216, true>(P, a, n, B, ldb, C, ldc, s);
+    if (P.kind == 18) return run_plan<Tacc28K176, true>(P, a, n, B, ldb, C, ldc, s);
   } else {
     if (P.kind == 20) return run_plan<Tacc28F64K160, true>(P, a, n, B, ldb, C, ldc, s);
     if (P.kind == 21) return run_plan<Tacc28F64K96, true>(P, a, n, B, ldb, C, ldc, s);

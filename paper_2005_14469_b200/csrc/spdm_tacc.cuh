@@ -95,13 +95,14 @@ using Tacc28K192 = TaccCfg<4, 192, 2, 16384, 28>;     // density 1.1 % .. 1.7 %
 // the denser configurations pack three entries per record (long runs fill
 // them; 3-10 % faster), the sparsest two (pairs of records in flight matter
 // more there)
-using Tacc28K160 = TaccCfg<4, 160, 2, 32768, 28, 3>;  //         .. 6 %
+using Tacc28K160 = TaccCfg<4, 160, 2, 32768, 28, 3>;  // 3.5 %   .. 6 %
 using Tacc28K128 = TaccCfg<4, 128, 2, 49152, 28, 3>;  //         .. 12 %
 using Tacc28K96 = TaccCfg<4, 96, 2, 65536, 28, 3>;    //         .. 30 %
 using Tacc28K64 = TaccCfg<4, 64, 2, 81920, 28, 3>;    //      >= 30 %
 // Deeper chunks (fewer TMEM swaps per entry) where a smaller record stage still
 // holds a chunk's records: density 0.35 % .. 1.1 % (28 warps) and < 0.22 % (16 warps)
 using Tacc28K200 = TaccCfg<4, 200, 2, 12288, 28>;
+using Tacc28K176 = TaccCfg<4, 176, 2, 24576, 28, 3>;  // three-entry records, density 1.7 % .. 3.5 %
 using TaccV4K216 = TaccCfg<4, 216, 2, 4096>;
 // fp64 (the reference's GCOO_SCALAR_F64 build): 64 doubles per CTA strip,
 // 504 rows, one entry per 16-byte record

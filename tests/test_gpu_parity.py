@@ -99,7 +99,7 @@ def test_random_shapes_bit_exact(gcoo, cuda, oracle, seed):
 
 
 @pytest.mark.parametrize("kernel", ["rowtile", "tile_v4", "tacc_v4", "tacc_v2", "tacc_v4w", "tacc28_k192", "tacc28_k160",
-                                    "tacc28_k128", "tacc28_k96", "tacc28_k64", "tacc28_k200", "tacc_v4_k216", "auto"])
+                                    "tacc28_k128", "tacc28_k96", "tacc28_k64", "tacc28_k200", "tacc_v4_k216", "tacc28_k176", "auto"])
 def test_each_fp32_kernel_bit_exact(gcoo, cuda, oracle, kernel):
     """Every fp32 kernel variant, on shapes that hit its edges (m not a multiple
     of the row block, k not a multiple of the chunk, n not a multiple of the
