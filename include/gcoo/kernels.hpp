@@ -17,12 +17,15 @@
 #include <cstdint>
 #include <span>
 #include <stdexcept>
-#include <thread>
 #include <vector>
 
 #include "gcoo/capi_bridge.hpp"
 #include "gcoo/matrix.hpp"
 #include "gcoo/types.hpp"
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 namespace gcoo {
 
@@ -39,10 +42,15 @@ struct ExecConfig {
   }
 };
 
+// kernels.hpp:39-46: all OpenMP threads (1 without OpenMP).  Reported by
+// run_benchmark; the GPU result does not depend on it.
 inline int resolve_workers(int workers) {
   if (workers > 0) return workers;
-  const unsigned hc = std::thread::hardware_concurrency();
-  return hc ? static_cast<int>(hc) : 1;
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
 }
 
 // Counters of the reference's tile schedule for the caller's b (:52-65):

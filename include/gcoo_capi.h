@@ -194,6 +194,10 @@ int gcoo_coo_to_gcoo_f32_dev(int64_t m, int64_t k, int32_t p, int64_t nnz, const
                              const int32_t* row_idx, const int32_t* col_idx, float* out_values,
                              int32_t* out_row_idx, int32_t* out_col_idx, int64_t* g_idxes,
                              int64_t* nnz_per_group, void* stream);
+int gcoo_coo_to_gcoo_f64_dev(int64_t m, int64_t k, int32_t p, int64_t nnz, const double* values,
+                             const int32_t* row_idx, const int32_t* col_idx, double* out_values,
+                             int32_t* out_row_idx, int32_t* out_col_idx, int64_t* g_idxes,
+                             int64_t* nnz_per_group, void* stream);
 
 /*
  * csr_to_gcoo — new entry point (the north star's "COO/CSR-to-GCOO"); the
@@ -208,6 +212,16 @@ int gcoo_csr_to_gcoo_f64(int64_t m, int64_t k, int32_t p, int64_t nnz, const dou
                          const int32_t* col_idx, const int64_t* row_ptr, double* out_values,
                          int32_t* out_row_idx, int32_t* out_col_idx, int64_t* g_idxes,
                          int64_t* nnz_per_group);
+/* Device variants (all arrays device pointers; synchronise `stream` for the
+ * validation verdict). */
+int gcoo_csr_to_gcoo_f32_dev(int64_t m, int64_t k, int32_t p, int64_t nnz, const float* values,
+                             const int32_t* col_idx, const int64_t* row_ptr, float* out_values,
+                             int32_t* out_row_idx, int32_t* out_col_idx, int64_t* g_idxes,
+                             int64_t* nnz_per_group, void* stream);
+int gcoo_csr_to_gcoo_f64_dev(int64_t m, int64_t k, int32_t p, int64_t nnz, const double* values,
+                             const int32_t* col_idx, const int64_t* row_ptr, double* out_values,
+                             int32_t* out_row_idx, int32_t* out_col_idx, int64_t* g_idxes,
+                             int64_t* nnz_per_group, void* stream);
 
 /*
  * dense_to_gcoo (matrix.hpp:306-353).  A is m x k row-major; entries != 0
@@ -230,6 +244,10 @@ int gcoo_dense_to_gcoo_f64(int64_t m, int64_t k, int32_t p, const double* A, int
  * the caller can allocate and call again). */
 int gcoo_dense_to_gcoo_f32_dev(int64_t m, int64_t k, int32_t p, const float* A, int64_t capacity,
                                float* out_values, int32_t* out_row_idx, int32_t* out_col_idx,
+                               int64_t* g_idxes, int64_t* nnz_per_group, int64_t* nnz,
+                               void* stream);
+int gcoo_dense_to_gcoo_f64_dev(int64_t m, int64_t k, int32_t p, const double* A, int64_t capacity,
+                               double* out_values, int32_t* out_row_idx, int32_t* out_col_idx,
                                int64_t* g_idxes, int64_t* nnz_per_group, int64_t* nnz,
                                void* stream);
 

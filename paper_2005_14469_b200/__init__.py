@@ -89,17 +89,22 @@ def lib():
     _sig(L, "gcoo_coo_to_gcoo_f32", _int, coo_args)
     _sig(L, "gcoo_coo_to_gcoo_f64", _int, coo_args)
     _sig(L, "gcoo_coo_to_gcoo_f32_dev", _int, coo_args + [_vp])
+    _sig(L, "gcoo_coo_to_gcoo_f64_dev", _int, coo_args + [_vp])
+    _sig(L, "gcoo_csr_to_gcoo_f32_dev", _int, coo_args + [_vp])
+    _sig(L, "gcoo_csr_to_gcoo_f64_dev", _int, coo_args + [_vp])
     _sig(L, "gcoo_csr_to_gcoo_f32", _int, coo_args)
     _sig(L, "gcoo_csr_to_gcoo_f64", _int, coo_args)
     dense_args = [_i64, _i64, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, C.POINTER(_i64)]
     _sig(L, "gcoo_dense_to_gcoo_f32", _int, dense_args)
     _sig(L, "gcoo_dense_to_gcoo_f64", _int, dense_args)
     _sig(L, "gcoo_dense_to_gcoo_f32_dev", _int, dense_args + [_vp])
+    _sig(L, "gcoo_dense_to_gcoo_f64_dev", _int, dense_args + [_vp])
     _sig(L, "gcoo_generate_uniform_sparse_f32", _int, [_i64, _dbl, _u64, _vp])
     _sig(L, "gcoo_generate_uniform_sparse_coo_f32", _int, [_i64, _dbl, _u64, _i64, _vp, _vp, _vp, C.POINTER(_i64)])
     _sig(L, "gcoo_generate_powerlaw_coo_f32", _int, [_i64, _dbl, _dbl, _u64, _i64, _vp, _vp, _vp, C.POINTER(_i64)])
     _sig(L, "gcoo_derive_seed", _u64, [_u64, _u64, _u64])
     _sig(L, "gcoo_debug_force_kernel", _int, [_int])
+    _sig(L, "gcoo_debug_last_kernel", _int, [])
     _sig(L, "gcoo_plan_create_f32_dev", _int, [_i64, _i64, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _int,
                                                 C.POINTER(_vp), _vp])
     _sig(L, "gcoo_plan_spdm_f32_dev", _int, [_vp, _i64, _vp, _i64, _vp, _i64, _vp])
@@ -143,7 +148,7 @@ def set_device(device: int) -> None:
     _check(lib().gcoo_set_device(device))
 
 
-KERNELS = {"auto": -1, "rowtile": 0, "tile_v4": 5, "tacc_v4": 8, "tacc_v2": 9, "tacc_v4w": 10, "tacc28_k192": 11, "tacc28_k160": 12,
+KERNELS = {"auto": -1, "rowtile": 0, "tacc_v4": 8, "tacc28_k192": 11, "tacc28_k160": 12,
            "tacc28_k128": 13, "tacc28_k96": 14, "tacc28_k64": 15, "tacc28_k200": 16, "tacc_v4_k216": 17, "tacc28_k176": 18,
            "tacc28_f64_k160": 20, "tacc28_f64_k96": 21, "tacc28_f64_k64": 22}
 
@@ -151,6 +156,12 @@ KERNELS = {"auto": -1, "rowtile": 0, "tile_v4": 5, "tacc_v4": 8, "tacc_v2": 9, "
 def force_kernel(which: str = "auto") -> None:
     """Test/benchmark hook: pin the fp32 multiply kernel (auto = heuristic)."""
     lib().gcoo_debug_force_kernel(KERNELS[which])
+
+
+def last_kernel() -> str:
+    """Test hook: the multiply kernel this thread's latest call ran (a KERNELS name)."""
+    k = int(lib().gcoo_debug_last_kernel())
+    return next((name for name, v in KERNELS.items() if v == k and name != "auto"), str(k))
 
 
 def kernel_timing(enable: bool = True) -> None:
@@ -498,6 +509,38 @@ def _stream_ptr(stream) -> Optional[int]:
     return stream if isinstance(stream, int) else stream.cuda_stream
 
 
+def _check_device_gcoo(a: "DeviceGcoo") -> None:
+    """A's device arrays: one CUDA device, contiguous, fp32/fp64 values, int32
+    coordinates, int64 group arrays — anything else would be read as garbage
+    by the C ABI, so it is rejected here."""
+    import torch
+    if a.values.dtype not in (torch.float32, torch.float64):
+        raise ValueError("DeviceGcoo: values must be float32 or float64")
+    for name, t, dt in (("values", a.values, a.values.dtype), ("row_idx", a.row_idx, torch.int32),
+                        ("col_idx", a.col_idx, torch.int32), ("g_idxes", a.g_idxes, torch.int64),
+                        ("nnz_per_group", a.nnz_per_group, torch.int64)):
+        if t.dtype != dt:
+            raise ValueError(f"DeviceGcoo: {name} must be {dt}")
+        if not t.is_cuda or t.device != a.values.device:
+            raise ValueError(f"DeviceGcoo: {name} must live on the values' CUDA device")
+        if not t.is_contiguous():
+            raise ValueError(f"DeviceGcoo: {name} must be contiguous")
+
+
+def _check_operands(a: "DeviceGcoo", b, c) -> None:
+    """B (k x n) and C (m x n): A's dtype and device, 2-D, unit column stride."""
+    _check_device_gcoo(a)
+    for name, t in (("B", b), ("C", c)):
+        if t.dim() != 2:
+            raise ValueError(f"spdm_gcoo_dev: {name} must be 2-D")
+        if t.dtype != a.values.dtype:
+            raise ValueError(f"spdm_gcoo_dev: {name} dtype {t.dtype} differs from A's {a.values.dtype}")
+        if t.device != a.values.device:
+            raise ValueError(f"spdm_gcoo_dev: {name} is not on A's device")
+        if t.stride(1) != 1:
+            raise ValueError("spdm_gcoo_dev: B and C need unit column stride")
+
+
 def spdm_gcoo_dev(a: DeviceGcoo, b, c, cfg: Optional[ExecConfig] = None, flavor: int = FLAVOR_FMA,
                   stream=None, stats: Optional[KernelStats] = None) -> None:
     """Stream-ordered C = A * B on device tensors (b: k x n, c: m x n; a
@@ -505,8 +548,7 @@ def spdm_gcoo_dev(a: DeviceGcoo, b, c, cfg: Optional[ExecConfig] = None, flavor:
     import torch
     cfg = cfg or ExecConfig(p=a.p)
     n = b.shape[1]
-    if b.stride(1) != 1 or c.stride(1) != 1:
-        raise ValueError("spdm_gcoo_dev: B and C need unit column stride")
+    _check_operands(a, b, c)
     if b.shape[0] != a.cols_dim:
         raise ValueError("spdm_gcoo: inner dimensions differ")
     if cfg.p != a.p:
@@ -515,7 +557,7 @@ def spdm_gcoo_dev(a: DeviceGcoo, b, c, cfg: Optional[ExecConfig] = None, flavor:
         raise ValueError("spdm_gcoo_dev: C has the wrong shape")
     st = _Stats()
     L = lib()
-    f = L.gcoo_spdm_f32_dev if b.dtype == torch.float32 else L.gcoo_spdm_f64_dev
+    f = L.gcoo_spdm_f32_dev if a.values.dtype == torch.float32 else L.gcoo_spdm_f64_dev
     _check(f(a.rows_dim, a.cols_dim, n, a.p, cfg.b, a.nnz(), _p(a.values), _p(a.row_idx), _p(a.col_idx),
              a.groups(), _p(a.g_idxes), _p(a.nnz_per_group), _p(b), b.stride(0), _p(c), c.stride(0),
              C.byref(st) if stats is not None else None, flavor, _stream_ptr(stream)))
@@ -535,6 +577,7 @@ class SpdmPlan:
         import torch
         self.a = a
         self._h = _vp()
+        _check_device_gcoo(a)
         self._f64 = a.values.dtype == torch.float64
         create = lib().gcoo_plan_create_f64_dev if self._f64 else lib().gcoo_plan_create_f32_dev
         _check(create(a.rows_dim, a.cols_dim, a.p, a.nnz(), _p(a.values), _p(a.row_idx), _p(a.col_idx), a.groups(),
@@ -542,8 +585,7 @@ class SpdmPlan:
 
     def run(self, b, c, stream=None) -> None:
         import torch
-        if b.stride(1) != 1 or c.stride(1) != 1:
-            raise ValueError("spdm_gcoo_dev: B and C need unit column stride")
+        _check_operands(self.a, b, c)
         if b.shape[0] != self.a.cols_dim or c.shape[0] != self.a.rows_dim or c.shape[1] != b.shape[1]:
             raise ValueError("spdm_gcoo: operand shapes do not match the plan's A")
         if self._h is None:
@@ -565,8 +607,26 @@ class SpdmPlan:
             pass
 
 
-def coo_to_gcoo_dev(rows_dim: int, cols_dim: int, values, row_idx, col_idx, p: int, stream=None) -> DeviceGcoo:
+def _dev_array(name: str, t, dtypes):
     import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype not in dtypes:
+        raise ValueError(f"{name} must be one of {dtypes}, got {t.dtype}")
+    return t.contiguous()
+
+
+def coo_to_gcoo_dev(rows_dim: int, cols_dim: int, values, row_idx, col_idx, p: int, stream=None) -> DeviceGcoo:
+    """coo_to_gcoo (matrix.hpp:366-405) on device arrays (fp32 or fp64 values,
+    int32 coordinates, one device); validated like CooMatrix::validate."""
+    import torch
+    values = _dev_array("values", values, (torch.float32, torch.float64))
+    row_idx = _dev_array("row_idx", row_idx, (torch.int32,))
+    col_idx = _dev_array("col_idx", col_idx, (torch.int32,))
+    if not (values.numel() == row_idx.numel() == col_idx.numel()):
+        raise ValueError("CooMatrix: array lengths differ")
+    if row_idx.device != values.device or col_idx.device != values.device:
+        raise ValueError("coo_to_gcoo_dev: arrays on different devices")
     n = values.numel()
     g = -(-rows_dim // p) if _pow2(p) else 1
     dev = values.device
@@ -576,15 +636,49 @@ def coo_to_gcoo_dev(rows_dim: int, cols_dim: int, values, row_idx, col_idx, p: i
     gi = torch.empty(g, dtype=torch.int64, device=dev)
     gn = torch.empty(g, dtype=torch.int64, device=dev)
     sp = _stream_ptr(stream)
-    _check(lib().gcoo_coo_to_gcoo_f32_dev(rows_dim, cols_dim, p, n, _p(values), _p(row_idx), _p(col_idx), _p(ov),
-                                          _p(orr), _p(oc), _p(gi), _p(gn), sp))
+    L = lib()
+    f = L.gcoo_coo_to_gcoo_f64_dev if values.dtype == torch.float64 else L.gcoo_coo_to_gcoo_f32_dev
+    _check(f(rows_dim, cols_dim, p, n, _p(values), _p(row_idx), _p(col_idx), _p(ov), _p(orr), _p(oc), _p(gi),
+             _p(gn), sp))
     # setup routine: finish before the arrays are handed to other streams
-    _check(lib().gcoo_stream_sync(sp))
+    _check(L.gcoo_stream_sync(sp))
+    return DeviceGcoo(rows_dim, cols_dim, p, ov, orr, oc, gi, gn)
+
+
+def csr_to_gcoo_dev(rows_dim: int, cols_dim: int, values, col_idx, row_ptr, p: int, stream=None) -> DeviceGcoo:
+    """CSR -> GCOO on device arrays (int64 row_ptr[rows_dim+1], int32 columns);
+    validated like CsrMatrix::validate (matrix.hpp:122-165)."""
+    import torch
+    values = _dev_array("values", values, (torch.float32, torch.float64))
+    col_idx = _dev_array("col_idx", col_idx, (torch.int32,))
+    row_ptr = _dev_array("row_ptr", row_ptr, (torch.int64,))
+    if values.numel() != col_idx.numel():
+        raise ValueError("CsrMatrix: array lengths differ")
+    if row_ptr.numel() != rows_dim + 1:
+        raise ValueError("CsrMatrix: row_ptr must have rows_dim+1 entries")
+    n = values.numel()
+    g = -(-rows_dim // p) if _pow2(p) else 1
+    dev = values.device
+    ov = torch.empty(n, dtype=values.dtype, device=dev)
+    orr = torch.empty(n, dtype=torch.int32, device=dev)
+    oc = torch.empty(n, dtype=torch.int32, device=dev)
+    gi = torch.empty(g, dtype=torch.int64, device=dev)
+    gn = torch.empty(g, dtype=torch.int64, device=dev)
+    sp = _stream_ptr(stream)
+    L = lib()
+    f = L.gcoo_csr_to_gcoo_f64_dev if values.dtype == torch.float64 else L.gcoo_csr_to_gcoo_f32_dev
+    _check(f(rows_dim, cols_dim, p, n, _p(values), _p(col_idx), _p(row_ptr), _p(ov), _p(orr), _p(oc), _p(gi),
+             _p(gn), sp))
+    _check(L.gcoo_stream_sync(sp))
     return DeviceGcoo(rows_dim, cols_dim, p, ov, orr, oc, gi, gn)
 
 
 def dense_to_gcoo_dev(a, p: int, stream=None) -> DeviceGcoo:
+    """dense_to_gcoo (matrix.hpp:306-353) on a device matrix (fp32 or fp64)."""
     import torch
+    a = _dev_array("A", a, (torch.float32, torch.float64))
+    if a.dim() != 2 or a.shape[0] < 1 or a.shape[1] < 1:
+        raise ValueError("DenseMatrix: dimensions must be >= 1")
     m, k = a.shape
     dev = a.device
     if not _pow2(p):
@@ -594,14 +688,14 @@ def dense_to_gcoo_dev(a, p: int, stream=None) -> DeviceGcoo:
     gn = torch.empty(g, dtype=torch.int64, device=dev)
     nnz = _i64(0)
     L = lib()
+    f = L.gcoo_dense_to_gcoo_f64_dev if a.dtype == torch.float64 else L.gcoo_dense_to_gcoo_f32_dev
     sp = _stream_ptr(stream)
-    _check(L.gcoo_dense_to_gcoo_f32_dev(m, k, p, _p(a), 0, None, None, None, _p(gi), _p(gn), C.byref(nnz), sp))
+    _check(f(m, k, p, _p(a), 0, None, None, None, _p(gi), _p(gn), C.byref(nnz), sp))
     n = int(nnz.value)
     ov = torch.empty(n, dtype=a.dtype, device=dev)
     orr = torch.empty(n, dtype=torch.int32, device=dev)
     oc = torch.empty(n, dtype=torch.int32, device=dev)
-    _check(L.gcoo_dense_to_gcoo_f32_dev(m, k, p, _p(a), n, _p(ov), _p(orr), _p(oc), _p(gi), _p(gn),
-                                        C.byref(nnz), sp))
+    _check(f(m, k, p, _p(a), n, _p(ov), _p(orr), _p(oc), _p(gi), _p(gn), C.byref(nnz), sp))
     # setup routine: finish before the arrays are handed to other streams
     _check(L.gcoo_stream_sync(sp))
     return DeviceGcoo(m, k, p, ov, orr, oc, gi, gn)
@@ -646,7 +740,8 @@ def generate_powerlaw_coo(n: int, s: float, alpha: float, seed: int):
 
 __all__ = [
     "ExecConfig", "KernelStats", "TimingBreakdown", "GcooMatrix", "DeviceGcoo", "dense_to_gcoo", "coo_to_gcoo",
-    "csr_to_gcoo", "spdm_gcoo", "spdm_gcoo_auto", "spdm_gcoo_dev", "coo_to_gcoo_dev", "dense_to_gcoo_dev",
+    "csr_to_gcoo", "spdm_gcoo", "spdm_gcoo_auto", "spdm_gcoo_dev", "coo_to_gcoo_dev", "csr_to_gcoo_dev",
+    "dense_to_gcoo_dev", "SpdmPlan",
     "derive_seed", "generate_uniform_sparse", "generate_uniform_sparse_coo", "generate_powerlaw_coo",
     "device_count", "set_device", "launch_count", "lib", "FLAVOR_FMA", "FLAVOR_MUL_ADD",
     "read_matrix_market", "write_matrix_market", "read_matrix_market_gcoo_dev", "CooMatrix", "ParseError",

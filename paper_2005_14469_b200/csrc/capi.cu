@@ -3,7 +3,7 @@
 // Host-side orchestration only: argument validation in the reference's order
 // (so the same inputs raise the same exception class), device buffers from the
 // stream-ordered pool, copies, and kernel launches.  All arithmetic on matrix
-// data happens in the CUDA kernels (spdm_rowtile.cuh, spdm_tile.cuh, spdm_tacc.cuh,
+// data happens in the CUDA kernels (spdm_rowtile.cuh, spdm_tacc.cuh,
 // construct.cuh); there is no host compute path.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -22,7 +22,6 @@
 #include "common.cuh"
 #include "construct.cuh"
 #include "spdm_rowtile.cuh"
-#include "spdm_tile.cuh"
 #include "spdm_tacc.cuh"
 
 namespace gcoo_b200 {
@@ -262,7 +261,7 @@ bool tile_fits(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const T
 // serves any number of B/C column strips with the same layout class
 // (the host-pointer path pipelines strips through one plan).
 struct SpdmPlan {
-  int kind = 0;  // 0 row-tile, 5 tile_v4, 8 tacc_v4, 9 tacc_v2, 10 tacc_v4w, 11-15 tacc28 (KC 192..64)
+  int kind = 0;  // 0 row-tile; TMEM configurations: 8 (16 warps, KC 192), 11-18 (fp32), 20-22 (fp64)
   DevBuf<int64_t> seg_off;
   DevBuf<unsigned char> ent;
   int64_t row_blocks = 0;
@@ -272,177 +271,167 @@ struct SpdmPlan {
   DevBuf<int32_t> skewed;  // 1: heaviest rows in row block 0 (launched first)
 };
 
-template <class Cfg, bool TACC>
+template <class Cfg>
 void set_smem_attr() {
-  static bool attr_set[64] = {};
-  int d = 0;
-  GCOO_CUDA(cudaGetDevice(&d));
-  if (attr_set[d]) return;
-  if constexpr (TACC)
-    GCOO_CUDA(cudaFuncSetAttribute(spdm_tacc_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)Cfg::SMEM));
-  else
-    GCOO_CUDA(cudaFuncSetAttribute(spdm_tile_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)Cfg::SMEM));
-  attr_set[d] = true;
+  // cudaFuncSetAttribute is idempotent; the flags only skip repeated calls
+  static std::atomic<bool> attr_set[64] = {};
+  const int d = current_device();
+  if (attr_set[d].load(std::memory_order_acquire)) return;
+  GCOO_CUDA(cudaFuncSetAttribute(spdm_tacc_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
+  attr_set[d].store(true, std::memory_order_release);
 }
 
 // Planner: counts -> segment sizes -> scan -> headers -> scatter, on stream s.
-// `min_ctas` (TMEM kernels): spread rows over enough row blocks that a launch
-// over `col_tiles` column tiles has at least that many CTAs (narrow strips of
-// the host pipeline); 0 = full row blocks.
-template <class Cfg, bool TACC, typename T>
+// `min_ctas`: spread rows over enough row blocks that a launch over
+// `col_tiles` column tiles has at least that many CTAs (narrow strips of the
+// host pipeline); 0 = full row blocks.
+template <class Cfg, typename T>
 void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ctas = 0, int64_t col_tiles = 1) {
-  set_smem_attr<Cfg, TACC>();
+  set_smem_attr<Cfg>();
   P.row_blocks = ceil_div(a.m, Cfg::RB);
   int64_t rpb = Cfg::RB;
-  if (TACC && min_ctas > P.row_blocks * col_tiles) {
+  if (min_ctas > P.row_blocks * col_tiles) {
     const int64_t want = std::min<int64_t>(ceil_div(min_ctas, col_tiles), ceil_div(a.m, 32));
     if (want > P.row_blocks) {
       rpb = ceil_div(a.m, want);
       P.row_blocks = ceil_div(a.m, rpb);
     }
   }
-  // TMEM kernels place rows anywhere in their row block's warps: every warp is a unit
-  const int64_t units = TACC ? P.row_blocks * Cfg::NW : ceil_div(a.m, Cfg::RW);
+  // rows are placed anywhere in their row block's warps: every warp is a unit
+  const int64_t units = P.row_blocks * Cfg::NW;
   P.nchunks = (int)ceil_div(a.k, Cfg::KC);
   const int nchunks = P.nchunks;
   const int64_t nseg = P.row_blocks * nchunks;
   // every buffer first: the kernels below form one uninterrupted PDL chain
   DevBuf<uint32_t> cnt(units * nchunks * Cfg::RW, s);
-  DevBuf<int32_t> row_nnz(TACC ? a.m : 0, s), hist(TACC ? 33 : 0, s), cursor(TACC ? 33 : 0, s);
-  if (TACC) {
-    P.unit_of = DevBuf<int32_t>(a.m, s);
-    P.row_of = DevBuf<int32_t>(P.row_blocks * Cfg::RB, s);
-    P.skewed = DevBuf<int32_t>(1, s);
-  }
+  DevBuf<int32_t> row_nnz(a.m, s), hist(33, s), cursor(33, s);
+  P.unit_of = DevBuf<int32_t>(a.m, s);
+  P.row_of = DevBuf<int32_t>(P.row_blocks * Cfg::RB, s);
+  P.skewed = DevBuf<int32_t>(1, s);
   DevBuf<int64_t> seg_len(nseg, s), scan_tmp(scan_scratch(nseg), s);
   P.seg_off = DevBuf<int64_t>(nseg + 1, s);
   // upper bound of the stream: headers + one record (16 B) per entry
   const int64_t bound = nseg * (Cfg::TABLE + Cfg::NW * Cfg::HDR) + (int64_t)Cfg::REC * a.nnz + 16;
   P.ent = DevBuf<unsigned char>(bound, s);
   DevBuf<int64_t> slot_pos(nseg * Cfg::NW * Cfg::RW, s);
-  DevBuf<uint32_t> woff(TACC ? nseg * Cfg::NW : 0, s);  // warp segment offsets inside a segment
+  DevBuf<uint32_t> woff(nseg * Cfg::NW, s);  // warp segment offsets inside a segment
 
-  const int64_t init_n = std::max<int64_t>((int64_t)cnt.count, TACC ? std::max<int64_t>(a.m, (int64_t)P.row_of.count) : 0);
+  const int64_t init_n = std::max<int64_t>((int64_t)cnt.count, std::max<int64_t>(a.m, (int64_t)P.row_of.count));
   GCOO_LAUNCH_PDL(plan_init_kernel, grid_for(init_n, 256), 256, 0, s, cnt.get(), (int64_t)cnt.count,
-                  row_nnz.get(), TACC ? a.m : (int64_t)0, hist.get(), cursor.get(), P.row_of.get(),
-                  TACC ? (int64_t)P.row_of.count : (int64_t)0);
-  if constexpr (TACC) {
-    // load-balanced row placement: heaviest rows first, dealt over a block's warps
-    if (a.nnz > 0)
-      GCOO_LAUNCH_PDL(row_nnz_kernel, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, row_nnz.get());
-    GCOO_LAUNCH_PDL(bucket_hist_kernel, grid_for(a.m, 256), 256, 0, s, a.m, (const int32_t*)row_nnz.get(), hist.get());
-    GCOO_LAUNCH_PDL(row_balance_kernel, grid_for(a.m, 256), 256, 0, s, a.m, (const int32_t*)row_nnz.get(),
-                    (const int32_t*)hist.get(), cursor.get(), (int32_t)Cfg::RB, (int32_t)Cfg::NW, (int32_t)Cfg::RW,
-                    (int32_t)std::min<int64_t>(INT32_MAX, 4 * ceil_div(a.nnz, a.m) + 16), (int32_t)rpb,
-                    P.unit_of.get(), P.row_of.get(), P.skewed.get());
-  }
-  if (a.nnz > 0) {
-    if constexpr (TACC)
-      GCOO_LAUNCH_PDL(tacc_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks,
-                      cnt.get(), (const int32_t*)P.unit_of.get());
-    else
-      GCOO_LAUNCH_PDL(tile_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks,
-                      cnt.get());
-  }
-  if constexpr (TACC)
-    GCOO_LAUNCH_PDL(tacc_size_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, (const uint32_t*)cnt.get(), units,
-                    nchunks, nseg, seg_len.get(), woff.get());
-  else
-    GCOO_LAUNCH_PDL(tile_size_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, (const uint32_t*)cnt.get(), units,
-                    nchunks, nseg, seg_len.get());
+                  row_nnz.get(), a.m, hist.get(), cursor.get(), P.row_of.get(), (int64_t)P.row_of.count);
+  // load-balanced row placement: heaviest rows first, dealt over a block's warps
+  if (a.nnz > 0)
+    GCOO_LAUNCH_PDL(row_nnz_kernel, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, row_nnz.get());
+  GCOO_LAUNCH_PDL(bucket_hist_kernel, grid_for(a.m, 256), 256, 0, s, a.m, (const int32_t*)row_nnz.get(), hist.get());
+  GCOO_LAUNCH_PDL(row_balance_kernel, grid_for(a.m, 256), 256, 0, s, a.m, (const int32_t*)row_nnz.get(),
+                  (const int32_t*)hist.get(), cursor.get(), (int32_t)Cfg::RB, (int32_t)Cfg::NW, (int32_t)Cfg::RW,
+                  (int32_t)std::min<int64_t>(INT32_MAX, 4 * ceil_div(a.nnz, a.m) + 16), (int32_t)rpb,
+                  P.unit_of.get(), P.row_of.get(), P.skewed.get());
+  if (a.nnz > 0)
+    GCOO_LAUNCH_PDL(tacc_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks,
+                    cnt.get(), (const int32_t*)P.unit_of.get());
+  GCOO_LAUNCH_PDL(tacc_size_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, (const uint32_t*)cnt.get(), units,
+                  nchunks, nseg, seg_len.get(), woff.get());
   exclusive_scan(seg_len.get(), P.seg_off.get(), nseg, s, scan_tmp.get());
-  if constexpr (TACC) {
-    GCOO_LAUNCH_PDL(tacc_header_kernel<Cfg>, grid_for(nseg * Cfg::NW * Cfg::RW, 256), 256, 0, s,
-                    (const uint32_t*)cnt.get(), units, nchunks, nseg, (const int64_t*)P.seg_off.get(),
-                    (const uint32_t*)woff.get(), P.ent.get(), slot_pos.get());
-    if (a.nnz > 0)
-      GCOO_LAUNCH_PDL(tacc_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols,
-                      a.gidx, nchunks, (const int64_t*)slot_pos.get(), P.ent.get(), (const int32_t*)P.unit_of.get());
-  } else {
-    GCOO_LAUNCH_PDL(tile_header_kernel<Cfg>, grid_for(nseg * 32, 256), 256, 0, s, (const uint32_t*)cnt.get(), units,
-                    nchunks, nseg, (const int64_t*)P.seg_off.get(), P.ent.get(), slot_pos.get());
-    if (a.nnz > 0)
-      GCOO_LAUNCH_PDL(tile_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols,
-                      a.gidx, nchunks, (const int64_t*)slot_pos.get(), P.ent.get());
-  }
+  GCOO_LAUNCH_PDL(tacc_header_kernel<Cfg>, grid_for(nseg * Cfg::NW * Cfg::RW, 256), 256, 0, s,
+                  (const uint32_t*)cnt.get(), units, nchunks, nseg, (const int64_t*)P.seg_off.get(),
+                  (const uint32_t*)woff.get(), P.ent.get(), slot_pos.get());
+  if (a.nnz > 0)
+    GCOO_LAUNCH_PDL(tacc_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols,
+                    a.gidx, nchunks, (const int64_t*)slot_pos.get(), P.ent.get(), (const int32_t*)P.unit_of.get());
 }
 
-template <class Cfg, bool TACC, typename T>
+template <class Cfg, typename T>
 void run_plan(const SpdmPlan& P, const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C,
               int64_t ldc, cudaStream_t s) {
   const CUtensorMap map = make_b_map(B, a.k, n, ldb, Cfg::W, Cfg::KC);
   const int64_t grid = P.row_blocks * ceil_div(n, Cfg::W);
   if (grid > INT32_MAX) fail(GCOO_EINVAL, "spdm_gcoo: problem too large for one launch");
   const cudaEvent_t kt0 = kt_start(s);
-  if constexpr (TACC)
-    GCOO_LAUNCH_PDL(spdm_tacc_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n,
-                    (const unsigned char*)P.ent.get(), (const int64_t*)P.seg_off.get(), C, ldc, P.row_blocks,
-                    P.nchunks, (const int32_t*)P.row_of.get(), (const int32_t*)P.skewed.get());
-  else
-    GCOO_LAUNCH_PDL(spdm_tile_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n,
-                    (const unsigned char*)P.ent.get(), (const int64_t*)P.seg_off.get(), C, ldc, P.row_blocks,
-                    P.nchunks);
+  GCOO_LAUNCH_PDL(spdm_tacc_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n,
+                  (const unsigned char*)P.ent.get(), (const int64_t*)P.seg_off.get(), C, ldc, P.row_blocks,
+                  P.nchunks, (const int32_t*)P.row_of.get(), (const int32_t*)P.skewed.get());
   kt_stop(s, kt0);
 }
 
-// Which fp32 kernel runs: a tiled configuration whenever the layout allows
-// (chosen by density), the row-tile kernel for everything else.
-int g_force_kernel = -1;  // test hook: -1 auto, 0 row-tile, 5 tile_v4, 8 tacc_v4, 9 tacc_v2
-
-template <typename T>
-int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const T* B, const T* C, int flavor) {
+// The TMEM kernel configurations by id (the ids are the test hook's and the
+// Python KERNELS table's): calls fn(Cfg{}) and returns true for a known id.
+template <typename T, typename Fn>
+bool with_cfg(int kind, Fn&& fn) {
   if constexpr (std::is_same<T, float>::value) {
-    if (flavor == GCOO_FLAVOR_MUL_ADD || g_force_kernel == 0 || a.m == 0) return 0;
-    // small products: the planner (~35 us) costs more than it saves, the
-    // row-tile kernel needs none (profiles/r01_small_n.jsonl: n <= 2000)
-    if (g_force_kernel < 0 && 2.0 * (double)a.nnz * (double)n < 4e8) return 0;
-    const double density = (double)a.nnz / ((double)a.m * (double)a.k);
-    // measured crossovers at n=8000 (profiles/r01_kernel_sweep_28w.jsonl): TMEM accumulators
-    // with 28 warps everywhere, the chunk depth shrinking as the density grows (the record
-    // stage must hold a chunk's records); 16 warps at the sparse end
-    // (profiles/r01_kernel_sweep_kc.jsonl: a deeper chunk with a smaller record stage where
-    // the stage still holds a chunk's records — KC 200 / 12 KB at 0.35-1.1 %, 16 warps with
-    // KC 216 / 4 KB up to 0.22 %)
-    const int pick = g_force_kernel > 0    ? g_force_kernel
-                     : density >= 0.3      ? 15
-                     : density >= 0.12     ? 14
-                     : density >= 0.06     ? 13
-                     : density >= 0.035    ? 12
-                     : density >= 0.017    ? 18
-                     : density >= 0.011    ? 11
-                     : density >= 0.0035   ? 16
-                     : density >= 0.0022   ? 8
-                                           : 17;
-    switch (pick) {
-      case 5: return tile_fits<TileV4>(a, n, ldb, ldc, B, C) ? 5 : 0;
-      case 8: return tile_fits<TaccV4>(a, n, ldb, ldc, B, C) ? 8 : 0;
-      case 9: return tile_fits<TaccV2>(a, n, ldb, ldc, B, C) ? 9 : 0;
-      case 10: return tile_fits<TaccV4W>(a, n, ldb, ldc, B, C) ? 10 : 0;
-      case 11: return tile_fits<Tacc28K192>(a, n, ldb, ldc, B, C) ? 11 : 0;
-      case 12: return tile_fits<Tacc28K160>(a, n, ldb, ldc, B, C) ? 12 : 0;
-      case 13: return tile_fits<Tacc28K128>(a, n, ldb, ldc, B, C) ? 13 : 0;
-      case 14: return tile_fits<Tacc28K96>(a, n, ldb, ldc, B, C) ? 14 : 0;
-      case 15: return tile_fits<Tacc28K64>(a, n, ldb, ldc, B, C) ? 15 : 0;
-      case 16: return tile_fits<Tacc28K200>(a, n, ldb, ldc, B, C) ? 16 : 0;
-      case 17: return tile_fits<TaccV4K216>(a, n, ldb, ldc, B, C) ? 17 : 0;
-      case 18: return tile_fits<Tacc28K176>(a, n, ldb, ldc, B, C) ? 18 : 0;
-      default: return 0;
+    switch (kind) {
+      case 8: fn(TaccV4{}); return true;
+      case 11: fn(Tacc28K192{}); return true;
+      case 12: fn(Tacc28K160{}); return true;
+      case 13: fn(Tacc28K128{}); return true;
+      case 14: fn(Tacc28K96{}); return true;
+      case 15: fn(Tacc28K64{}); return true;
+      case 16: fn(Tacc28K200{}); return true;
+      case 17: fn(TaccV4K216{}); return true;
+      case 18: fn(Tacc28K176{}); return true;
+      default: return false;
     }
-  } else {  // fp64: TMEM kernels with one-entry records
-    if (flavor == GCOO_FLAVOR_MUL_ADD || g_force_kernel == 0 || a.m == 0) return 0;
-    if (g_force_kernel < 0 && 2.0 * (double)a.nnz * (double)n < 4e8) return 0;
-    const double density = (double)a.nnz / ((double)a.m * (double)a.k);
-    const int pick = g_force_kernel > 0 ? g_force_kernel : density >= 0.07 ? 22 : density >= 0.025 ? 21 : 20;
-    switch (pick) {
-      case 20: return tile_fits<Tacc28F64K160>(a, n, ldb, ldc, B, C) ? 20 : 0;
-      case 21: return tile_fits<Tacc28F64K96>(a, n, ldb, ldc, B, C) ? 21 : 0;
-      case 22: return tile_fits<Tacc28F64K64>(a, n, ldb, ldc, B, C) ? 22 : 0;
-      default: return 0;
+  } else {
+    switch (kind) {
+      case 20: fn(Tacc28F64K160{}); return true;
+      case 21: fn(Tacc28F64K96{}); return true;
+      case 22: fn(Tacc28F64K64{}); return true;
+      default: return false;
     }
   }
-  return 0;
+}
+
+// Which kernel runs: a TMEM configuration whenever the layout allows (chosen
+// by density), the row-tile kernel for everything else.
+std::atomic<int> g_force_kernel{-1};  // test hook: -1 auto, 0 row-tile, else a configuration id
+
+// measured crossovers at n=8000 (profiles/r01_kernel_sweep_28w.jsonl): TMEM accumulators
+// with 28 warps everywhere, the chunk depth shrinking as the density grows (the record
+// stage must hold a chunk's records); 16 warps at the sparse end
+// (profiles/r01_kernel_sweep_kc.jsonl: a deeper chunk with a smaller record stage where
+// the stage still holds a chunk's records — KC 200 / 12 KB at 0.35-1.1 %, 16 warps with
+// KC 216 / 4 KB up to 0.22 %)
+int pick_by_density(double density, bool f64) {
+  if (f64) return density >= 0.07 ? 22 : density >= 0.025 ? 21 : 20;
+  return density >= 0.3      ? 15
+         : density >= 0.12   ? 14
+         : density >= 0.06   ? 13
+         : density >= 0.035  ? 12
+         : density >= 0.017  ? 18
+         : density >= 0.011  ? 11
+         : density >= 0.0035 ? 16
+         : density >= 0.0022 ? 8
+                             : 17;
+}
+
+// `small_gate`: products below 0.4 GFLOP take the planner-free row-tile kernel
+// (the planner, ~35 us, costs more than it saves; profiles/r01_small_n.jsonl).
+// A caller that reuses a plan (gcoo_plan_*) pays the planner once, so plans
+// are chosen without it.
+template <typename T>
+int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const T* B, const T* C, int flavor,
+                bool small_gate = true) {
+  const int force = g_force_kernel.load(std::memory_order_relaxed);
+  if (flavor == GCOO_FLAVOR_MUL_ADD || force == 0 || a.m == 0) return 0;
+  if (force < 0 && small_gate && 2.0 * (double)a.nnz * (double)n < 4e8) return 0;
+  const double density = (double)a.nnz / ((double)a.m * (double)a.k);
+  const int pick = force > 0 ? force : pick_by_density(density, sizeof(T) == 8);
+  int kind = 0;
+  with_cfg<T>(pick, [&](auto c) {
+    using Cfg = decltype(c);
+    if (!tile_fits<Cfg>(a, n, ldb, ldc, B, C)) return;
+    if (force < 0) {
+      // hypersparse A: a TMEM CTA streams every KC x W tile of its column strip
+      // whatever its row block holds, and the planner's per-(row, chunk)
+      // scratch (12 B per slot) grows with m*k/KC rather than nnz — the
+      // row-tile kernel reads only the B rows A touches
+      const double per_segment = (double)Cfg::RB * Cfg::KC * density;  // entries per (row block, chunk)
+      const double scratch = 12.0 * (double)ceil_div(a.m, Cfg::RB) * Cfg::RB * (double)ceil_div(a.k, Cfg::KC);
+      if (per_segment < 8.0 || scratch > 1e9 + 192.0 * (double)a.nnz) return;
+    }
+    kind = pick;
+  });
+  return kind;
 }
 
 // strip_n > 0: the plan will serve B/C of that width (a direct call, or the
@@ -452,48 +441,22 @@ template <typename T>
 void make_plan(SpdmPlan& P, const DevGcoo<T>& a, int kind, cudaStream_t s, int64_t strip_n = 0) {
   P.kind = kind;
   const int64_t wave = strip_n ? sm_count() : 0;
-  if constexpr (std::is_same<T, float>::value) {
-    if (kind == 5) build_plan<TileV4, false>(P, a, s);
-    if (kind == 8) build_plan<TaccV4, true>(P, a, s, wave, ceil_div(strip_n, TaccV4::W));
-    if (kind == 9) build_plan<TaccV2, true>(P, a, s, wave, ceil_div(strip_n, TaccV2::W));
-    if (kind == 10) build_plan<TaccV4W, true>(P, a, s, wave, ceil_div(strip_n, TaccV4W::W));
-    if (kind == 11) build_plan<Tacc28K192, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K192::W));
-    if (kind == 12) build_plan<Tacc28K160, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K160::W));
-    if (kind == 13) build_plan<Tacc28K128, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K128::W));
-    if (kind == 14) build_plan<Tacc28K96, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K96::W));
-    if (kind == 15) build_plan<Tacc28K64, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K64::W));
-    if (kind == 16) build_plan<Tacc28K200, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K200::W));
-    if (kind == 17) build_plan<TaccV4K216, true>(P, a, s, wave, ceil_div(strip_n, TaccV4K216::W));
-    if (kind == 18) build_plan<Tacc28K176, true>(P, a, s, wave, ceil_div(strip_n, Tacc28K176::W));
-  } else {
-    if (kind == 20) build_plan<Tacc28F64K160, true>(P, a, s, wave, ceil_div(strip_n, Tacc28F64K160::W));
-    if (kind == 21) build_plan<Tacc28F64K96, true>(P, a, s, wave, ceil_div(strip_n, Tacc28F64K96::W));
-    if (kind == 22) build_plan<Tacc28F64K64, true>(P, a, s, wave, ceil_div(strip_n, Tacc28F64K64::W));
-  }
+  with_cfg<T>(kind, [&](auto c) {
+    using Cfg = decltype(c);
+    build_plan<Cfg>(P, a, s, wave, ceil_div(strip_n, Cfg::W));
+  });
 }
+
+// The kernel id of this thread's latest multiply (test hook gcoo_debug_last_kernel).
+thread_local int t_last_kind = -1;
 
 template <typename T>
 void run_spdm(const SpdmPlan& P, const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C, int64_t ldc,
               int flavor, cudaStream_t s) {
   if (a.m == 0 || n == 0) return;
-  if constexpr (std::is_same<T, float>::value) {
-    if (P.kind == 5) return run_plan<TileV4, false>(P, a, n, B, ldb, C, ldc, s);
-    if (P.kind == 8) return run_plan<TaccV4, true>(P, a, n, B, ldb, C, ldc, s);
-    if (P.kind == 9) return run_plan<TaccV2, true>(P, a, n, B, ldb, C, ldc, s);
-    if (P.kind == 10) return run_plan<TaccV4W, true>(P, a, n, B, ldb, C, ldc, s);
-    if (P.kind == 11) return run_plan<Tacc28K192, true>(P, a, n, B, ldb, C, ldc, s);
-    if (P.kind == 12) return run_plan<Tacc28K160, true>(P, a, n, B, ldb, C, ldc, s);
-    if (P.kind == 13) return run_plan<Tacc28K128, true>(P, a, n, B, ldb, C, ldc, s);
-    if (P.kind == 14) return run_plan<Tacc28K96, true>(P, a, n, B, ldb, C, ldc, s);
-    if (P.kind == 15) return run_plan<Tacc28K64, true>(P, a, n, B, ldb, C, ldc, s);
-    if (P.kind == 16) return run_plan<Tacc28K200, true>(P, a, n, B, ldb, C, ldc, s);
-    if (P.kind == 17) return run_plan<TaccV4K216, true>(P, a, n, B, ldb, C, ldc, s);
-    if (P.kind == 18) return run_plan<Tacc28K176, true>(P, a, n, B, ldb, C, ldc, s);
-  } else {
-    if (P.kind == 20) return run_plan<Tacc28F64K160, true>(P, a, n, B, ldb, C, ldc, s);
-    if (P.kind == 21) return run_plan<Tacc28F64K96, true>(P, a, n, B, ldb, C, ldc, s);
-    if (P.kind == 22) return run_plan<Tacc28F64K64, true>(P, a, n, B, ldb, C, ldc, s);
-  }
+  t_last_kind = P.kind;
+  if (P.kind != 0 && with_cfg<T>(P.kind, [&](auto c) { run_plan<decltype(c)>(P, a, n, B, ldb, C, ldc, s); }))
+    return;
   if (flavor != GCOO_FLAVOR_MUL_ADD) launch_rowtile_p<T, true>(a, n, B, ldb, C, ldc, s);
   else launch_rowtile_p<T, false>(a, n, B, ldb, C, ldc, s);
 }
@@ -595,7 +558,7 @@ bool tile_order_is_permutation(const int64_t* order, int64_t count) {
 // starts crossing PCIe (the other direction) as soon as A is planned: the
 // link runs both directions at once (profiles/r01_pcie_probe.jsonl: 99 GB/s
 // H2D+D2H vs 55 GB/s one way), so the D2H stream's start is the critical path.
-int g_pipeline_strips = 32;  // tuning hook (gcoo_debug_pipeline_strips)
+std::atomic<int> g_pipeline_strips{32};  // tuning hook (gcoo_debug_pipeline_strips)
 constexpr int NBUF = 3;
 
 // Pageable (not page-locked) host memory crosses PCIe through the driver's
@@ -612,7 +575,8 @@ bool host_pageable(const void* p) {
 }
 
 int64_t pipeline_strip(int64_t m, int64_t k, int64_t n, bool pageable) {
-  const int strips = pageable ? std::min(g_pipeline_strips, 4) : g_pipeline_strips;
+  const int want = g_pipeline_strips.load(std::memory_order_relaxed);
+  const int strips = pageable ? std::min(want, 4) : want;
   if (strips <= 1 || n < 2048 || (m + k) * n < (int64_t)32 << 20) return 0;  // small: one shot
   int64_t w = ceil_div(ceil_div(n, strips), 128) * 128;
   return std::max<int64_t>(w, 256);
@@ -832,10 +796,12 @@ void plan_create(int64_t m, int64_t k, int32_t p, int64_t nnz, const T* values, 
   h->flavor = flavor;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (m > 0) {
-    // the kernel class for 16-byte aligned B/C with n % 4 == 0 (checked again per multiply)
+    // the kernel class for 16-byte aligned B/C with n % 4 == 0 (checked again per
+    // multiply); no small-product gate: the planner runs once here, not per call
     static const double aligned[2] __attribute__((aligned(16))) = {};
     const T* al = reinterpret_cast<const T*>(aligned);
-    make_plan<T>(h->plan, plan_a<T>(h.get()), choose_kind<T>(plan_a<T>(h.get()), 4, 4, 4, al, al, flavor), s);
+    make_plan<T>(h->plan, plan_a<T>(h.get()),
+                 choose_kind<T>(plan_a<T>(h.get()), 4, 4, 4, al, al, flavor, /*small_gate=*/false), s);
   }
   *plan = h.release();
 }
@@ -848,7 +814,7 @@ void plan_spdm(const gcoo_plan* plan, int64_t n, const T* B, int64_t ldb, T* C, 
   const DevGcoo<T>& a = plan_a<T>(plan);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (a.m == 0 || n == 0) return;
-  const int kind = choose_kind<T>(a, n, ldb, ldc, B, C, plan->flavor);
+  const int kind = choose_kind<T>(a, n, ldb, ldc, B, C, plan->flavor, /*small_gate=*/false);
   if (kind == plan->plan.kind) {
     run_spdm<T>(plan->plan, a, n, B, ldb, C, ldc, plan->flavor, s);
   } else {  // this B/C layout needs another kernel class: plan it for this call
@@ -936,25 +902,23 @@ void coo_to_gcoo_host(int64_t m, int64_t k, int32_t p, int64_t nnz, const T* val
   GCOO_CUDA(cudaStreamSynchronize(s));
 }
 
+// CSR -> GCOO on device arrays: CsrMatrix::validate (matrix.hpp:122-165) in its
+// order, then row expansion and the coo_to_gcoo rounds.
 template <typename T>
-void csr_to_gcoo_host(int64_t m, int64_t k, int32_t p, int64_t nnz, const T* vals, const int32_t* cols,
-                      const int64_t* row_ptr, T* ovals, int32_t* orows, int32_t* ocols, int64_t* gidx,
-                      int64_t* gnnz) {
-  // CsrMatrix::validate, host-checkable parts first (matrix.hpp:126-133)
+void csr_to_gcoo_device(int64_t m, int64_t k, int32_t p, int64_t nnz, const T* vals, const int32_t* cols,
+                        const int64_t* row_ptr, T* ovals, int32_t* orows, int32_t* ocols, int64_t* gidx,
+                        int64_t* gnnz, cudaStream_t s) {
   if (m < 1 || k < 1) einval("CsrMatrix: dimensions must be >= 1");
   if (nnz < 0) einval("CsrMatrix: array lengths differ");
-  if (row_ptr[0] != 0 || row_ptr[m] != nnz) einval("CsrMatrix: row_ptr endpoints wrong");
-  cudaStream_t s = thread_stream();
-  DevBuf<int64_t> drp(m + 1, s);
-  DevBuf<T> dv(nnz, s), dov(nnz, s);
-  DevBuf<int32_t> dr(nnz, s), dc(nnz, s), dor(nnz, s), doc(nnz, s);
-  h2d(drp.get(), row_ptr, m + 1, s);
-  h2d(dv.get(), vals, nnz, s);
-  h2d(dc.get(), cols, nnz, s);
   {
+    int64_t ends[2] = {0, 0};
+    d2h(&ends[0], row_ptr, 1, s);
+    d2h(&ends[1], row_ptr + m, 1, s);
+    GCOO_CUDA(cudaStreamSynchronize(s));
+    if (ends[0] != 0 || ends[1] != nnz) einval("CsrMatrix: row_ptr endpoints wrong");
     DevBuf<unsigned long long> bad(1, s);
     GCOO_CUDA(cudaMemsetAsync(bad.get(), 0xff, sizeof(unsigned long long), s));
-    GCOO_LAUNCH(validate_csr_kernel, grid_for(m, 256), 256, 0, s, m, k, nnz, drp.get(), dc.get(), bad.get());
+    GCOO_LAUNCH(validate_csr_kernel, grid_for(m, 256), 256, 0, s, m, k, nnz, row_ptr, cols, bad.get());
     unsigned long long h = 0;
     d2h(&h, bad.get(), 1, s);
     GCOO_CUDA(cudaStreamSynchronize(s));
@@ -965,11 +929,30 @@ void csr_to_gcoo_host(int64_t m, int64_t k, int32_t p, int64_t nnz, const T* val
     }
   }
   if (!is_pow2(p)) einval("csr_to_gcoo: p must be a power of two");
-  const int64_t groups = ceil_div(m, p);
+  DevBuf<int32_t> dr(nnz, s);
+  if (nnz > 0) GCOO_LAUNCH(expand_rows_kernel, grid_for(nnz, 256), 256, 0, s, nnz, m, row_ptr, dr.get());
+  coo_to_gcoo_device<T>(m, k, p, nnz, vals, dr.get(), cols, ovals, orows, ocols, gidx, gnnz, false, s);
+}
+
+template <typename T>
+void csr_to_gcoo_host(int64_t m, int64_t k, int32_t p, int64_t nnz, const T* vals, const int32_t* cols,
+                      const int64_t* row_ptr, T* ovals, int32_t* orows, int32_t* ocols, int64_t* gidx,
+                      int64_t* gnnz) {
+  // CsrMatrix::validate, host-checkable parts first (matrix.hpp:126-133)
+  if (m < 1 || k < 1) einval("CsrMatrix: dimensions must be >= 1");
+  if (nnz < 0) einval("CsrMatrix: array lengths differ");
+  if (row_ptr[0] != 0 || row_ptr[m] != nnz) einval("CsrMatrix: row_ptr endpoints wrong");
+  cudaStream_t s = thread_stream();
+  const int64_t groups = is_pow2(p) ? ceil_div(m, p) : 0;
+  DevBuf<int64_t> drp(m + 1, s);
+  DevBuf<T> dv(nnz, s), dov(nnz, s);
+  DevBuf<int32_t> dc(nnz, s), dor(nnz, s), doc(nnz, s);
   DevBuf<int64_t> dgi(groups, s), dgn(groups, s);
-  if (nnz > 0) GCOO_LAUNCH(expand_rows_kernel, grid_for(nnz, 256), 256, 0, s, nnz, m, drp.get(), dr.get());
-  coo_to_gcoo_device<T>(m, k, p, nnz, dv.get(), dr.get(), dc.get(), dov.get(), dor.get(), doc.get(), dgi.get(),
-                        dgn.get(), false, s);
+  h2d(drp.get(), row_ptr, m + 1, s);
+  h2d(dv.get(), vals, nnz, s);
+  h2d(dc.get(), cols, nnz, s);
+  csr_to_gcoo_device<T>(m, k, p, nnz, dv.get(), dc.get(), drp.get(), dov.get(), dor.get(), doc.get(), dgi.get(),
+                        dgn.get(), s);
   d2h(ovals, dov.get(), nnz, s);
   d2h(orows, dor.get(), nnz, s);
   d2h(ocols, doc.get(), nnz, s);
@@ -1123,13 +1106,17 @@ int gcoo_debug_kernel_time(double* total_ms, int64_t* launches) {
 
 // Tuning hook (not in the public header): column strips of the host pipeline.
 int gcoo_debug_pipeline_strips(int strips) {
-  g_pipeline_strips = strips;
+  g_pipeline_strips.store(strips, std::memory_order_relaxed);
   return GCOO_OK;
 }
 
 // Test/benchmark hook (not in the public header): pin the fp32 kernel choice.
+// Test hook (not in the public header): the kernel id this thread's latest
+// multiply ran (0 row-tile, else a TMEM configuration; -1 none yet).
+int gcoo_debug_last_kernel(void) { return t_last_kind; }
+
 int gcoo_debug_force_kernel(int which) {
-  g_force_kernel = which;
+  g_force_kernel.store(which, std::memory_order_relaxed);
   return GCOO_OK;
 }
 
@@ -1370,6 +1357,45 @@ int gcoo_dense_to_gcoo_f32_dev(int64_t m, int64_t k, int32_t p, const float* A, 
   return guarded([&] {
     *nnz = dense_to_gcoo_device<float>(m, k, p, A, capacity, out_values, out_row_idx, out_col_idx, g_idxes,
                                        nnz_per_group, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int gcoo_dense_to_gcoo_f64_dev(int64_t m, int64_t k, int32_t p, const double* A, int64_t capacity,
+                               double* out_values, int32_t* out_row_idx, int32_t* out_col_idx, int64_t* g_idxes,
+                               int64_t* nnz_per_group, int64_t* nnz, void* stream) {
+  return guarded([&] {
+    *nnz = dense_to_gcoo_device<double>(m, k, p, A, capacity, out_values, out_row_idx, out_col_idx, g_idxes,
+                                        nnz_per_group, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int gcoo_coo_to_gcoo_f64_dev(int64_t m, int64_t k, int32_t p, int64_t nnz, const double* values,
+                             const int32_t* row_idx, const int32_t* col_idx, double* out_values,
+                             int32_t* out_row_idx, int32_t* out_col_idx, int64_t* g_idxes,
+                             int64_t* nnz_per_group, void* stream) {
+  return guarded([&] {
+    coo_to_gcoo_device<double>(m, k, p, nnz, values, row_idx, col_idx, out_values, out_row_idx, out_col_idx,
+                               g_idxes, nnz_per_group, true, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int gcoo_csr_to_gcoo_f32_dev(int64_t m, int64_t k, int32_t p, int64_t nnz, const float* values,
+                             const int32_t* col_idx, const int64_t* row_ptr, float* out_values,
+                             int32_t* out_row_idx, int32_t* out_col_idx, int64_t* g_idxes,
+                             int64_t* nnz_per_group, void* stream) {
+  return guarded([&] {
+    csr_to_gcoo_device<float>(m, k, p, nnz, values, col_idx, row_ptr, out_values, out_row_idx, out_col_idx,
+                              g_idxes, nnz_per_group, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int gcoo_csr_to_gcoo_f64_dev(int64_t m, int64_t k, int32_t p, int64_t nnz, const double* values,
+                             const int32_t* col_idx, const int64_t* row_ptr, double* out_values,
+                             int32_t* out_row_idx, int32_t* out_col_idx, int64_t* g_idxes,
+                             int64_t* nnz_per_group, void* stream) {
+  return guarded([&] {
+    csr_to_gcoo_device<double>(m, k, p, nnz, values, col_idx, row_ptr, out_values, out_row_idx, out_col_idx,
+                               g_idxes, nnz_per_group, static_cast<cudaStream_t>(stream));
   });
 }
 

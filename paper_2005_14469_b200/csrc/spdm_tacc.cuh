@@ -85,8 +85,6 @@ struct TaccCfg {
 
 //                      V  KC   S  CAP
 using TaccV4 = TaccCfg<4, 192, 2, 16384>;   // W=128, RB=512, 16 warps: density 0.22 % .. 0.35 %
-using TaccV2 = TaccCfg<2, 256, 2, 16384>;   // W=64,  RB=1024 (tests / measurements only)
-using TaccV4W = TaccCfg<4, 192, 2, 16384, 24>;  // W=128, RB=480, 24 warps (previous default; tests / measurements)
 // 28 consumer warps (RB=504): the chunk depth KC trades run length (swaps per
 // entry) against the record-stage capacity, which must hold a row block's
 // records for one chunk (an oversize segment is read from global memory):
@@ -495,12 +493,14 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
         const int64_t hi_next = so[c + 2 <= nchunks ? c + 2 : nchunks];  // prefetch
         const uint32_t len = (uint32_t)(hi - lo);
         const uint32_t bytes = len <= Cfg::CAP ? len : 0u;  // oversize: consumers read global memory
+        // a segment of empty warp headers only: no consumer reads this chunk's B tile
+        const bool any = len > (uint32_t)(Cfg::TABLE + Cfg::NW * Cfg::HDR);
         if (c >= S) mbar_wait(&empty[s], (uint32_t)((c / S) - 1) & 1u);
         unsigned char* stage = smem_raw + (size_t)s * Cfg::STAGE_BYTES;
         stage_lo[s] = lo;
         stage_len[s] = len;
-        mbar_arrive_expect_tx(&full[s], Cfg::BTILE + bytes);
-        tma_load_2d(stage, &tmap_b, x, c * Cfg::KC, &full[s]);
+        mbar_arrive_expect_tx(&full[s], (any ? Cfg::BTILE : 0u) + bytes);
+        if (any) tma_load_2d(stage, &tmap_b, x, c * Cfg::KC, &full[s]);
         if (bytes) bulk_g2s(smem_u32(stage + Cfg::BTILE), ent + lo, bytes, &full[s]);
         lo = hi;
         hi = hi_next;
