@@ -1,6 +1,6 @@
 """World-size-2 `gloo` test of the column-sharded multi-rank path (CPU only).
 
-Each rank multiplies its column block of B with the CPU checker (the GPU
+Each rank multiplies its column block of B with the CPU checker (the product
 kernel is covered by tests/test_gpu_parity.py::test_strided_column_shards_
 bitwise_equal); the blocks are gathered and must equal the single-shot C bit
 for bit, and the max-over-ranks timing reduction must pick the slowest rank —
