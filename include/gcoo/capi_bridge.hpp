@@ -68,4 +68,27 @@ inline int dense_to_gcoo(std::int64_t m, std::int64_t k, std::int32_t p, const d
   return gcoo_dense_to_gcoo_f64(m, k, p, A, cap, ov, orr, oc, gi, gn, nnz);
 }
 
+inline int spdm_csr(std::int64_t m, std::int64_t k, std::int64_t n, std::int64_t nnz, const float* v,
+                    const std::int32_t* c, const std::int64_t* rp, const float* B, float* C) {
+  return gcoo_spdm_csr_f32(m, k, n, nnz, v, c, rp, B, C);
+}
+inline int spdm_csr(std::int64_t m, std::int64_t k, std::int64_t n, std::int64_t nnz, const double* v,
+                    const std::int32_t* c, const std::int64_t* rp, const double* B, double* C) {
+  return gcoo_spdm_csr_f64(m, k, n, nnz, v, c, rp, B, C);
+}
+inline int spdm_coo(std::int64_t m, std::int64_t k, std::int64_t n, std::int64_t nnz, const float* v,
+                    const std::int32_t* r, const std::int32_t* c, const float* B, float* C) {
+  return gcoo_spdm_coo_f32(m, k, n, nnz, v, r, c, B, C);
+}
+inline int spdm_coo(std::int64_t m, std::int64_t k, std::int64_t n, std::int64_t nnz, const double* v,
+                    const std::int32_t* r, const std::int32_t* c, const double* B, double* C) {
+  return gcoo_spdm_coo_f64(m, k, n, nnz, v, r, c, B, C);
+}
+inline int gemm_dense(std::int64_t m, std::int64_t k, std::int64_t n, const float* A, const float* B, float* C) {
+  return gcoo_gemm_dense_f32(m, k, n, A, B, C);
+}
+inline int gemm_dense(std::int64_t m, std::int64_t k, std::int64_t n, const double* A, const double* B, double* C) {
+  return gcoo_gemm_dense_f64(m, k, n, A, B, C);
+}
+
 }  // namespace gcoo::capi

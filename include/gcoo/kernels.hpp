@@ -6,10 +6,10 @@
 // B200 through gcoo_spdm_{f32,f64} (libgcoo_cuda.so).  C is bitwise
 // independent of p, b, tile order and worker count (as in the reference) and
 // equals the reference's column-ascending accumulation chain with FMA
-// contraction.  spdm_csr / spdm_coo (:163-232) — C is the same per-row
-// column-ascending chain — run through the same GPU path after a device
-// CSR/COO -> GCOO conversion.  gemm_oracle (the test oracle) and
-// gemm_dense_blocked (the dense crossover baseline) stay host loops.
+// contraction.  spdm_csr / spdm_coo (:163-232) and gemm_dense_blocked
+// (:107-155) run as their own row-split / ungrouped-COO / tiled-GEMM kernels
+// on the B200 with the reference's accumulation orders; gemm_oracle (the test
+// oracle, double accumulation) stays a host loop.
 #pragma once
 
 #include <algorithm>
@@ -92,22 +92,15 @@ DenseMatrix<T> gemm_oracle(const DenseMatrix<T>& a, const DenseMatrix<T>& b) {
   return c;
 }
 
-// Dense blocked GEMM baseline (:107-155): per C element the sum runs over l
-// ascending regardless of the tile geometry, so the result does not depend on
-// cfg (host loop; out of the GPU path's scope).
+// Dense blocked GEMM baseline (:107-155) on the B200 (gcoo_gemm_dense_*):
+// per C element the sum runs over l ascending whatever the tile geometry, as
+// in the reference, so the result does not depend on cfg.
 template <typename T>
 DenseMatrix<T> gemm_dense_blocked(const DenseMatrix<T>& a, const DenseMatrix<T>& b, const ExecConfig& cfg) {
   cfg.validate();
   if (a.cols != b.rows) throw std::invalid_argument("gemm_dense_blocked: inner dimensions differ");
   DenseMatrix<T> c(a.rows, b.cols);
-  for (std::int64_t i = 0; i < a.rows; ++i) {
-    T* crow = c.row_ptr(i);
-    for (std::int64_t l = 0; l < a.cols; ++l) {
-      const T av = a(i, l);
-      const T* brow = b.row_ptr(l);
-      for (std::int64_t j = 0; j < b.cols; ++j) crow[j] += av * brow[j];
-    }
-  }
+  capi::check(capi::gemm_dense(a.rows, a.cols, b.cols, a.data.data(), b.data.data(), c.data.data()));
   return c;
 }
 
@@ -166,22 +159,33 @@ DenseMatrix<T> spdm_gcoo_auto(const DenseMatrix<T>& a, const DenseMatrix<T>& b, 
 }
 
 // ---------------------------------------------- CSR / COO baselines (GPU) --
-/// Row-split CSR SpDM (:163-184).  Per C element: the row's nonzeros in
-/// ascending column order — the GCOO kernel's chain — so the CSR is grouped on
-/// the device and multiplied by the same kernel.
+/// Row-split CSR SpDM (:163-184) on the B200 (gcoo_spdm_csr_*): each row's
+/// nonzeros in CSR order, no staging or reuse.  Like the reference it does
+/// not validate the CSR (out-of-range indices are rejected, not read).
 template <typename T>
 DenseMatrix<T> spdm_csr(const CsrMatrix<T>& a, const DenseMatrix<T>& b, const ExecConfig& cfg) {
   cfg.validate();
   if (a.cols_dim != b.rows) throw std::invalid_argument("spdm_csr: inner dimensions differ");
-  return spdm_gcoo(csr_to_gcoo(a, cfg.p), b, cfg);
+  DenseMatrix<T> c(a.rows_dim, b.cols);
+  if (a.row_ptr.size() != static_cast<std::size_t>(a.rows_dim) + 1 || a.col_idx.size() != a.values.size())
+    throw std::invalid_argument("spdm_csr: inconsistent CSR arrays");
+  capi::check(capi::spdm_csr(a.rows_dim, a.cols_dim, b.cols, a.nnz(), a.values.data(), a.col_idx.data(),
+                             a.row_ptr.data(), b.data.data(), c.data.data()));
+  return c;
 }
 
-/// Ungrouped COO SpDM ablation (:193-232); same per-element chain.
+/// Ungrouped COO SpDM ablation (:193-232) on the B200 (gcoo_spdm_coo_*): any
+/// entry order, as the reference (each row's chain in array order).
 template <typename T>
 DenseMatrix<T> spdm_coo(const CooMatrix<T>& a, const DenseMatrix<T>& b, const ExecConfig& cfg) {
   cfg.validate();
   if (a.cols_dim != b.rows) throw std::invalid_argument("spdm_coo: inner dimensions differ");
-  return spdm_gcoo(coo_to_gcoo(a, cfg.p), b, cfg);
+  DenseMatrix<T> c(a.rows_dim, b.cols);
+  if (a.row_idx.size() != a.values.size() || a.col_idx.size() != a.values.size())
+    throw std::invalid_argument("spdm_coo: inconsistent COO arrays");
+  capi::check(capi::spdm_coo(a.rows_dim, a.cols_dim, b.cols, a.nnz(), a.values.data(), a.row_idx.data(),
+                             a.col_idx.data(), b.data.data(), c.data.data()));
+  return c;
 }
 
 }  // namespace gcoo

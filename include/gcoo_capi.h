@@ -251,6 +251,47 @@ int gcoo_dense_to_gcoo_f64_dev(int64_t m, int64_t k, int32_t p, const double* A,
                                int64_t* g_idxes, int64_t* nnz_per_group, int64_t* nnz,
                                void* stream);
 
+/* ------------------------------------------- baselines */
+/*
+ * The reference's comparison kernels on the GPU, each with the reference's
+ * per-element accumulation order (bit-identical to it built with FMA
+ * contraction; `flavor` as for spdm):
+ *  - spdm_csr (kernels.hpp:163-184): row-split over a CSR (int64 row_ptr[m+1],
+ *    int32 columns, any order inside a row), C(r,:) = chain in CSR order;
+ *  - spdm_coo (kernels.hpp:193-232): any COO entry order (duplicates too),
+ *    C(r,:) = chain over row r's entries in array order;
+ *  - gemm_dense (kernels.hpp:107-155, gemm_dense_blocked): C = A*B with every
+ *    element summed over l ascending.
+ * The reference does not validate these inputs (an out-of-range index is
+ * undefined behaviour there); here it is GCOO_EINVAL.  C is fully written.
+ */
+int gcoo_spdm_csr_f32(int64_t m, int64_t k, int64_t n, int64_t nnz, const float* values, const int32_t* col_idx,
+                      const int64_t* row_ptr, const float* B, float* C);
+int gcoo_spdm_csr_f64(int64_t m, int64_t k, int64_t n, int64_t nnz, const double* values, const int32_t* col_idx,
+                      const int64_t* row_ptr, const double* B, double* C);
+int gcoo_spdm_csr_f32_dev(int64_t m, int64_t k, int64_t n, int64_t nnz, const float* values, const int32_t* col_idx,
+                          const int64_t* row_ptr, const float* B, int64_t ldb, float* C, int64_t ldc, int flavor,
+                          void* stream);
+int gcoo_spdm_csr_f64_dev(int64_t m, int64_t k, int64_t n, int64_t nnz, const double* values,
+                          const int32_t* col_idx, const int64_t* row_ptr, const double* B, int64_t ldb, double* C,
+                          int64_t ldc, int flavor, void* stream);
+int gcoo_spdm_coo_f32(int64_t m, int64_t k, int64_t n, int64_t nnz, const float* values, const int32_t* row_idx,
+                      const int32_t* col_idx, const float* B, float* C);
+int gcoo_spdm_coo_f64(int64_t m, int64_t k, int64_t n, int64_t nnz, const double* values, const int32_t* row_idx,
+                      const int32_t* col_idx, const double* B, double* C);
+int gcoo_spdm_coo_f32_dev(int64_t m, int64_t k, int64_t n, int64_t nnz, const float* values, const int32_t* row_idx,
+                          const int32_t* col_idx, const float* B, int64_t ldb, float* C, int64_t ldc, int flavor,
+                          void* stream);
+int gcoo_spdm_coo_f64_dev(int64_t m, int64_t k, int64_t n, int64_t nnz, const double* values,
+                          const int32_t* row_idx, const int32_t* col_idx, const double* B, int64_t ldb, double* C,
+                          int64_t ldc, int flavor, void* stream);
+int gcoo_gemm_dense_f32(int64_t m, int64_t k, int64_t n, const float* A, const float* B, float* C);
+int gcoo_gemm_dense_f64(int64_t m, int64_t k, int64_t n, const double* A, const double* B, double* C);
+int gcoo_gemm_dense_f32_dev(int64_t m, int64_t k, int64_t n, const float* A, int64_t lda, const float* B,
+                            int64_t ldb, float* C, int64_t ldc, int flavor, void* stream);
+int gcoo_gemm_dense_f64_dev(int64_t m, int64_t k, int64_t n, const double* A, int64_t lda, const double* B,
+                            int64_t ldb, double* C, int64_t ldc, int flavor, void* stream);
+
 /* ------------------------------------------------ synthetic inputs ------ */
 /*
  * generate_uniform_sparse<T>(n, s, seed) (io.hpp:129-145, io.cpp:224-258):

@@ -101,6 +101,13 @@ class Oracle:
         L.orc_spdm_gcoo_rows_f32.argtypes = [_i64, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, C.c_int]
         L.orc_fnv1a32.restype = C.c_uint32
         L.orc_fnv1a32.argtypes = [_vp, _i64]
+        for t in ("f32", "f64"):
+            for name, args in (("orc_spdm_csr_", [_i64, _i64, _vp, _vp, _vp, _vp, _vp, C.c_int]),
+                               ("orc_spdm_coo_", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, C.c_int]),
+                               ("orc_gemm_dense_", [_i64, _i64, _i64, _vp, _vp, _vp, C.c_int])):
+                f = getattr(L, name + t)
+                f.restype = None
+                f.argtypes = args
 
     # -- inputs -------------------------------------------------------------
     def derive_seed(self, base: int, a: int, b: int = 0) -> int:
@@ -180,6 +187,36 @@ class Oracle:
         st = (_u64 * 4)()
         self.lib.orc_gcoo_stats(n, b, g.groups, _p(g.col_idx), _p(g.g_idxes), _p(g.nnz_per_group), st)
         return tuple(int(x) for x in st)
+
+    # -- the reference's comparison kernels (kernels.hpp:107-232) ----------
+    def spdm_csr(self, m: int, vals, cols, row_ptr, B: np.ndarray, fma: bool = True) -> np.ndarray:
+        """Row-split CSR: each row's chain in CSR order (kernels.hpp:163-184)."""
+        B = np.ascontiguousarray(B)
+        vals = np.ascontiguousarray(vals, dtype=B.dtype)
+        Cm = np.empty((m, B.shape[1]), dtype=B.dtype)
+        f = self.lib.orc_spdm_csr_f32 if B.dtype == np.float32 else self.lib.orc_spdm_csr_f64
+        f(m, B.shape[1], _p(vals), _p(np.ascontiguousarray(cols, dtype=np.int32)),
+          _p(np.ascontiguousarray(row_ptr, dtype=np.int64)), _p(B), _p(Cm), int(fma))
+        return Cm
+
+    def spdm_coo(self, m: int, vals, rows, cols, B: np.ndarray, fma: bool = True) -> np.ndarray:
+        """Ungrouped COO: each row's chain in entry order (kernels.hpp:193-232)."""
+        B = np.ascontiguousarray(B)
+        vals = np.ascontiguousarray(vals, dtype=B.dtype)
+        Cm = np.empty((m, B.shape[1]), dtype=B.dtype)
+        f = self.lib.orc_spdm_coo_f32 if B.dtype == np.float32 else self.lib.orc_spdm_coo_f64
+        f(m, B.shape[1], vals.size, _p(vals), _p(np.ascontiguousarray(rows, dtype=np.int32)),
+          _p(np.ascontiguousarray(cols, dtype=np.int32)), _p(B), _p(Cm), int(fma))
+        return Cm
+
+    def gemm_dense(self, A: np.ndarray, B: np.ndarray, fma: bool = True) -> np.ndarray:
+        """gemm_dense_blocked: l-ascending chain per element (kernels.hpp:107-155)."""
+        A = np.ascontiguousarray(A)
+        B = np.ascontiguousarray(B, dtype=A.dtype)
+        Cm = np.empty((A.shape[0], B.shape[1]), dtype=A.dtype)
+        f = self.lib.orc_gemm_dense_f32 if A.dtype == np.float32 else self.lib.orc_gemm_dense_f64
+        f(A.shape[0], A.shape[1], B.shape[1], _p(A), _p(B), _p(Cm), int(fma))
+        return Cm
 
     def fnv(self, a: np.ndarray) -> str:
         a = np.ascontiguousarray(a)
@@ -322,6 +359,40 @@ class Reference:
                       _p(g.g_idxes), _p(g.nnz_per_group), _p(np.ascontiguousarray(B)), _p(Cm), st, workers,
                       _p(to), 0 if to is None else to.size))
         return Cm, tuple(int(x) for x in st)
+
+    def spdm_csr(self, m, k, vals, cols, row_ptr, B, p=4, b=64, workers=0):
+        B = np.ascontiguousarray(B)
+        Cm = np.empty((m, B.shape[1]), dtype=B.dtype)
+        f = self.lib.ref_spdm_csr_f32 if B.dtype == np.float32 else self.lib.ref_spdm_csr_f64
+        f.restype = C.c_int
+        f.argtypes = [_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _i32, C.c_int]
+        vals = np.ascontiguousarray(vals, dtype=B.dtype)
+        self._check(f(_n(m), _n(k), _n(B.shape[1]), _n(vals.size), _p(vals),
+                      _p(np.ascontiguousarray(cols, dtype=np.int32)), _p(np.ascontiguousarray(row_ptr, dtype=np.int64)),
+                      _p(B), _p(Cm), p, b, workers))
+        return Cm
+
+    def spdm_coo(self, m, k, vals, rows, cols, B, p=4, b=64, workers=0):
+        B = np.ascontiguousarray(B)
+        Cm = np.empty((m, B.shape[1]), dtype=B.dtype)
+        f = self.lib.ref_spdm_coo_f32 if B.dtype == np.float32 else self.lib.ref_spdm_coo_f64
+        f.restype = C.c_int
+        f.argtypes = [_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _i32, C.c_int]
+        vals = np.ascontiguousarray(vals, dtype=B.dtype)
+        self._check(f(_n(m), _n(k), _n(B.shape[1]), _n(vals.size), _p(vals),
+                      _p(np.ascontiguousarray(rows, dtype=np.int32)), _p(np.ascontiguousarray(cols, dtype=np.int32)),
+                      _p(B), _p(Cm), p, b, workers))
+        return Cm
+
+    def gemm_dense(self, A, B, p=4, b=64, workers=0):
+        A = np.ascontiguousarray(A)
+        B = np.ascontiguousarray(B, dtype=A.dtype)
+        Cm = np.empty((A.shape[0], B.shape[1]), dtype=A.dtype)
+        f = self.lib.ref_gemm_dense_f32 if A.dtype == np.float32 else self.lib.ref_gemm_dense_f64
+        f.restype = C.c_int
+        f.argtypes = [_i64, _i64, _i64, _vp, _vp, _vp, _i32, _i32, C.c_int]
+        self._check(f(_n(A.shape[0]), _n(A.shape[1]), _n(B.shape[1]), _p(A), _p(B), _p(Cm), p, b, workers))
+        return Cm
 
     def gemm_oracle(self, A: np.ndarray, B: np.ndarray) -> np.ndarray:
         m, k = A.shape

@@ -478,6 +478,56 @@ void orc_gcoo_stats(int64_t n, int32_t b, int64_t groups, const int32_t* cols,
   st->b_loads_reused = (nnz - runs) * (uint64_t)n;
 }
 
+/* ------------------------------------------------- comparison kernels --
+ * The reference's baselines (kernels.hpp:107-232) restated: every C element is
+ * the chain over its terms in the reference's order, one rounding per step
+ * (fma) or two (mul+add), starting from +0.
+ *   spdm_csr   (:163-184): row r's entries in CSR order;
+ *   spdm_coo   (:193-232): row r's entries in COO array order (the reference
+ *              walks column strips, then b-entry chunks of the stream, then the
+ *              chunk's entries: per element that is array order);
+ *   gemm_dense (:107-155): l ascending (its kb depth blocks run in order). */
+#define ORC_MAC(T, FMA, acc, a, b) ((FMA) ? ORC_FMA_##T((a), (b), (acc)) : (acc) + (T)((a) * (b)))
+#define ORC_FMA_float(a, b, c) fmaf((a), (b), (c))
+#define ORC_FMA_double(a, b, c) fma((a), (b), (c))
+
+#define ORC_BASELINES(T, SFX)                                                                                 \
+  void orc_spdm_csr_##SFX(int64_t m, int64_t n, const T* vals, const int32_t* cols, const int64_t* rp,      \
+                          const T* B, T* C, int fma_flavour) {                                             \
+    for (int64_t r = 0; r < m; ++r) {                                                                     \
+      T* crow = C + r * n;                                                                                \
+      for (int64_t j = 0; j < n; ++j) crow[j] = (T)0;                                                     \
+      for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {                                                       \
+        const T a = vals[e];                                                                              \
+        const T* brow = B + (int64_t)cols[e] * n;                                                         \
+        for (int64_t j = 0; j < n; ++j) crow[j] = ORC_MAC(T, fma_flavour, crow[j], a, brow[j]);           \
+      }                                                                                                   \
+    }                                                                                                     \
+  }                                                                                                       \
+  void orc_spdm_coo_##SFX(int64_t m, int64_t n, int64_t nnz, const T* vals, const int32_t* rows,           \
+                          const int32_t* cols, const T* B, T* C, int fma_flavour) {                        \
+    for (int64_t i = 0; i < m * n; ++i) C[i] = (T)0;                                                      \
+    for (int64_t e = 0; e < nnz; ++e) {                                                                   \
+      const T a = vals[e];                                                                                \
+      const T* brow = B + (int64_t)cols[e] * n;                                                           \
+      T* crow = C + (int64_t)rows[e] * n;                                                                 \
+      for (int64_t j = 0; j < n; ++j) crow[j] = ORC_MAC(T, fma_flavour, crow[j], a, brow[j]);             \
+    }                                                                                                     \
+  }                                                                                                       \
+  void orc_gemm_dense_##SFX(int64_t m, int64_t k, int64_t n, const T* A, const T* B, T* C, int fma_flavour) { \
+    for (int64_t i = 0; i < m; ++i) {                                                                     \
+      T* crow = C + i * n;                                                                                \
+      for (int64_t j = 0; j < n; ++j) crow[j] = (T)0;                                                     \
+      for (int64_t l = 0; l < k; ++l) {                                                                   \
+        const T a = A[i * k + l];                                                                         \
+        const T* brow = B + l * n;                                                                        \
+        for (int64_t j = 0; j < n; ++j) crow[j] = ORC_MAC(T, fma_flavour, crow[j], a, brow[j]);           \
+      }                                                                                                   \
+    }                                                                                                     \
+  }
+ORC_BASELINES(float, f32)
+ORC_BASELINES(double, f64)
+
 uint32_t orc_fnv1a32(const void* data, int64_t nbytes) {
   const uint8_t* q = (const uint8_t*)data;
   uint32_t h = 2166136261u;

@@ -172,6 +172,85 @@ int ref_spdm_gcoo_f64(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, int
                       workers, tile_order, tile_count);
 }
 
+// The reference's comparison kernels (kernels.hpp:107-232), unvalidated as
+// there: spdm_csr over a CSR, spdm_coo over a COO in any entry order,
+// gemm_dense_blocked.  cfg = {p, b, workers}.
+}  // extern "C"
+namespace {
+template <typename T>
+int ref_csr(int64_t m, int64_t k, int64_t n, int64_t nnz, const T* vals, const int32_t* cols, const int64_t* rp,
+            const T* B, T* C, int32_t p, int32_t b, int workers) {
+  return guarded([&] {
+    CsrMatrix<T> a;
+    a.rows_dim = m;
+    a.cols_dim = k;
+    a.values.assign(vals, vals + nnz);
+    a.col_idx.assign(cols, cols + nnz);
+    a.row_ptr.assign(rp, rp + m + 1);
+    ExecConfig cfg;
+    cfg.p = p;
+    cfg.b = b;
+    cfg.workers = workers;
+    const auto c = spdm_csr(a, make_dense<T>(k, n, B), cfg);
+    std::memcpy(C, c.data.data(), sizeof(T) * c.data.size());
+  });
+}
+template <typename T>
+int ref_coo(int64_t m, int64_t k, int64_t n, int64_t nnz, const T* vals, const int32_t* rows, const int32_t* cols,
+            const T* B, T* C, int32_t p, int32_t b, int workers) {
+  return guarded([&] {
+    CooMatrix<T> a;
+    a.rows_dim = m;
+    a.cols_dim = k;
+    a.values.assign(vals, vals + nnz);
+    a.row_idx.assign(rows, rows + nnz);
+    a.col_idx.assign(cols, cols + nnz);
+    ExecConfig cfg;
+    cfg.p = p;
+    cfg.b = b;
+    cfg.workers = workers;
+    const auto c = spdm_coo(a, make_dense<T>(k, n, B), cfg);
+    std::memcpy(C, c.data.data(), sizeof(T) * c.data.size());
+  });
+}
+template <typename T>
+int ref_dense(int64_t m, int64_t k, int64_t n, const T* A, const T* B, T* C, int32_t p, int32_t b, int workers) {
+  return guarded([&] {
+    ExecConfig cfg;
+    cfg.p = p;
+    cfg.b = b;
+    cfg.workers = workers;
+    const auto c = gemm_dense_blocked(make_dense<T>(m, k, A), make_dense<T>(k, n, B), cfg);
+    std::memcpy(C, c.data.data(), sizeof(T) * c.data.size());
+  });
+}
+}  // namespace
+extern "C" {
+int ref_spdm_csr_f32(int64_t m, int64_t k, int64_t n, int64_t nnz, const float* v, const int32_t* c,
+                     const int64_t* rp, const float* B, float* C, int32_t p, int32_t b, int w) {
+  return ref_csr<float>(m, k, n, nnz, v, c, rp, B, C, p, b, w);
+}
+int ref_spdm_csr_f64(int64_t m, int64_t k, int64_t n, int64_t nnz, const double* v, const int32_t* c,
+                     const int64_t* rp, const double* B, double* C, int32_t p, int32_t b, int w) {
+  return ref_csr<double>(m, k, n, nnz, v, c, rp, B, C, p, b, w);
+}
+int ref_spdm_coo_f32(int64_t m, int64_t k, int64_t n, int64_t nnz, const float* v, const int32_t* r,
+                     const int32_t* c, const float* B, float* C, int32_t p, int32_t b, int w) {
+  return ref_coo<float>(m, k, n, nnz, v, r, c, B, C, p, b, w);
+}
+int ref_spdm_coo_f64(int64_t m, int64_t k, int64_t n, int64_t nnz, const double* v, const int32_t* r,
+                     const int32_t* c, const double* B, double* C, int32_t p, int32_t b, int w) {
+  return ref_coo<double>(m, k, n, nnz, v, r, c, B, C, p, b, w);
+}
+int ref_gemm_dense_f32(int64_t m, int64_t k, int64_t n, const float* A, const float* B, float* C, int32_t p,
+                       int32_t b, int w) {
+  return ref_dense<float>(m, k, n, A, B, C, p, b, w);
+}
+int ref_gemm_dense_f64(int64_t m, int64_t k, int64_t n, const double* A, const double* B, double* C, int32_t p,
+                       int32_t b, int w) {
+  return ref_dense<double>(m, k, n, A, B, C, p, b, w);
+}
+
 // gemm_oracle (kernels.hpp:80-98): double accumulation, used by the
 // reference's own ≤1e-5 / ≤1e-12 gates.
 int ref_gemm_oracle_f32(int64_t m, int64_t k, int64_t n, const float* A, const float* B,

@@ -99,6 +99,13 @@ def lib():
     _sig(L, "gcoo_dense_to_gcoo_f64", _int, dense_args)
     _sig(L, "gcoo_dense_to_gcoo_f32_dev", _int, dense_args + [_vp])
     _sig(L, "gcoo_dense_to_gcoo_f64_dev", _int, dense_args + [_vp])
+    for t in ("f32", "f64"):
+        _sig(L, f"gcoo_spdm_csr_{t}", _int, [_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp])
+        _sig(L, f"gcoo_spdm_csr_{t}_dev", _int, [_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _int, _vp])
+        _sig(L, f"gcoo_spdm_coo_{t}", _int, [_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp])
+        _sig(L, f"gcoo_spdm_coo_{t}_dev", _int, [_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _int, _vp])
+        _sig(L, f"gcoo_gemm_dense_{t}", _int, [_i64, _i64, _i64, _vp, _vp, _vp])
+        _sig(L, f"gcoo_gemm_dense_{t}_dev", _int, [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _vp])
     _sig(L, "gcoo_generate_uniform_sparse_f32", _int, [_i64, _dbl, _u64, _vp])
     _sig(L, "gcoo_generate_uniform_sparse_coo_f32", _int, [_i64, _dbl, _u64, _i64, _vp, _vp, _vp, C.POINTER(_i64)])
     _sig(L, "gcoo_generate_powerlaw_coo_f32", _int, [_i64, _dbl, _dbl, _u64, _i64, _vp, _vp, _vp, C.POINTER(_i64)])
@@ -413,6 +420,113 @@ def spdm_gcoo_auto(a: np.ndarray, b: np.ndarray, cfg: Optional[ExecConfig] = Non
     if timing is not None:
         timing.eo_seconds, timing.kc_seconds = t1 - t0, t2 - t1
     return c
+
+
+# ------------------------------------------- baselines ---
+def _sfx(dtype) -> str:
+    if dtype == np.float32:
+        return "f32"
+    if dtype == np.float64:
+        return "f64"
+    raise TypeError("float32 or float64 required")
+
+
+def spdm_csr(rows_dim: int, cols_dim: int, values: np.ndarray, col_idx: np.ndarray, row_ptr: np.ndarray,
+             b: np.ndarray, cfg: Optional[ExecConfig] = None) -> np.ndarray:
+    """spdm_csr (kernels.hpp:163-184) on the GPU: row-split, each row's chain in
+    CSR order (no grouping or staging — the paper's CSR baseline)."""
+    (cfg or ExecConfig()).validate()
+    b = np.ascontiguousarray(b)
+    if b.ndim != 2 or b.shape[0] != cols_dim:
+        raise ValueError("spdm_csr: inner dimensions differ")
+    values = np.ascontiguousarray(values, dtype=b.dtype)
+    col_idx = np.ascontiguousarray(col_idx, dtype=np.int32)
+    row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    if row_ptr.size != rows_dim + 1 or col_idx.size != values.size:
+        raise ValueError("spdm_csr: inconsistent CSR arrays")
+    c = np.empty((rows_dim, b.shape[1]), b.dtype)
+    _check(getattr(lib(), f"gcoo_spdm_csr_{_sfx(b.dtype)}")(rows_dim, cols_dim, b.shape[1], values.size, _p(values),
+                                                            _p(col_idx), _p(row_ptr), _p(b), _p(c)))
+    return c
+
+
+def spdm_coo(rows_dim: int, cols_dim: int, values: np.ndarray, row_idx: np.ndarray, col_idx: np.ndarray,
+             b: np.ndarray, cfg: Optional[ExecConfig] = None) -> np.ndarray:
+    """spdm_coo (kernels.hpp:193-232) on the GPU: any entry order (each row's
+    chain in array order), the ungrouped ablation of GCOO."""
+    (cfg or ExecConfig()).validate()
+    b = np.ascontiguousarray(b)
+    if b.ndim != 2 or b.shape[0] != cols_dim:
+        raise ValueError("spdm_coo: inner dimensions differ")
+    values = np.ascontiguousarray(values, dtype=b.dtype)
+    row_idx = np.ascontiguousarray(row_idx, dtype=np.int32)
+    col_idx = np.ascontiguousarray(col_idx, dtype=np.int32)
+    if not (values.size == row_idx.size == col_idx.size):
+        raise ValueError("spdm_coo: inconsistent COO arrays")
+    c = np.empty((rows_dim, b.shape[1]), b.dtype)
+    _check(getattr(lib(), f"gcoo_spdm_coo_{_sfx(b.dtype)}")(rows_dim, cols_dim, b.shape[1], values.size, _p(values),
+                                                            _p(row_idx), _p(col_idx), _p(b), _p(c)))
+    return c
+
+
+def gemm_dense_blocked(a: np.ndarray, b: np.ndarray, cfg: Optional[ExecConfig] = None) -> np.ndarray:
+    """gemm_dense_blocked (kernels.hpp:107-155) on the GPU: every element summed
+    over l ascending (the dense crossover baseline)."""
+    (cfg or ExecConfig()).validate()
+    a = _dense_check(a)
+    b = np.ascontiguousarray(b, dtype=a.dtype)
+    if b.ndim != 2 or a.shape[1] != b.shape[0]:
+        raise ValueError("gemm_dense_blocked: inner dimensions differ")
+    c = np.empty((a.shape[0], b.shape[1]), a.dtype)
+    _check(getattr(lib(), f"gcoo_gemm_dense_{_sfx(a.dtype)}")(a.shape[0], a.shape[1], b.shape[1], _p(a), _p(b),
+                                                              _p(c)))
+    return c
+
+
+def spdm_csr_dev(rows_dim: int, cols_dim: int, values, col_idx, row_ptr, b, c, flavor: int = FLAVOR_FMA,
+                 stream=None) -> None:
+    """Stream-ordered spdm_csr on device tensors (b: k x n, c: m x n, unit column stride)."""
+    import torch
+    values = _dev_array("values", values, (torch.float32, torch.float64))
+    col_idx = _dev_array("col_idx", col_idx, (torch.int32,))
+    row_ptr = _dev_array("row_ptr", row_ptr, (torch.int64,))
+    _check_dense_pair(values.dtype, b, c, rows_dim, cols_dim)
+    f = getattr(lib(), f"gcoo_spdm_csr_{'f64' if values.dtype == torch.float64 else 'f32'}_dev")
+    _check(f(rows_dim, cols_dim, b.shape[1], values.numel(), _p(values), _p(col_idx), _p(row_ptr), _p(b), b.stride(0),
+             _p(c), c.stride(0), flavor, _stream_ptr(stream)))
+
+
+def spdm_coo_dev(rows_dim: int, cols_dim: int, values, row_idx, col_idx, b, c, flavor: int = FLAVOR_FMA,
+                 stream=None) -> None:
+    """Stream-ordered spdm_coo on device tensors (any entry order)."""
+    import torch
+    values = _dev_array("values", values, (torch.float32, torch.float64))
+    row_idx = _dev_array("row_idx", row_idx, (torch.int32,))
+    col_idx = _dev_array("col_idx", col_idx, (torch.int32,))
+    _check_dense_pair(values.dtype, b, c, rows_dim, cols_dim)
+    f = getattr(lib(), f"gcoo_spdm_coo_{'f64' if values.dtype == torch.float64 else 'f32'}_dev")
+    _check(f(rows_dim, cols_dim, b.shape[1], values.numel(), _p(values), _p(row_idx), _p(col_idx), _p(b), b.stride(0),
+             _p(c), c.stride(0), flavor, _stream_ptr(stream)))
+
+
+def gemm_dense_dev(a, b, c, flavor: int = FLAVOR_FMA, stream=None) -> None:
+    """Stream-ordered gemm_dense_blocked on device tensors."""
+    import torch
+    a = _dev_array("A", a, (torch.float32, torch.float64))
+    if a.dim() != 2:
+        raise ValueError("gemm_dense_blocked: A must be 2-D")
+    _check_dense_pair(a.dtype, b, c, a.shape[0], a.shape[1])
+    f = getattr(lib(), f"gcoo_gemm_dense_{'f64' if a.dtype == torch.float64 else 'f32'}_dev")
+    _check(f(a.shape[0], a.shape[1], b.shape[1], _p(a), a.stride(0), _p(b), b.stride(0), _p(c), c.stride(0), flavor,
+             _stream_ptr(stream)))
+
+
+def _check_dense_pair(dtype, b, c, m: int, k: int) -> None:
+    for name, t in (("B", b), ("C", c)):
+        if t.dim() != 2 or t.dtype != dtype or not t.is_cuda or t.stride(1) != 1:
+            raise ValueError(f"{name}: 2-D CUDA tensor of the operands' dtype with unit column stride required")
+    if b.shape[0] != k or c.shape[0] != m or c.shape[1] != b.shape[1]:
+        raise ValueError("inner dimensions differ / C has the wrong shape")
 
 
 # ------------------------------------------------------ device-resident ----
@@ -741,7 +855,8 @@ def generate_powerlaw_coo(n: int, s: float, alpha: float, seed: int):
 __all__ = [
     "ExecConfig", "KernelStats", "TimingBreakdown", "GcooMatrix", "DeviceGcoo", "dense_to_gcoo", "coo_to_gcoo",
     "csr_to_gcoo", "spdm_gcoo", "spdm_gcoo_auto", "spdm_gcoo_dev", "coo_to_gcoo_dev", "csr_to_gcoo_dev",
-    "dense_to_gcoo_dev", "SpdmPlan",
+    "dense_to_gcoo_dev", "SpdmPlan", "spdm_csr", "spdm_coo", "gemm_dense_blocked", "spdm_csr_dev", "spdm_coo_dev",
+    "gemm_dense_dev",
     "derive_seed", "generate_uniform_sparse", "generate_uniform_sparse_coo", "generate_powerlaw_coo",
     "device_count", "set_device", "launch_count", "lib", "FLAVOR_FMA", "FLAVOR_MUL_ADD",
     "read_matrix_market", "write_matrix_market", "read_matrix_market_gcoo_dev", "CooMatrix", "ParseError",

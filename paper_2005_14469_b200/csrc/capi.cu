@@ -4,7 +4,7 @@
 // (so the same inputs raise the same exception class), device buffers from the
 // stream-ordered pool, copies, and kernel launches.  All arithmetic on matrix
 // data happens in the CUDA kernels (spdm_rowtile.cuh, spdm_tacc.cuh,
-// construct.cuh); there is no host compute path.
+// construct.cuh, baselines.cuh); there is no host compute path.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -21,8 +21,11 @@
 
 #include "common.cuh"
 #include "construct.cuh"
+#include "baselines.cuh"
 #include "spdm_rowtile.cuh"
 #include "spdm_tacc.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
 
 namespace gcoo_b200 {
 
@@ -1042,6 +1045,177 @@ void dense_to_gcoo_host(int64_t m, int64_t k, int32_t p, const T* A, int64_t cap
   st = DenseStash{};
 }
 
+// ------------------------------------------------ baselines (§8f row 3) ---
+template <typename T>
+bool vec_ok(int64_t n, int64_t ldb, int64_t ldc, const T* B, const T* C) {
+  constexpr int V = VecOf<T>::V;
+  return n % V == 0 && ldb % V == 0 && ldc % V == 0 && (reinterpret_cast<uintptr_t>(B) % 16) == 0 &&
+         (reinterpret_cast<uintptr_t>(C) % 16) == 0;
+}
+
+// Row-split multiply over row_ptr (ranges: nullptr = one row per warp).
+template <typename T>
+void launch_rowsplit(int64_t units, const int64_t* ranges, int64_t n, const int64_t* rp, const int32_t* cols,
+                     const T* vals, const T* B, int64_t ldb, T* C, int64_t ldc, int flavor, cudaStream_t s) {
+  if (units == 0 || n == 0) return;
+  constexpr int V = VecOf<T>::V;
+  const int64_t ub = ceil_div(units, kSplitWarps);
+  const int64_t grid = ub * ceil_div(n, 32 * V);
+  if (grid > INT32_MAX) fail(GCOO_EINVAL, "spdm: problem too large for one launch");
+  const bool vec = vec_ok<T>(n, ldb, ldc, B, C);
+  const bool fma = flavor != GCOO_FLAVOR_MUL_ADD;
+  const cudaEvent_t kt0 = kt_start(s);
+#define GCOO_SPLIT(VEC, FMA)                                                                                 \
+  GCOO_LAUNCH((spdm_rowsplit_kernel<T, VEC, FMA>), (unsigned)grid, kSplitWarps * 32, 0, s, units, n, ranges, rp, \
+              cols, vals, B, ldb, C, ldc, ub)
+  if (vec && fma) GCOO_SPLIT(true, true);
+  else if (vec) GCOO_SPLIT(true, false);
+  else if (fma) GCOO_SPLIT(false, true);
+  else GCOO_SPLIT(false, false);
+#undef GCOO_SPLIT
+  kt_stop(s, kt0);
+}
+
+// spdm_csr (kernels.hpp:163-184): row-split over the caller's CSR, entries in
+// CSR order.  The reference reads an invalid CSR out of bounds; here a row_ptr
+// or column outside the matrix is an invalid_argument instead.
+template <typename T>
+void csr_spdm_device(int64_t m, int64_t k, int64_t n, int64_t nnz, const T* vals, const int32_t* cols,
+                     const int64_t* rp, const T* B, int64_t ldb, T* C, int64_t ldc, int flavor, cudaStream_t s) {
+  if (m < 1 || k < 1 || n < 1) einval("spdm_csr: dimensions must be >= 1");
+  if (nnz < 0 || ldb < n || ldc < n) einval("spdm_csr: bad sizes");
+  DevBuf<unsigned long long> bad(1, s);
+  GCOO_CUDA(cudaMemsetAsync(bad.get(), 0xff, sizeof(unsigned long long), s));
+  int64_t ends[2] = {0, 0};
+  d2h(&ends[0], rp, 1, s);
+  d2h(&ends[1], rp + m, 1, s);
+  GCOO_LAUNCH(csr_range_kernel, grid_for(m, 256), 256, 0, s, m, k, nnz, rp, cols, bad.get());
+  unsigned long long h = 0;
+  d2h(&h, bad.get(), 1, s);
+  GCOO_CUDA(cudaStreamSynchronize(s));
+  if (ends[0] != 0 || ends[1] != nnz) einval("spdm_csr: row_ptr endpoints wrong");
+  if (h != ~0ull) einval("spdm_csr: row_ptr or column out of range in row " + std::to_string(h));
+  launch_rowsplit<T>(m, nullptr, n, rp, cols, vals, B, ldb, C, ldc, flavor, s);
+}
+
+// spdm_coo (kernels.hpp:193-232): any entry order (duplicates too).  The
+// entries are stably sorted by row on the device when they are not already
+// row-ordered (CUB radix sort of (row, index) pairs — preprocessing of this
+// yardstick only), then row-aligned chunks of ~kCooChunk entries each go to one
+// warp per column strip.
+constexpr int64_t kCooChunk = 256;
+
+template <typename T>
+void coo_spdm_device(int64_t m, int64_t k, int64_t n, int64_t nnz, const T* vals, const int32_t* rows,
+                     const int32_t* cols, const T* B, int64_t ldb, T* C, int64_t ldc, int flavor, cudaStream_t s) {
+  if (m < 1 || k < 1 || n < 1) einval("spdm_coo: dimensions must be >= 1");
+  if (nnz < 0 || ldb < n || ldc < n) einval("spdm_coo: bad sizes");
+  if (m > INT32_MAX) einval("spdm_coo: too many rows");
+  DevBuf<unsigned long long> bad(1, s);
+  DevBuf<int> unsorted(1, s);
+  GCOO_CUDA(cudaMemsetAsync(bad.get(), 0xff, sizeof(unsigned long long), s));
+  GCOO_CUDA(cudaMemsetAsync(unsorted.get(), 0, sizeof(int), s));
+  if (nnz > 0)
+    GCOO_LAUNCH(coo_range_kernel, grid_for(nnz, 256), 256, 0, s, nnz, m, k, rows, cols, bad.get(), unsorted.get());
+  unsigned long long h = 0;
+  int h_unsorted = 0;
+  d2h(&h, bad.get(), 1, s);
+  d2h(&h_unsorted, unsorted.get(), 1, s);
+  GCOO_CUDA(cudaStreamSynchronize(s));
+  if (h != ~0ull) einval("spdm_coo: coordinate out of range at entry " + std::to_string(h));
+  const int32_t* srows = rows;
+  const int32_t* scols = cols;
+  const T* svals = vals;
+  DevBuf<int32_t> rows2, cols2;
+  DevBuf<T> vals2;
+  if (h_unsorted) {
+    DevBuf<int64_t> idx(nnz, s), perm(nnz, s);
+    rows2 = DevBuf<int32_t>(nnz, s);
+    cols2 = DevBuf<int32_t>(nnz, s);
+    vals2 = DevBuf<T>(nnz, s);
+    GCOO_LAUNCH(iota_kernel, grid_for(nnz, 256), 256, 0, s, nnz, idx.get());
+    size_t temp = 0;
+    const int bits = ilog2(m) + 1;
+    GCOO_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, rows, rows2.get(), idx.get(), perm.get(), nnz, 0, bits, s));
+    DevBuf<unsigned char> tmp(temp, s);
+    GCOO_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), temp, rows, rows2.get(), idx.get(), perm.get(), nnz, 0, bits, s));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    GCOO_LAUNCH(gather_entries_kernel<T>, grid_for(nnz, 256), 256, 0, s, nnz, (const int64_t*)perm.get(), vals, cols,
+                vals2.get(), cols2.get());
+    srows = rows2.get();
+    scols = cols2.get();
+    svals = vals2.get();
+  }
+  DevBuf<int64_t> rp(m + 1, s);
+  GCOO_LAUNCH(row_ptr_kernel, (unsigned)ceil_div(m + 1, 256), 256, 0, s, m, nnz, srows, rp.get());
+  const int64_t units = std::max<int64_t>(1, std::min<int64_t>(m, ceil_div(nnz, kCooChunk)));
+  DevBuf<int64_t> ranges(units + 1, s);
+  GCOO_LAUNCH(coo_chunk_ranges_kernel, grid_for(units + 1, 256), 256, 0, s, units, m, nnz,
+              std::max<int64_t>(1, ceil_div(nnz, units)), (const int64_t*)rp.get(), ranges.get());
+  launch_rowsplit<T>(units, ranges.get(), n, rp.get(), scols, svals, B, ldb, C, ldc, flavor, s);
+}
+
+// gemm_dense_blocked (kernels.hpp:107-155): the dense baseline.
+template <typename T>
+void gemm_dense_device(int64_t m, int64_t k, int64_t n, const T* A, int64_t lda, const T* B, int64_t ldb, T* C,
+                       int64_t ldc, int flavor, cudaStream_t s) {
+  if (m < 1 || k < 1 || n < 1) einval("gemm_dense_blocked: dimensions must be >= 1");
+  if (lda < k || ldb < n || ldc < n) einval("gemm_dense_blocked: leading dimension too small");
+  constexpr int BM = (kGemmThreads / 16) * GemmCfg<T>::TM, BN = 16 * GemmCfg<T>::TN;
+  const dim3 grid((unsigned)ceil_div(n, BN), (unsigned)ceil_div(m, BM));
+  if (ceil_div(m, BM) > 65535) einval("gemm_dense_blocked: too many rows for one launch");
+  if (flavor != GCOO_FLAVOR_MUL_ADD)
+    GCOO_LAUNCH((gemm_dense_kernel<T, true>), grid, kGemmThreads, 0, s, m, k, n, A, lda, B, ldb, C, ldc);
+  else
+    GCOO_LAUNCH((gemm_dense_kernel<T, false>), grid, kGemmThreads, 0, s, m, k, n, A, lda, B, ldb, C, ldc);
+}
+
+// Host-pointer wrappers: upload, compute, download (one stream, synchronised).
+template <typename T>
+void csr_spdm_host(int64_t m, int64_t k, int64_t n, int64_t nnz, const T* vals, const int32_t* cols,
+                   const int64_t* rp, const T* B, T* C) {
+  if (m < 1 || k < 1 || n < 1 || nnz < 0) einval("spdm_csr: dimensions must be >= 1");
+  cudaStream_t s = thread_stream();
+  DevBuf<T> dv(nnz, s), dB(k * n, s), dC(m * n, s);
+  DevBuf<int32_t> dc(nnz, s);
+  DevBuf<int64_t> drp(m + 1, s);
+  h2d(dv.get(), vals, nnz, s);
+  h2d(dc.get(), cols, nnz, s);
+  h2d(drp.get(), rp, m + 1, s);
+  h2d(dB.get(), B, k * n, s);
+  csr_spdm_device<T>(m, k, n, nnz, dv.get(), dc.get(), drp.get(), dB.get(), n, dC.get(), n, GCOO_FLAVOR_FMA, s);
+  d2h(C, dC.get(), m * n, s);
+  GCOO_CUDA(cudaStreamSynchronize(s));
+}
+
+template <typename T>
+void coo_spdm_host(int64_t m, int64_t k, int64_t n, int64_t nnz, const T* vals, const int32_t* rows,
+                   const int32_t* cols, const T* B, T* C) {
+  if (m < 1 || k < 1 || n < 1 || nnz < 0) einval("spdm_coo: dimensions must be >= 1");
+  cudaStream_t s = thread_stream();
+  DevBuf<T> dv(nnz, s), dB(k * n, s), dC(m * n, s);
+  DevBuf<int32_t> dr(nnz, s), dc(nnz, s);
+  h2d(dv.get(), vals, nnz, s);
+  h2d(dr.get(), rows, nnz, s);
+  h2d(dc.get(), cols, nnz, s);
+  h2d(dB.get(), B, k * n, s);
+  coo_spdm_device<T>(m, k, n, nnz, dv.get(), dr.get(), dc.get(), dB.get(), n, dC.get(), n, GCOO_FLAVOR_FMA, s);
+  d2h(C, dC.get(), m * n, s);
+  GCOO_CUDA(cudaStreamSynchronize(s));
+}
+
+template <typename T>
+void gemm_dense_host(int64_t m, int64_t k, int64_t n, const T* A, const T* B, T* C) {
+  if (m < 1 || k < 1 || n < 1) einval("gemm_dense_blocked: dimensions must be >= 1");
+  cudaStream_t s = thread_stream();
+  DevBuf<T> dA(m * k, s), dB(k * n, s), dC(m * n, s);
+  h2d(dA.get(), A, m * k, s);
+  h2d(dB.get(), B, k * n, s);
+  gemm_dense_device<T>(m, k, n, dA.get(), k, dB.get(), n, dC.get(), n, GCOO_FLAVOR_FMA, s);
+  d2h(C, dC.get(), m * n, s);
+  GCOO_CUDA(cudaStreamSynchronize(s));
+}
+
 }  // namespace gcoo_b200
 
 // =================================================================== C ABI =
@@ -1398,5 +1572,44 @@ int gcoo_csr_to_gcoo_f64_dev(int64_t m, int64_t k, int32_t p, int64_t nnz, const
                                g_idxes, nnz_per_group, static_cast<cudaStream_t>(stream));
   });
 }
+
+// ---------------------------------------------------------------- baselines
+#define GCOO_BASELINE_ABI(SFX, T)                                                                               \
+  int gcoo_spdm_csr_##SFX(int64_t m, int64_t k, int64_t n, int64_t nnz, const T* values, const int32_t* col_idx, \
+                          const int64_t* row_ptr, const T* B, T* C) {                                          \
+    return guarded([&] { csr_spdm_host<T>(m, k, n, nnz, values, col_idx, row_ptr, B, C); });                  \
+  }                                                                                                            \
+  int gcoo_spdm_csr_##SFX##_dev(int64_t m, int64_t k, int64_t n, int64_t nnz, const T* values,                 \
+                                const int32_t* col_idx, const int64_t* row_ptr, const T* B, int64_t ldb, T* C, \
+                                int64_t ldc, int flavor, void* stream) {                                       \
+    return guarded([&] {                                                                                       \
+      csr_spdm_device<T>(m, k, n, nnz, values, col_idx, row_ptr, B, ldb, C, ldc, flavor,                       \
+                         static_cast<cudaStream_t>(stream));                                                   \
+    });                                                                                                        \
+  }                                                                                                            \
+  int gcoo_spdm_coo_##SFX(int64_t m, int64_t k, int64_t n, int64_t nnz, const T* values, const int32_t* row_idx, \
+                          const int32_t* col_idx, const T* B, T* C) {                                          \
+    return guarded([&] { coo_spdm_host<T>(m, k, n, nnz, values, row_idx, col_idx, B, C); });                   \
+  }                                                                                                            \
+  int gcoo_spdm_coo_##SFX##_dev(int64_t m, int64_t k, int64_t n, int64_t nnz, const T* values,                 \
+                                const int32_t* row_idx, const int32_t* col_idx, const T* B, int64_t ldb, T* C, \
+                                int64_t ldc, int flavor, void* stream) {                                       \
+    return guarded([&] {                                                                                       \
+      coo_spdm_device<T>(m, k, n, nnz, values, row_idx, col_idx, B, ldb, C, ldc, flavor,                       \
+                         static_cast<cudaStream_t>(stream));                                                   \
+    });                                                                                                        \
+  }                                                                                                            \
+  int gcoo_gemm_dense_##SFX(int64_t m, int64_t k, int64_t n, const T* A, const T* B, T* C) {                   \
+    return guarded([&] { gemm_dense_host<T>(m, k, n, A, B, C); });                                             \
+  }                                                                                                            \
+  int gcoo_gemm_dense_##SFX##_dev(int64_t m, int64_t k, int64_t n, const T* A, int64_t lda, const T* B,        \
+                                  int64_t ldb, T* C, int64_t ldc, int flavor, void* stream) {                  \
+    return guarded([&] {                                                                                       \
+      gemm_dense_device<T>(m, k, n, A, lda, B, ldb, C, ldc, flavor, static_cast<cudaStream_t>(stream));        \
+    });                                                                                                        \
+  }
+GCOO_BASELINE_ABI(f32, float)
+GCOO_BASELINE_ABI(f64, double)
+#undef GCOO_BASELINE_ABI
 
 }  // extern "C"

@@ -42,8 +42,8 @@ def _worker(rank, world, port, q, mode):
             from oracle import Oracle
             O = Oracle()
             rng = np.random.default_rng(7)
-            m, k, n = 3000, 2500, 1000
-            a = np.where(rng.random((m, k)) < 0.01, 1.0 - rng.random((m, k)), 0.0).astype(np.float32)
+            m, k, n = 4000, 4000, 2048  # each 1024-column shard is a 0.66 GFLOP product: the TMEM kernel
+            a = np.where(rng.random((m, k)) < 0.02, 1.0 - rng.random((m, k)), 0.0).astype(np.float32)
             b = (1.0 - rng.random((k, n))).astype(np.float32)
             dg = G.dense_to_gcoo_dev(torch.from_numpy(a).to(dev), 4)
             lo, hi = column_shards(n, world)[rank]

@@ -242,3 +242,29 @@ def test_traffic_restatement_vs_reference_random(reference):
             for csr in (False, True):
                 assert model_traffic(rows, cols, m, k, n, p, b, inf, csr) == \
                     R.model_traffic(rows, cols, m, k, n, p, b, inf, csr), (m, k, n, p, b, inf, csr)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_baseline_restatements_match_reference(oracle, reference, dtype):
+    """The plain-C restatements of the reference's comparison kernels —
+    spdm_csr (kernels.hpp:163-184), spdm_coo in any entry order with
+    duplicates (:193-232), gemm_dense_blocked (:107-155) — equal the compiled
+    reference bit for bit, as shipped (mul+add) and built -mfma, for several
+    (p, b, workers) (the reference's result must not depend on them)."""
+    R, RF = reference
+    rng = np.random.default_rng(5 if dtype == np.float32 else 6)
+    for trial in range(8):
+        m, k, n = (int(x) for x in rng.integers(1, 120, size=3))
+        a = np.where(rng.random((m, k)) < 0.15, 1.0 - rng.random((m, k)), 0.0).astype(dtype)
+        b = (1.0 - rng.random((k, n))).astype(dtype)
+        r, c = np.nonzero(a)
+        v = a[r, c]
+        rp = np.concatenate([[0], np.cumsum(np.count_nonzero(a, axis=1))]).astype(np.int64)
+        perm = rng.permutation(r.size)
+        dup = rng.integers(0, max(r.size, 1), size=min(4, r.size))
+        rr, cc, vv = (np.concatenate([x[perm], x[dup]]) for x in (r, c, v))
+        p, bw, w = 1 << int(rng.integers(0, 5)), 1 << int(rng.integers(0, 8)), int(rng.integers(0, 4))
+        for fma, Rx in ((False, R), (True, RF)):
+            assert np.array_equal(oracle.spdm_csr(m, v, c, rp, b, fma), Rx.spdm_csr(m, k, v, c, rp, b, p, bw, w))
+            assert np.array_equal(oracle.spdm_coo(m, vv, rr, cc, b, fma), Rx.spdm_coo(m, k, vv, rr, cc, b, p, bw, w))
+            assert np.array_equal(oracle.gemm_dense(a, b, fma), Rx.gemm_dense(a, b, p, bw, w))
