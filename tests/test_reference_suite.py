@@ -76,18 +76,34 @@ def test_matrix_market_into_gpu_path(cuda, gcoo):
 @pytest.mark.gpu
 def test_reference_acceptance_gate_on_b200(cuda, gcoo):
     """The reference's acceptance gate (proj/tests/acceptance.cpp, compiled
-    unmodified against the drop-in headers): c1 oracle equivalence (fp32 <=
-    1e-5, fp64 <= 1e-12 over 400 instances, < 120 s), c2 golden example, c3
-    round trips, c4 reuse accounting == traffic model, c5 traffic trends, c6
-    roofline constants, c7 desk-scale performance properties, c8 determinism.
-    c9 drives the reference's CLI (gcoo_bench needs CLI11, absent here; not on
-    the hot path), so it is the one expected FAIL."""
+    unmodified against the drop-in headers) reaches the same verdicts on the
+    B200 as the reference built natively on its own CPU code
+    (tests/golden/acceptance_native.json, tests/golden/make_acceptance_golden.py):
+    c1 oracle equivalence (fp32 <= 1e-5, fp64 <= 1e-12 over 400 instances,
+    < 120 s), c2 golden example, c3 round trips, c4 reuse accounting == traffic
+    model, c6 roofline constants, c7 desk-scale performance properties, c8
+    determinism PASS.  c5 FAILS in the reference itself (its modeled traffic
+    grows with exponent ~2.95 in n, outside the gate's [1.7, 2.3]) and must
+    fail here with the same model numbers; c9 drives the reference CLI
+    (gcoo_bench needs CLI11, absent; not on the hot path)."""
+    import json
+    import re
     exe = os.path.join(BUILD, "ref_acceptance")
     if not os.path.exists(exe):
         pytest.skip(f"{exe} not built (needs the reference sources: make -C tests/cpp)")
+    with open(os.path.join(ROOT, "tests", "golden", "acceptance_native.json")) as f:
+        native = json.load(f)
     r = subprocess.run([exe, "/nonexistent/gcoo_bench"], capture_output=True, text=True, timeout=900)
-    lines = [x for x in r.stdout.splitlines() if x.startswith(("PASS", "FAIL"))]
-    for c in range(1, 9):
-        assert any(x.startswith(f"PASS: criterion {c} ") for x in lines), r.stdout
-    assert any(x.startswith("FAIL: criterion 9 ") for x in lines), r.stdout
-    assert r.returncode == 1, r.stdout
+    got = {}
+    for line in r.stdout.splitlines():
+        m = re.match(r"(PASS|FAIL): criterion (\d+) - (.*?)(?: \[(.*)\])?$", line)
+        if m:
+            got[m.group(2)] = (m.group(1), m.group(4) or "")
+    assert sorted(got, key=int) == [str(c) for c in range(1, 10)], r.stdout
+    for c, ref in native.items():
+        assert got[c][0] == ref["verdict"], (c, got[c], ref)
+    for c in ("1", "2", "3", "4", "6", "7", "8"):
+        assert got[c][0] == "PASS", (c, r.stdout)
+    nums = lambda t: [float(x) for x in re.findall(r"exponent=([0-9.e+-]+)", t)]  # noqa: E731
+    assert nums(got["5"][1]) == pytest.approx(nums(native["5"]["detail_model"]), rel=1e-12)
+    assert r.returncode == sum(v["verdict"] == "FAIL" for v in native.values()), r.stdout
