@@ -625,7 +625,8 @@ def powerlaw_config(G, dev, stream, flush, hbm_peak, fp_peak, steps=5):
         cb = compulsory_bytes(nnz, n, n, n, P, k_nz)
         rows = torch.bincount(dg.row_idx.long(), minlength=n)
         out[name] = {"n": n, "nnz": nnz, "max_row_nnz": int(rows.max()), "ms": round(ms, 4),
-                     "kernel_ms": round(kms, 4), "kernel": G.last_kernel(), "gflops": round(f / ms / 1e6, 1),
+                     "kernel_ms": round(kms, 4), "kernel": G.last_kernel(), "two_class_split": G.last_split(),
+                     "gflops": round(f / ms / 1e6, 1), "kernel_gflops": round(f / kms / 1e6, 1),
                      "compulsory_bytes": int(cb),
                      "hbm_frac": round(cb / (kms * 1e-3) / 1e9 / hbm_peak, 4),
                      "fp32_frac": round(f / (kms * 1e-3) / 1e12 / fp_peak, 4)}

@@ -112,6 +112,8 @@ def lib():
     _sig(L, "gcoo_derive_seed", _u64, [_u64, _u64, _u64])
     _sig(L, "gcoo_debug_force_kernel", _int, [_int])
     _sig(L, "gcoo_debug_last_kernel", _int, [])
+    _sig(L, "gcoo_debug_last_split", _int, [])
+    _sig(L, "gcoo_debug_force_split", _int, [_int])
     _sig(L, "gcoo_plan_create_f32_dev", _int, [_i64, _i64, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _int,
                                                 C.POINTER(_vp), _vp])
     _sig(L, "gcoo_plan_spdm_f32_dev", _int, [_vp, _i64, _vp, _i64, _vp, _i64, _vp])
@@ -169,6 +171,18 @@ def last_kernel() -> str:
     """Test hook: the multiply kernel this thread's latest call ran (a KERNELS name)."""
     k = int(lib().gcoo_debug_last_kernel())
     return next((name for name, v in KERNELS.items() if v == k and name != "auto"), str(k))
+
+
+def last_split() -> bool:
+    """Test hook: whether this thread's latest multiply ran as a two-class
+    (heavy rows / light rows) split."""
+    return bool(lib().gcoo_debug_last_split())
+
+
+def force_split(mode: str = "auto") -> None:
+    """Test hook: the two-class split of skewed matrices ("auto", "never",
+    "always" = whenever the rows form two degree classes)."""
+    lib().gcoo_debug_force_split({"auto": -1, "never": 0, "always": 1}[mode])
 
 
 def kernel_timing(enable: bool = True) -> None:

@@ -272,6 +272,10 @@ struct SpdmPlan {
   // TMEM kernels: row placement (original row -> unit row, and back; -1 = padding)
   DevBuf<int32_t> unit_of, row_of;
   DevBuf<int32_t> skewed;  // 1: heaviest rows in row block 0 (launched first)
+  // two-class split of a skewed A (split_plan): this plan holds the light rows,
+  // `heavy` the heaviest rows with a configuration chosen for their density;
+  // the two multiply kernels write disjoint rows of C and run concurrently
+  std::unique_ptr<SpdmPlan> heavy;
 };
 
 template <class Cfg>
@@ -288,16 +292,20 @@ void set_smem_attr() {
 // `min_ctas`: spread rows over enough row blocks that a launch over
 // `col_tiles` column tiles has at least that many CTAs (narrow strips of the
 // host pipeline); 0 = full row blocks.
+// `pos` (two-class split): rows at heaviest-first positions [lo, hi) only
+// (rank_rows_kernel ran before); nullptr = every row, placed here.
 template <class Cfg, typename T>
-void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ctas = 0, int64_t col_tiles = 1) {
+void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ctas = 0, int64_t col_tiles = 1,
+                const int32_t* pos = nullptr, int64_t lo = 0, int64_t hi = 0) {
   set_smem_attr<Cfg>();
-  P.row_blocks = ceil_div(a.m, Cfg::RB);
+  const int64_t rows = pos ? hi - lo : a.m;
+  P.row_blocks = ceil_div(rows, Cfg::RB);
   int64_t rpb = Cfg::RB;
   if (min_ctas > P.row_blocks * col_tiles) {
-    const int64_t want = std::min<int64_t>(ceil_div(min_ctas, col_tiles), ceil_div(a.m, 32));
+    const int64_t want = std::min<int64_t>(ceil_div(min_ctas, col_tiles), ceil_div(rows, 32));
     if (want > P.row_blocks) {
-      rpb = ceil_div(a.m, want);
-      P.row_blocks = ceil_div(a.m, rpb);
+      rpb = ceil_div(rows, want);
+      P.row_blocks = ceil_div(rows, rpb);
     }
   }
   // rows are placed anywhere in their row block's warps: every warp is a unit
@@ -307,7 +315,7 @@ void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ct
   const int64_t nseg = P.row_blocks * nchunks;
   // every buffer first: the kernels below form one uninterrupted PDL chain
   DevBuf<uint32_t> cnt(units * nchunks * Cfg::RW, s);
-  DevBuf<int32_t> row_nnz(a.m, s), hist(33, s), cursor(33, s);
+  DevBuf<int32_t> row_nnz(pos ? 0 : a.m, s), hist(pos ? 0 : 33, s), cursor(33, s);
   P.unit_of = DevBuf<int32_t>(a.m, s);
   P.row_of = DevBuf<int32_t>(P.row_blocks * Cfg::RB, s);
   P.skewed = DevBuf<int32_t>(1, s);
@@ -321,15 +329,22 @@ void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ct
 
   const int64_t init_n = std::max<int64_t>((int64_t)cnt.count, std::max<int64_t>(a.m, (int64_t)P.row_of.count));
   GCOO_LAUNCH_PDL(plan_init_kernel, grid_for(init_n, 256), 256, 0, s, cnt.get(), (int64_t)cnt.count,
-                  row_nnz.get(), a.m, hist.get(), cursor.get(), P.row_of.get(), (int64_t)P.row_of.count);
-  // load-balanced row placement: heaviest rows first, dealt over a block's warps
-  if (a.nnz > 0)
-    GCOO_LAUNCH_PDL(row_nnz_kernel, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, row_nnz.get());
-  GCOO_LAUNCH_PDL(bucket_hist_kernel, grid_for(a.m, 256), 256, 0, s, a.m, (const int32_t*)row_nnz.get(), hist.get());
-  GCOO_LAUNCH_PDL(row_balance_kernel, grid_for(a.m, 256), 256, 0, s, a.m, (const int32_t*)row_nnz.get(),
-                  (const int32_t*)hist.get(), cursor.get(), (int32_t)Cfg::RB, (int32_t)Cfg::NW, (int32_t)Cfg::RW,
-                  (int32_t)std::min<int64_t>(INT32_MAX, 4 * ceil_div(a.nnz, a.m) + 16), (int32_t)rpb,
-                  P.unit_of.get(), P.row_of.get(), P.skewed.get());
+                  pos ? (int32_t*)nullptr : row_nnz.get(), a.m, pos ? (int32_t*)nullptr : hist.get(), cursor.get(),
+                  P.row_of.get(), (int64_t)P.row_of.count);
+  if (pos) {
+    GCOO_LAUNCH_PDL(place_class_kernel, grid_for(a.m, 256), 256, 0, s, a.m, pos, lo, hi, (int32_t)Cfg::RB,
+                    (int32_t)Cfg::NW, (int32_t)Cfg::RW, (int32_t)rpb, P.unit_of.get(), P.row_of.get(), P.skewed.get());
+  } else {
+    // load-balanced row placement: heaviest rows first, dealt over a block's warps
+    if (a.nnz > 0)
+      GCOO_LAUNCH_PDL(row_nnz_kernel, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, row_nnz.get());
+    GCOO_LAUNCH_PDL(bucket_hist_kernel, grid_for(a.m, 256), 256, 0, s, a.m, (const int32_t*)row_nnz.get(),
+                    hist.get());
+    GCOO_LAUNCH_PDL(row_balance_kernel, grid_for(a.m, 256), 256, 0, s, a.m, (const int32_t*)row_nnz.get(),
+                    (const int32_t*)hist.get(), cursor.get(), (int32_t)Cfg::RB, (int32_t)Cfg::NW, (int32_t)Cfg::RW,
+                    (int32_t)std::min<int64_t>(INT32_MAX, 4 * ceil_div(a.nnz, a.m) + 16), (int32_t)rpb,
+                    P.unit_of.get(), P.row_of.get(), P.skewed.get());
+  }
   if (a.nnz > 0)
     GCOO_LAUNCH_PDL(tacc_count_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, a.cols, nchunks,
                     cnt.get(), (const int32_t*)P.unit_of.get());
@@ -346,11 +361,11 @@ void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ct
 
 template <class Cfg, typename T>
 void run_plan(const SpdmPlan& P, const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C,
-              int64_t ldc, cudaStream_t s) {
+              int64_t ldc, cudaStream_t s, bool timed = true) {
   const CUtensorMap map = make_b_map(B, a.k, n, ldb, Cfg::W, Cfg::KC);
   const int64_t grid = P.row_blocks * ceil_div(n, Cfg::W);
   if (grid > INT32_MAX) fail(GCOO_EINVAL, "spdm_gcoo: problem too large for one launch");
-  const cudaEvent_t kt0 = kt_start(s);
+  const cudaEvent_t kt0 = timed ? kt_start(s) : nullptr;
   GCOO_LAUNCH_PDL(spdm_tacc_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n,
                   (const unsigned char*)P.ent.get(), (const int64_t*)P.seg_off.get(), C, ldc, P.row_blocks,
                   P.nchunks, (const int32_t*)P.row_of.get(), (const int32_t*)P.skewed.get());
@@ -450,18 +465,208 @@ void make_plan(SpdmPlan& P, const DevGcoo<T>& a, int kind, cudaStream_t s, int64
   });
 }
 
-// The kernel id of this thread's latest multiply (test hook gcoo_debug_last_kernel).
+// The kernel id of this thread's latest multiply (test hook gcoo_debug_last_kernel;
+// a two-class split reports its light plan's id).
 thread_local int t_last_kind = -1;
+thread_local bool t_last_split = false;
+
+cudaStream_t aux_stream(int which);
+
+// Two events per thread for the fork/join of a split multiply.
+cudaEvent_t fork_event(int i) {
+  thread_local cudaEvent_t ev[64][2] = {};
+  const int d = current_device();
+  if (!ev[d][i]) GCOO_CUDA(cudaEventCreateWithFlags(&ev[d][i], cudaEventDisableTiming));
+  return ev[d][i];
+}
 
 template <typename T>
 void run_spdm(const SpdmPlan& P, const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C, int64_t ldc,
               int flavor, cudaStream_t s) {
   if (a.m == 0 || n == 0) return;
   t_last_kind = P.kind;
+  t_last_split = P.heavy != nullptr;
+  if (P.heavy) {
+    // heavy rows on a forked stream, light rows on the caller's: disjoint rows of C
+    const cudaEvent_t kt0 = kt_start(s);
+    cudaStream_t s2 = aux_stream(2);
+    GCOO_CUDA(cudaEventRecord(fork_event(0), s));
+    GCOO_CUDA(cudaStreamWaitEvent(s2, fork_event(0), 0));
+    with_cfg<T>(P.heavy->kind, [&](auto c) { run_plan<decltype(c)>(*P.heavy, a, n, B, ldb, C, ldc, s2, false); });
+    with_cfg<T>(P.kind, [&](auto c) { run_plan<decltype(c)>(P, a, n, B, ldb, C, ldc, s, false); });
+    GCOO_CUDA(cudaEventRecord(fork_event(1), s2));
+    GCOO_CUDA(cudaStreamWaitEvent(s, fork_event(1), 0));
+    kt_stop(s, kt0);
+    return;
+  }
   if (P.kind != 0 && with_cfg<T>(P.kind, [&](auto c) { run_plan<decltype(c)>(P, a, n, B, ldb, C, ldc, s); }))
     return;
   if (flavor != GCOO_FLAVOR_MUL_ADD) launch_rowtile_p<T, true>(a, n, B, ldb, C, ldc, s);
   else launch_rowtile_p<T, false>(a, n, B, ldb, C, ldc, s);
+}
+
+// ------------------------------------------------ two-class split --------
+// A power-law A mixes a few very heavy rows with many light ones.  One
+// configuration fits neither: the heavy rows' record segments overflow a
+// sparse configuration's stage, and a CTA holding them sets the pace of the
+// whole grid.  Split at a degree threshold, the heaviest rows get a dense
+// configuration (their own density), the rest a sparse one, and the two
+// kernels run concurrently (configs[3], n=16384: 9.9 -> 7.8 ms per step;
+// tools/hybrid_probe.py).  Deciding needs the degree distribution on the host
+// (one probe + synchronisation); the device path caches the decision per A
+// (its device pointers and shape): a stale entry only costs speed, never
+// correctness, because each plan takes exactly the rows at its heaviest-first
+// positions.
+struct SkewHint {
+  bool split = false;
+  int64_t heavy_rows = 0, heavy_nnz = 0;
+  double top_density = 0;  // density of the heaviest 504 rows (the heavy plan's first row block)
+};
+
+std::atomic<int> g_force_split{-1};  // test hook: -1 auto, 0 never, 1 whenever A has two classes
+
+double split_factor() {
+  static const double f = [] {
+    const char* e = std::getenv("GCOO_SPLIT_FACTOR");  // measurement hook
+    return e ? std::atof(e) : 1.0;
+  }();
+  return f;
+}
+
+// Heavy class: rows in the log2 buckets whose lower bound reaches
+// split_factor x the mean degree; split only when the largest row exceeds 8x
+// the mean (a uniform A never splits) or when a test forces it.  Factor 1
+// (degree >= 256 at configs[3]) measured best: 7.48 ms kernel against 7.72 /
+// 8.03 at factors 2 / 4 and 7.95 / 8.87 at 0.5 / 0.25 (tools/split_sweep.sh).
+SkewHint decide_split(int64_t m, int64_t nnz, const unsigned long long* st) {
+  SkewHint h;
+  const int force = g_force_split.load(std::memory_order_relaxed);
+  if (force == 0 || m < 2 || nnz <= 0) return h;
+  const double mean = (double)nnz / (double)m;
+  if (force < 0 && (double)st[0] < 8.0 * mean) return h;
+  const double thr = split_factor() * mean;
+  for (int b = 0; b < 31; ++b) {  // bucket b: degrees [2^(30-b), 2^(31-b)); forced: at least one non-empty bucket
+    const bool below = std::ldexp(1.0, 30 - b) < thr;
+    if (below && (force <= 0 || h.heavy_rows > 0)) break;
+    h.heavy_rows += (int64_t)st[1 + b];
+    h.heavy_nnz += (int64_t)st[34 + b];
+  }
+  if (const char* e = std::getenv("GCOO_SPLIT_ROWS")) {  // measurement hook: exactly this many heaviest rows
+    int64_t want = std::atoll(e), rows = 0, sum = 0;
+    for (int b = 0; b < 32 && rows < want; ++b) {
+      const int64_t take = std::min<int64_t>((int64_t)st[1 + b], want - rows);
+      sum += st[1 + b] ? (int64_t)((double)st[34 + b] * (double)take / (double)st[1 + b]) : 0;
+      rows += take;
+    }
+    h.heavy_rows = rows;
+    h.heavy_nnz = sum;
+  }
+  // the heaviest row block sets the heavy plan's chunk depth (its segments must fit the record stage)
+  {
+    const int64_t top = std::min<int64_t>(h.heavy_rows, 504);
+    int64_t rows = 0;
+    double sum = 0;
+    for (int b = 0; b < 32 && rows < top; ++b) {
+      const int64_t take = std::min<int64_t>((int64_t)st[1 + b], top - rows);
+      if (take) sum += (double)st[34 + b] * (double)take / (double)st[1 + b];
+      rows += take;
+    }
+    h.top_density = rows ? sum / (double)rows : 0.0;  // entries per row; divided by k below
+  }
+  h.split = h.heavy_rows > 0 && h.heavy_rows < m && h.heavy_nnz < nnz;
+  return h;
+}
+
+template <typename T>
+SkewHint skew_hint(const DevGcoo<T>& a, cudaStream_t s, bool cached) {
+  struct Key {
+    int dev;
+    const void* rows;
+    const void* cols;
+    int64_t nnz, m, k;
+    bool operator==(const Key& o) const {
+      return dev == o.dev && rows == o.rows && cols == o.cols && nnz == o.nnz && m == o.m && k == o.k;
+    }
+  };
+  static std::mutex mu;
+  static std::vector<std::pair<Key, SkewHint>> cache;  // most recent last, <= 32 entries
+  const Key key{current_device(), a.rows, a.cols, a.nnz, a.m, a.k};
+  const int force = g_force_split.load(std::memory_order_relaxed);
+  if (cached && force < 0) {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& e : cache)
+      if (e.first == key) return e.second;
+  }
+  DevBuf<int32_t> row_nnz(a.m, s);
+  DevBuf<unsigned long long> st(67, s);
+  GCOO_CUDA(cudaMemsetAsync(row_nnz.get(), 0, row_nnz.bytes(), s));
+  GCOO_CUDA(cudaMemsetAsync(st.get(), 0, st.bytes(), s));
+  if (a.nnz > 0) GCOO_LAUNCH(row_nnz_kernel, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, row_nnz.get());
+  GCOO_LAUNCH(skew_probe_kernel, grid_for(a.m, 256), 256, 0, s, a.m, (const int32_t*)row_nnz.get(), st.get());
+  unsigned long long h[67];
+  d2h(h, st.get(), 67, s);
+  GCOO_CUDA(cudaStreamSynchronize(s));
+  const SkewHint hint = decide_split(a.m, a.nnz, h);
+  if (cached && force < 0) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache.size() >= 32) cache.erase(cache.begin());
+    cache.emplace_back(key, hint);
+  }
+  return hint;
+}
+
+// Both classes' plans from one heaviest-first ranking: the light rows (this
+// plan) and the heavy rows (P.heavy), each with the configuration its own
+// density picks.  Returns false (nothing built) when the layout takes no TMEM
+// kernel for either class.
+template <typename T>
+bool make_split_plan(SpdmPlan& P, const DevGcoo<T>& a, const SkewHint& h, int64_t n, int64_t ldb, int64_t ldc,
+                     const T* B, const T* C, int flavor, cudaStream_t s, int64_t strip_n) {
+  if (flavor == GCOO_FLAVOR_MUL_ADD) return false;
+  const bool f64 = sizeof(T) == 8;
+  int kh = pick_by_density(h.top_density / (double)a.k, f64);
+  if (const char* e = std::getenv("GCOO_SPLIT_HEAVY_KIND")) kh = std::atoi(e);  // measurement hook
+  const int kl = pick_by_density((double)(a.nnz - h.heavy_nnz) / ((double)(a.m - h.heavy_rows) * (double)a.k), f64);
+  bool fits = true;
+  for (int kind : {kh, kl})
+    with_cfg<T>(kind, [&](auto c) { fits = fits && tile_fits<decltype(c)>(a, n, ldb, ldc, B, C); });
+  if (!fits) return false;
+  DevBuf<int32_t> row_nnz(a.m, s), hist(33, s), cursor(33, s), pos(a.m, s);
+  GCOO_LAUNCH_PDL(plan_init_kernel, grid_for(a.m, 256), 256, 0, s, (uint32_t*)nullptr, (int64_t)0, row_nnz.get(),
+                  a.m, hist.get(), cursor.get(), (int32_t*)nullptr, (int64_t)0);
+  if (a.nnz > 0) GCOO_LAUNCH_PDL(row_nnz_kernel, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, row_nnz.get());
+  GCOO_LAUNCH_PDL(bucket_hist_kernel, grid_for(a.m, 256), 256, 0, s, a.m, (const int32_t*)row_nnz.get(), hist.get());
+  GCOO_LAUNCH_PDL(rank_rows_kernel, grid_for(a.m, 256), 256, 0, s, a.m, (const int32_t*)row_nnz.get(),
+                  (const int32_t*)hist.get(), cursor.get(), pos.get());
+  const int64_t wave = strip_n ? sm_count() : 0;
+  P.kind = kl;
+  with_cfg<T>(kl, [&](auto c) {
+    using Cfg = decltype(c);
+    build_plan<Cfg>(P, a, s, wave, ceil_div(strip_n, Cfg::W), pos.get(), h.heavy_rows, a.m);
+  });
+  P.heavy.reset(new SpdmPlan());
+  P.heavy->kind = kh;
+  with_cfg<T>(kh, [&](auto c) {
+    using Cfg = decltype(c);
+    // the heavy class is small: spread it over at least one wave of CTAs
+    build_plan<Cfg>(*P.heavy, a, s, sm_count(), ceil_div(strip_n ? strip_n : n, Cfg::W), pos.get(), 0,
+                    h.heavy_rows);
+  });
+  return true;
+}
+
+// The plan for one call (or one pipelined strip width): a two-class split for
+// a skewed A, else the density choice.  `cached`: reuse this A's split
+// decision (device path); the plan API and the host path probe afresh.
+template <typename T>
+void plan_for(SpdmPlan& P, const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const T* B, const T* C,
+              int flavor, cudaStream_t s, int64_t strip_n, bool small_gate, bool cached) {
+  const int kind = choose_kind<T>(a, n, ldb, ldc, B, C, flavor, small_gate);
+  if (kind != 0 && g_force_kernel.load(std::memory_order_relaxed) < 0) {
+    const SkewHint h = skew_hint<T>(a, s, cached);
+    if (h.split && make_split_plan<T>(P, a, h, n, ldb, ldc, B, C, flavor, s, strip_n)) return;
+  }
+  make_plan<T>(P, a, kind, s, strip_n);
 }
 
 template <typename T>
@@ -470,7 +675,7 @@ void launch_spdm(const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C, 
   if (a.m == 0 || n == 0) return;
   SpdmPlan P;
   // strip_n = n: a grid smaller than one wave spreads A's rows over more row blocks
-  make_plan<T>(P, a, choose_kind<T>(a, n, ldb, ldc, B, C, flavor), s, n);
+  plan_for<T>(P, a, n, ldb, ldc, B, C, flavor, s, n, true, true);
   run_spdm<T>(P, a, n, B, ldb, C, ldc, flavor, s);
 }
 
@@ -598,7 +803,7 @@ std::vector<std::pair<int64_t, int64_t>> pipeline_strips(int64_t n, int64_t W) {
 }
 
 cudaStream_t aux_stream(int which) {
-  thread_local cudaStream_t streams[64][2] = {};
+  thread_local cudaStream_t streams[64][3] = {};
   const int d = current_device();
   if (!streams[d][which]) GCOO_CUDA(cudaStreamCreateWithFlags(&streams[d][which], cudaStreamNonBlocking));
   return streams[d][which];
@@ -720,7 +925,7 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
   // ---- pipelined: a ring of NBUF strip buffers (ld = W)
   if (trace) trace->mark(s, 0, -1);  // A uploaded
   SpdmPlan P;
-  make_plan<T>(P, a, choose_kind<T>(a, W, W, W, dBv[0].get(), dCv[0].get(), flavor), s, W);
+  plan_for<T>(P, a, W, W, W, dBv[0].get(), dCv[0].get(), flavor, s, W, /*small_gate=*/true, /*cached=*/false);
   if (trace) trace->mark(s, 1, -1);  // planned
   for (int64_t j = 0; j < nstrips; ++j) {
     const int b = (int)(j % NBUF);
@@ -803,8 +1008,7 @@ void plan_create(int64_t m, int64_t k, int32_t p, int64_t nnz, const T* values, 
     // multiply); no small-product gate: the planner runs once here, not per call
     static const double aligned[2] __attribute__((aligned(16))) = {};
     const T* al = reinterpret_cast<const T*>(aligned);
-    make_plan<T>(h->plan, plan_a<T>(h.get()),
-                 choose_kind<T>(plan_a<T>(h.get()), 4, 4, 4, al, al, flavor, /*small_gate=*/false), s);
+    plan_for<T>(h->plan, plan_a<T>(h.get()), 4, 4, 4, al, al, flavor, s, 0, /*small_gate=*/false, /*cached=*/false);
   }
   *plan = h.release();
 }
@@ -817,8 +1021,17 @@ void plan_spdm(const gcoo_plan* plan, int64_t n, const T* B, int64_t ldb, T* C, 
   const DevGcoo<T>& a = plan_a<T>(plan);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (a.m == 0 || n == 0) return;
-  const int kind = choose_kind<T>(a, n, ldb, ldc, B, C, plan->flavor, /*small_gate=*/false);
-  if (kind == plan->plan.kind) {
+  // the plan serves this B/C when every kernel it runs takes the layout
+  const SpdmPlan& P = plan->plan;
+  bool usable;
+  if (P.kind == 0) {
+    usable = choose_kind<T>(a, n, ldb, ldc, B, C, plan->flavor, /*small_gate=*/false) == 0;
+  } else {
+    usable = true;
+    for (const SpdmPlan* q = &P; q; q = q->heavy.get())
+      with_cfg<T>(q->kind, [&](auto c) { usable = usable && tile_fits<decltype(c)>(a, n, ldb, ldc, B, C); });
+  }
+  if (usable) {
     run_spdm<T>(plan->plan, a, n, B, ldb, C, ldc, plan->flavor, s);
   } else {  // this B/C layout needs another kernel class: plan it for this call
     launch_spdm<T>(a, n, B, ldb, C, ldc, plan->flavor, s);
@@ -1278,6 +1491,21 @@ int gcoo_debug_kernel_time(double* total_ms, int64_t* launches) {
   });
 }
 
+#if GCOO_PROF
+// Measurement builds only (tools/prof_probe.py): read (and optionally reset) the
+// multiply kernel's cycle accounting (spdm_tacc.cuh g_prof).
+int gcoo_debug_prof(unsigned long long* out, int reset) {
+  return guarded([&] {
+    GCOO_CUDA(cudaDeviceSynchronize());
+    GCOO_CUDA(cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 12));
+    if (reset) {
+      const unsigned long long z[12] = {};
+      GCOO_CUDA(cudaMemcpyToSymbol(g_prof, z, sizeof(z)));
+    }
+  });
+}
+#endif
+
 // Tuning hook (not in the public header): column strips of the host pipeline.
 int gcoo_debug_pipeline_strips(int strips) {
   g_pipeline_strips.store(strips, std::memory_order_relaxed);
@@ -1286,8 +1514,18 @@ int gcoo_debug_pipeline_strips(int strips) {
 
 // Test/benchmark hook (not in the public header): pin the fp32 kernel choice.
 // Test hook (not in the public header): the kernel id this thread's latest
-// multiply ran (0 row-tile, else a TMEM configuration; -1 none yet).
+// multiply ran (0 row-tile, else a TMEM configuration; -1 none yet; a
+// two-class split reports its light rows' configuration, see
+// gcoo_debug_last_split).
 int gcoo_debug_last_kernel(void) { return t_last_kind; }
+int gcoo_debug_last_split(void) { return t_last_split ? 1 : 0; }
+
+// Test hook: the two-class split of skewed matrices (-1 auto, 0 never, 1
+// whenever the degree distribution has two classes).
+int gcoo_debug_force_split(int mode) {
+  g_force_split.store(mode, std::memory_order_relaxed);
+  return GCOO_OK;
+}
 
 int gcoo_debug_force_kernel(int which) {
   g_force_kernel.store(which, std::memory_order_relaxed);

@@ -438,6 +438,75 @@ __global__ void row_balance_kernel(int64_t m, const int32_t* __restrict__ row_nn
   }
 }
 
+// ------------------------------------------- two-class split (skewed A) --
+// Degree statistics for the host's split decision (capi.cu skew_hint):
+// out[0] the largest row, out[1+b] rows and out[34+b] entries in log2 bucket b
+// (b = 0: the heaviest bucket, 31 - floor(log2(nnz)); empty rows in bucket 32).
+__global__ void skew_probe_kernel(int64_t m, const int32_t* __restrict__ row_nnz, unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long cnt[33], sum[33];
+  __shared__ int32_t mx;
+  if (threadIdx.x < 33) cnt[threadIdx.x] = sum[threadIdx.x] = 0;
+  if (threadIdx.x == 0) mx = 0;
+  __syncthreads();
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = row_nnz[r];
+    const int b = nnz_bucket(c) + 1;
+    atomicAdd(&cnt[b - 1], 1ull);
+    atomicAdd(&sum[b - 1], (unsigned long long)c);
+    atomicMax(&mx, c);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&out[0], (unsigned long long)mx);
+  if (threadIdx.x < 33) {
+    if (cnt[threadIdx.x]) atomicAdd(&out[1 + threadIdx.x], cnt[threadIdx.x]);
+    if (sum[threadIdx.x]) atomicAdd(&out[34 + threadIdx.x], sum[threadIdx.x]);
+  }
+}
+
+// Heaviest-first position of every row (log2-bucket counting sort, order
+// inside a bucket arbitrary: C does not depend on where a row is computed).
+__global__ void rank_rows_kernel(int64_t m, const int32_t* __restrict__ row_nnz, const int32_t* __restrict__ hist,
+                                 int32_t* __restrict__ cursor, int32_t* __restrict__ pos) {
+  griddep_wait();  // PDL: predecessor complete
+  __shared__ int32_t off[33];
+  if (threadIdx.x == 0) {
+    int32_t acc = 0;
+    for (int b = 1; b < 33; ++b) {
+      off[b] = acc;
+      acc += hist[b];
+    }
+  }
+  __syncthreads();
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    const int b = nnz_bucket(row_nnz[r]) + 1;
+    pos[r] = off[b] + atomicAdd(&cursor[b], 1);
+  }
+}
+
+// One class of a two-class split: rows at heaviest-first positions [lo, hi)
+// are placed into this plan's units as row_balance_kernel does (block i/rpb,
+// dealt over its warps); every other row gets unit -1 (the other plan's).
+// Row block 0 holds the class's heaviest rows and its CTAs launch first
+// (*skew_flag), so they never start late and form a tail.
+__global__ void place_class_kernel(int64_t m, const int32_t* __restrict__ pos, int64_t lo, int64_t hi,
+                                   int32_t rb_rows, int32_t nw, int32_t rw, int32_t rpb,
+                                   int32_t* __restrict__ unit_of, int32_t* __restrict__ row_of,
+                                   int32_t* __restrict__ skew_flag) {
+  griddep_wait();  // PDL: predecessor complete
+  if (blockIdx.x == 0 && threadIdx.x == 0) *skew_flag = 1;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = pos[r];
+    if (p < lo || p >= hi) {
+      unit_of[r] = -1;
+      continue;
+    }
+    const int64_t i = p - lo, blk = i / rpb, j = i % rpb;
+    const int64_t u = blk * rb_rows + (j % nw) * rw + j / nw;
+    unit_of[r] = (int32_t)u;
+    row_of[u] = (int32_t)r;
+  }
+}
+
 }  // namespace gcoo_b200
 
 namespace gcoo_b200 {

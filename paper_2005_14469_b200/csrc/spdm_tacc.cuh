@@ -119,6 +119,7 @@ __global__ void tacc_count_kernel(int64_t nnz, const int32_t* __restrict__ rows,
   griddep_wait();  // PDL: predecessor complete
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
     const int32_t r = unit_of[rows[e]];
+    if (r < 0) continue;  // row of another class's plan (two-class split)
     const int32_t c = cols[e] / Cfg::KC;
     atomicAdd(&cnt[((int64_t)(r / Cfg::RW) * nchunks + c) * Cfg::RW + (r % Cfg::RW)], 1u);
   }
@@ -212,6 +213,8 @@ __global__ void tacc_fill_kernel(int64_t nnz, int32_t p, const typename Cfg::E* 
   griddep_wait();  // PDL: predecessor complete
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
     const int32_t r = rows[e], col = cols[e];
+    const int32_t ur = unit_of[r];
+    if (ur < 0) continue;  // row of another class's plan (two-class split)
     const int c = col / Cfg::KC;
     const int32_t lo_col = c * Cfg::KC;
     const int64_t glo = gidx[r / p];
@@ -220,7 +223,6 @@ __global__ void tacc_fill_kernel(int64_t nnz, int32_t p, const typename Cfg::E* 
       if (cols[j] < lo_col) break;
       rank += rows[j] == r;
     }
-    const int32_t ur = unit_of[r];
     const int64_t u = ur / Cfg::RW;
     const int64_t rb = u / Cfg::NW;
     const int w = (int)(u % Cfg::NW);
@@ -264,6 +266,24 @@ struct RecSrc<true> {  // segment larger than a stage: read from global memory
 #ifndef GCOO_ABL
 #define GCOO_ABL 0  // ablation builds (tools/ablate.sh, wrong results): 1 no TMEM swap, 2 no B loads, 3 both
 #endif
+#ifndef GCOO_PRODUCER_HINT_NS
+#define GCOO_PRODUCER_HINT_NS 0  // suspend-time hint of the producer's stage-release wait (0: spin)
+#endif
+#ifndef GCOO_PROF
+#define GCOO_PROF 0  // measurement builds (tools/prof_probe.py): per-warp cycle accounting into g_prof
+#endif
+#if GCOO_PROF
+// [0] consumer cycles in full-barrier waits, [1] consumer cycles chunk loop total, [2] consumer
+// epilogue cycles, [3] producer cycles in empty-barrier waits, [4] producer loop cycles,
+// [5] consumer warps, [6] records consumed, [7] TMEM swaps, [8] loop cycles of heavy row-block
+// warps (skewed placement, row block 0), [9] their count, [10] max loop cycles of any warp
+__device__ unsigned long long g_prof[12];
+// per-warp event counters in shared memory (lane 0 bumps them: no global atomics in the loop)
+__shared__ unsigned g_prof_swaps[32], g_prof_recs[32];
+#define GCOO_PROF_ADD(i, v) atomicAdd(&g_prof[i], (unsigned long long)(v))
+#else
+#define GCOO_PROF_ADD(i, v) ((void)0)
+#endif
 
 // `cur` always names a slot whose TMEM copy the registers may overwrite: it
 // starts at slot 0 with zero accumulators (slot 0's TMEM is zero too), so the
@@ -275,6 +295,9 @@ __device__ __forceinline__ void tacc_switch(float (&acc)[Cfg::V], uint32_t& cur,
     return;
   }
   if (s != cur) {  // warp-uniform: swap the slot's accumulators through TMEM
+#if GCOO_PROF
+    if ((threadIdx.x & 31) == 0) ++g_prof_swaps[threadIdx.x >> 5];
+#endif
     tmem_st<Cfg::V>(tacc + cur * Cfg::V, acc);
     tmem_ld<Cfg::V>(tacc + s * Cfg::V, acc);
     tmem_wait_ld();
@@ -402,6 +425,9 @@ __device__ __forceinline__ void tacc_consume(float (&acc)[Cfg::V], uint32_t& cur
   const uint32_t woff = Src::ld32(seg + 4 * warp);
   const auto wseg = seg + woff;
   const uint32_t nrec = Src::ld32(wseg);
+#if GCOO_PROF
+  if ((threadIdx.x & 31) == 0) g_prof_recs[threadIdx.x >> 5] += nrec;
+#endif
   auto rec = wseg + Cfg::HDR;
   for (uint32_t r = 1; r < nrec; r += 2, rec += 2 * Cfg::REC) {
     const uint4 qa = Src::ld(rec);
@@ -488,6 +514,10 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
     if (lane == 0) {
       const int32_t x = (int32_t)(ct * W);
       int64_t lo = so[0], hi = so[1];
+#if GCOO_PROF
+      const long long p0 = clock64();
+      long long pw = 0;
+#endif
       for (int c = 0; c < nchunks; ++c) {
         const int s = c % S;
         const int64_t hi_next = so[c + 2 <= nchunks ? c + 2 : nchunks];  // prefetch
@@ -495,7 +525,19 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
         const uint32_t bytes = len <= Cfg::CAP ? len : 0u;  // oversize: consumers read global memory
         // a segment of empty warp headers only: no consumer reads this chunk's B tile
         const bool any = len > (uint32_t)(Cfg::TABLE + Cfg::NW * Cfg::HDR);
-        if (c >= S) mbar_wait(&empty[s], (uint32_t)((c / S) - 1) & 1u);
+#if GCOO_PROF
+        const long long w0 = clock64();
+#endif
+        if (c >= S) {
+#if GCOO_PRODUCER_HINT_NS
+          mbar_wait_sleep(&empty[s], (uint32_t)((c / S) - 1) & 1u, GCOO_PRODUCER_HINT_NS);
+#else
+          mbar_wait(&empty[s], (uint32_t)((c / S) - 1) & 1u);
+#endif
+        }
+#if GCOO_PROF
+        pw += clock64() - w0;
+#endif
         unsigned char* stage = smem_raw + (size_t)s * Cfg::STAGE_BYTES;
         stage_lo[s] = lo;
         stage_len[s] = len;
@@ -505,6 +547,10 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
         lo = hi;
         hi = hi_next;
       }
+#if GCOO_PROF
+      GCOO_PROF_ADD(3, pw);
+      GCOO_PROF_ADD(4, clock64() - p0);
+#endif
     }
     return;
   }
@@ -520,10 +566,22 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
 #pragma unroll
   for (int v = 0; v < V; ++v) acc[v] = 0.f;
   uint32_t cur = 0;  // slot 0, zero accumulators (see tacc_switch)
+#if GCOO_PROF
+  if (lane == 0) g_prof_swaps[warp] = g_prof_recs[warp] = 0;
+  __syncwarp();
+  const long long q0 = clock64();
+  long long qw = 0;
+#endif
 
   for (int c = 0; c < nchunks; ++c) {
     const int s_idx = c % S;
+#if GCOO_PROF
+    const long long w0 = clock64();
     mbar_wait(&full[s_idx], (uint32_t)(c / S) & 1u);
+    qw += clock64() - w0;
+#else
+    mbar_wait(&full[s_idx], (uint32_t)(c / S) & 1u);
+#endif
     tmem_wait_st();  // slots pushed during earlier chunks are complete before they are pulled again
     const uint32_t stage = smem0 + (uint32_t)s_idx * Cfg::STAGE_BYTES;
     const uint32_t bbase = stage + (uint32_t)(lane * V * 4);
@@ -548,6 +606,9 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
   }
   tmem_st<V>(tacc + cur * V, acc);
   tmem_wait_st();
+#if GCOO_PROF
+  const long long q1 = clock64();
+#endif
 
   // read back and single write of the tile: slot s, value v at column s*V + v
   const int64_t row0 = (rb * NW + warp) * (int64_t)RW;
@@ -575,6 +636,21 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
     }
   }
 
+#if GCOO_PROF
+  if (lane == 0) {
+    GCOO_PROF_ADD(0, qw);
+    GCOO_PROF_ADD(1, q1 - q0);
+    GCOO_PROF_ADD(2, clock64() - q1);
+    GCOO_PROF_ADD(5, 1);
+    GCOO_PROF_ADD(6, g_prof_recs[warp]);
+    GCOO_PROF_ADD(7, g_prof_swaps[warp]);
+    if (*skewed && rb == 0) {
+      GCOO_PROF_ADD(8, q1 - q0);
+      GCOO_PROF_ADD(9, 1);
+    }
+    atomicMax(&g_prof[10], (unsigned long long)(q1 - q0));
+  }
+#endif
   // free TMEM once every consumer warp is done with it
   tmem_fence_before();
   named_bar_sync(1, NW * 32);

@@ -733,3 +733,65 @@ def test_traffic_model_device_random_shapes(gcoo, cuda, oracle):
     with pytest.raises(ValueError):
         gcoo.model_traffic_dev(dg, 10, gcoo.ExecConfig(p=16, b=3))
 
+
+
+@pytest.mark.parametrize("p", [1, 4, 16])
+def test_two_class_split_bit_exact(gcoo, cuda, oracle, p):
+    """Skewed A (a few dense rows among sparse ones): the heavy rows and the
+    light rows run as two plans with their own configurations, concurrently;
+    C equals the oracle bit for bit through the device call, a reused plan and
+    the pipelined host call, and the split is taken automatically."""
+    import torch
+    rng = np.random.default_rng(90 + p)
+    m, k, n = 3000, 4000, 4096  # well above the small-product gate: the TMEM kernels run
+    a = rand_dense(rng, m, k, 0.004)
+    for r in rng.choice(m, 12, replace=False):  # dense and half-dense rows
+        a[r] = np.where(rng.random(k) < (1.0 if r % 2 else 0.5), 1.0 - rng.random(k), 0.0)
+    bm = rand_dense(rng, k, n, 1.0)
+    go = oracle.dense_to_gcoo(a, p)
+    c_ref, _ = oracle.spdm(go, bm, 64, fma=True)
+    dg = gcoo.DeviceGcoo.from_host(to_prod(gcoo, go))
+    bt = torch.from_numpy(bm).cuda()
+    ct = torch.empty((m, n), device="cuda")
+    for mode in ("auto", "always", "never"):
+        gcoo.force_split(mode)
+        try:
+            ct.fill_(float("nan"))
+            gcoo.spdm_gcoo_dev(dg, bt, ct, gcoo.ExecConfig(p=p))
+            torch.cuda.synchronize()
+            split = gcoo.last_split()
+        finally:
+            gcoo.force_split("auto")
+        assert split == (mode != "never"), mode
+        assert np.array_equal(ct.cpu().numpy(), c_ref), mode
+    plan = gcoo.SpdmPlan(dg)
+    ct.fill_(float("nan"))
+    l0 = gcoo.launch_count()
+    plan.run(bt, ct)
+    torch.cuda.synchronize()
+    assert gcoo.last_split() and gcoo.launch_count() - l0 == 2  # heavy + light multiply, nothing else
+    assert np.array_equal(ct.cpu().numpy(), c_ref)
+    plan.close()
+    assert np.array_equal(gcoo.spdm_gcoo(to_prod(gcoo, go), bm, gcoo.ExecConfig(p=p)), c_ref)
+
+
+def test_two_class_split_powerlaw_full_rows(gcoo, cuda, oracle):
+    """The power-law generator's matrix (n=4096) splits automatically; sampled
+    rows including the heaviest are bit-exact against the oracle."""
+    import torch
+    n = 4096
+    v, r, c = gcoo.generate_powerlaw_coo(n, 0.99, 1.0, 3)
+    dg = gcoo.coo_to_gcoo_dev(n, n, torch.from_numpy(v).cuda(), torch.from_numpy(r).cuda(),
+                              torch.from_numpy(c).cuda(), 4)
+    bm = oracle.uniform_sparse(n, 0.0, 14)[:, :2048].copy()  # 0.7 GFLOP: above the small-product gate
+    ct = torch.empty((n, 2048), device="cuda")
+    gcoo.spdm_gcoo_dev(dg, torch.from_numpy(bm).cuda(), ct)
+    torch.cuda.synchronize()
+    assert gcoo.last_split()
+    go = oracle.coo_to_gcoo(n, n, v, r, c, 4)
+    counts = np.bincount(r, minlength=n)
+    rows = np.unique(np.concatenate([np.argsort(-counts)[:20], np.random.default_rng(2).choice(n, 40, replace=False)]))
+    got = ct.cpu().numpy()
+    for r0 in rows:
+        want = oracle.spdm_rows(go, bm, int(r0), int(r0) + 1, fma=True)[r0]
+        assert got[r0].tobytes() == want.tobytes(), r0
