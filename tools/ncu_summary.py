@@ -21,7 +21,31 @@ def page(rep, name, extra=()):
 def main():
     rep = sys.argv[1]
     rows = page(rep, "raw")
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    if len(rows) > 3:  # several profiled launches (e.g. a two-class split): raw metrics of each
+        outs = [summarise(rows[0], rows[1], r) for r in rows[2:]]
+        tot = {k: sum(o[k] or 0 for o in outs) for k in ("duration_s", "dram_read_bytes", "dram_write_bytes",
+                                                          "l2_read_bytes_from_sm", "smem_wavefronts", "inst_executed")}
+        print(json.dumps({"launches": outs, "sum": tot}, indent=1))
+        return
+    out = summarise(rows[0], rows[1], rows[2])
+    src = page(rep, "source", ["--print-source", "sass"])
+    h = src[1]
+    data = src[2:]
+    scols = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
+    tot = {c: sum(float(r[h.index(c)] or 0) for r in data) for c in scols}
+    T = sum(tot.values()) or 1
+    out["stalls_pct"] = {c[6:]: round(v / T * 100, 1) for c, v in sorted(tot.items(), key=lambda x: -x[1]) if v / T > 0.005}
+    iE = h.index("Instructions Executed")
+    mix = Counter()
+    for r in data:
+        t = r[1].split()
+        op = (t[1] if t[0].startswith("@") else t[0]).split(".")[0]
+        mix[op] += float(r[iE] or 0)
+    out["inst_mix_M"] = {k: round(v / 1e6, 1) for k, v in mix.most_common(14)}
+    print(json.dumps(out, indent=1))
+
+
+def summarise(hdr, units, vals):
     raw = {h: (vals[i], units[i]) for i, h in enumerate(hdr)}
 
     def num(k):
@@ -49,21 +73,7 @@ def main():
         "sm_clock_hz": num("sm__cycles_elapsed.avg.per_second"),
         "registers": num("launch__registers_per_thread"),
     }
-    src = page(rep, "source", ["--print-source", "sass"])
-    h = src[1]
-    data = src[2:]
-    scols = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
-    tot = {c: sum(float(r[h.index(c)] or 0) for r in data) for c in scols}
-    T = sum(tot.values()) or 1
-    out["stalls_pct"] = {c[6:]: round(v / T * 100, 1) for c, v in sorted(tot.items(), key=lambda x: -x[1]) if v / T > 0.005}
-    iE = h.index("Instructions Executed")
-    mix = Counter()
-    for r in data:
-        t = r[1].split()
-        op = (t[1] if t[0].startswith("@") else t[0]).split(".")[0]
-        mix[op] += float(r[iE] or 0)
-    out["inst_mix_M"] = {k: round(v / 1e6, 1) for k, v in mix.most_common(14)}
-    print(json.dumps(out, indent=1))
+    return out
 
 
 if __name__ == "__main__":
