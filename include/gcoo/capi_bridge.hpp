@@ -91,4 +91,13 @@ inline int gemm_dense(std::int64_t m, std::int64_t k, std::int64_t n, const doub
   return gcoo_gemm_dense_f64(m, k, n, A, B, C);
 }
 
+inline int spdm_auto(std::int64_t m, std::int64_t k, std::int64_t n, std::int32_t p, std::int32_t b, const float* A,
+                     const float* B, float* C, gcoo_stats* st, double* eo, double* kc) {
+  return gcoo_spdm_auto_f32(m, k, n, p, b, A, B, C, st, eo, kc);
+}
+inline int spdm_auto(std::int64_t m, std::int64_t k, std::int64_t n, std::int32_t p, std::int32_t b, const double* A,
+                     const double* B, double* C, gcoo_stats* st, double* eo, double* kc) {
+  return gcoo_spdm_auto_f64(m, k, n, p, b, A, B, C, st, eo, kc);
+}
+
 }  // namespace gcoo::capi

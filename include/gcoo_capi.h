@@ -238,6 +238,17 @@ int gcoo_dense_to_gcoo_f32(int64_t m, int64_t k, int32_t p, const float* A, int6
 int gcoo_dense_to_gcoo_f64(int64_t m, int64_t k, int32_t p, const double* A, int64_t capacity,
                            double* out_values, int32_t* out_row_idx, int32_t* out_col_idx,
                            int64_t* g_idxes, int64_t* nnz_per_group, int64_t* nnz);
+/*
+ * spdm_gcoo_auto (kernels.hpp:353-367) with the GCOO kept on the device: A
+ * (m x k, host) is grouped on the GPU and multiplied by B (k x n, host) into C
+ * (m x n, host) without the GCOO arrays crossing PCIe.  eo_seconds /
+ * kc_seconds (nullable) receive the wall-clock phases (EO: A up + grouping;
+ * KC: B up + multiply + C down), stats (nullable) the KernelStats for b.
+ */
+int gcoo_spdm_auto_f32(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, const float* A, const float* B,
+                       float* C, gcoo_stats* stats, double* eo_seconds, double* kc_seconds);
+int gcoo_spdm_auto_f64(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, const double* A, const double* B,
+                       double* C, gcoo_stats* stats, double* eo_seconds, double* kc_seconds);
 /* Device variant: counts into g_idxes/nnz_per_group (device, ceil(m/p)),
  * returns *nnz (host; synchronises), and fills the entry arrays when
  * capacity >= *nnz (otherwise leaves them untouched and returns GCOO_OK so

@@ -32,7 +32,6 @@ from __future__ import annotations
 
 import ctypes as C
 import os
-import time
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -78,6 +77,9 @@ def lib():
                  C.POINTER(_Stats), _vp, _i64]
     _sig(L, "gcoo_spdm_f32", _int, spdm_args)
     _sig(L, "gcoo_spdm_f64", _int, spdm_args)
+    for t in ("f32", "f64"):
+        _sig(L, f"gcoo_spdm_auto_{t}", _int, [_i64, _i64, _i64, _i32, _i32, _vp, _vp, _vp, C.POINTER(_Stats),
+                                                C.POINTER(_dbl), C.POINTER(_dbl)])
     dev_args = [_i64, _i64, _i64, _i32, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _i64,
                 C.POINTER(_Stats), _int, _vp]
     _sig(L, "gcoo_spdm_f32_dev", _int, dev_args)
@@ -123,6 +125,7 @@ def lib():
     _sig(L, "gcoo_plan_destroy", _int, [_vp])
     _sig(L, "gcoo_debug_kernel_timing", _int, [_int])
     _sig(L, "gcoo_debug_pipeline_strips", _int, [_int])
+    _sig(L, "gcoo_debug_host_staging", _int, [_int])
     _sig(L, "gcoo_debug_kernel_time", _int, [C.POINTER(_dbl), C.POINTER(_i64)])
     _lib = L
     return L
@@ -171,6 +174,12 @@ def last_kernel() -> str:
     """Test hook: the multiply kernel this thread's latest call ran (a KERNELS name)."""
     k = int(lib().gcoo_debug_last_kernel())
     return next((name for name, v in KERNELS.items() if v == k and name != "auto"), str(k))
+
+
+def host_staging(on: bool = True) -> None:
+    """Test hook: pageable host buffers through the library's pinned staging
+    ring (default) or through the driver's own staging (off)."""
+    lib().gcoo_debug_host_staging(1 if on else 0)
 
 
 def last_split() -> bool:
@@ -423,16 +432,26 @@ def spdm_gcoo(a: GcooMatrix, b: np.ndarray, cfg: Optional[ExecConfig] = None,
 
 def spdm_gcoo_auto(a: np.ndarray, b: np.ndarray, cfg: Optional[ExecConfig] = None,
                    timing: Optional[TimingBreakdown] = None, stats: Optional[KernelStats] = None) -> np.ndarray:
-    """spdm_gcoo_auto (kernels.hpp:353-367): EO = dense_to_gcoo, KC = spdm_gcoo."""
+    """spdm_gcoo_auto (kernels.hpp:353-367): EO = dense_to_gcoo, KC = spdm_gcoo,
+    with the GCOO kept on the device between them (gcoo_spdm_auto_*): only A,
+    B and C cross PCIe."""
     cfg = cfg or ExecConfig()
     cfg.validate()
-    t0 = time.perf_counter()
-    g = dense_to_gcoo(a, cfg.p)
-    t1 = time.perf_counter()
-    c = spdm_gcoo(g, b, cfg, stats=stats)
-    t2 = time.perf_counter()
+    a = _dense_check(a)
+    b = np.ascontiguousarray(b, dtype=a.dtype)
+    if b.ndim != 2 or b.shape[0] != a.shape[1]:
+        raise ValueError("spdm_gcoo: inner dimensions differ")
+    c = np.empty((a.shape[0], b.shape[1]), a.dtype)
+    st, eo, kc = _Stats(), _dbl(0.0), _dbl(0.0)
+    _check(getattr(lib(), f"gcoo_spdm_auto_{_sfx(a.dtype)}")(a.shape[0], a.shape[1], b.shape[1], cfg.p, cfg.b, _p(a),
+                                                             _p(b), _p(c), C.byref(st) if stats is not None else None,
+                                                             C.byref(eo), C.byref(kc)))
     if timing is not None:
-        timing.eo_seconds, timing.kc_seconds = t1 - t0, t2 - t1
+        timing.eo_seconds, timing.kc_seconds = float(eo.value), float(kc.value)
+    if stats is not None:
+        s = KernelStats._from(st)
+        stats.flops, stats.b_loads_total, stats.b_loads_reused, stats.staging_fills = (
+            s.flops, s.b_loads_total, s.b_loads_reused, s.staging_fills)
     return c
 
 

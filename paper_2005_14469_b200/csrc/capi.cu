@@ -10,6 +10,10 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <functional>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -782,9 +786,15 @@ bool host_pageable(const void* p) {
   return at.type == cudaMemoryTypeUnregistered;
 }
 
-int64_t pipeline_strip(int64_t m, int64_t k, int64_t n, bool pageable) {
+// Pageable buffers go through the library's own pinned staging ring instead
+// (staged = true): host threads pack B strips into page-locked buffers and
+// unpack C strips out of them while the DMA engines and the multiply work on
+// neighbouring strips.
+std::atomic<int> g_host_staging{1};  // test hook: 0 = let the driver stage pageable copies
+
+int64_t pipeline_strip(int64_t m, int64_t k, int64_t n, bool pageable, bool staged) {
   const int want = g_pipeline_strips.load(std::memory_order_relaxed);
-  const int strips = pageable ? std::min(want, 4) : want;
+  const int strips = staged ? std::min(want, 16) : pageable ? std::min(want, 4) : want;
   if (strips <= 1 || n < 2048 || (m + k) * n < (int64_t)32 << 20) return 0;  // small: one shot
   int64_t w = ceil_div(ceil_div(n, strips), 128) * 128;
   return std::max<int64_t>(w, 256);
@@ -800,6 +810,114 @@ std::vector<std::pair<int64_t, int64_t>> pipeline_strips(int64_t n, int64_t W) {
   }
   for (; c0 < n; c0 += W) v.emplace_back(c0, std::min<int64_t>(W, n - c0));
   return v;
+}
+
+// ------------------------------------------------ host staging (pageable) --
+// A process-wide pool of host threads for the strip pack/unpack copies (one
+// caller at a time; a pageable memcpy runs at ~1.5 GB/s per thread here, so
+// the copies need many threads to keep up with PCIe).
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool pool;
+    return pool;
+  }
+  // fn(lo, hi) over [0, n) split into one range per worker; returns when all are done
+  void run(int64_t n, const std::function<void(int64_t, int64_t)>& fn) {
+    std::lock_guard<std::mutex> caller(run_mu_);
+    const int nt = (int)std::min<int64_t>((int64_t)workers_.size() + 1, std::max<int64_t>(n, 1));
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      n_ = n;
+      parts_ = nt;
+      next_ = 1;  // part 0 runs on the caller
+      pending_ = nt - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    part(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const unsigned hc = std::thread::hardware_concurrency();
+    const int nt = (int)std::max(1u, std::min(hc ? hc : 4u, 32u)) - 1;
+    for (int i = 0; i < nt; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void part(int i) {
+    const int64_t lo = n_ * i / parts_, hi = n_ * (i + 1) / parts_;
+    if (hi > lo) (*fn_)(lo, hi);
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      int i;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || (gen_ != seen && next_ < parts_); });
+        if (stop_) return;
+        i = next_++;
+        if (next_ >= parts_) seen = gen_;
+      }
+      part(i);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, run_mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int64_t, int64_t)>* fn_ = nullptr;
+  int64_t n_ = 0;
+  int parts_ = 0, next_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+// Page-locked staging buffers kept per thread (grown on demand) so that a
+// pageable caller pays cudaHostAlloc once, not per call.
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void* ensure(size_t want) {
+    if (want > bytes) {
+      if (p) GCOO_CUDA(cudaFreeHost(p));
+      p = nullptr;
+      GCOO_CUDA(cudaHostAlloc(&p, want, cudaHostAllocPortable));
+      bytes = want;
+    }
+    return p;
+  }
+};
+
+// rows x w elements between a strided matrix (leading dimension ld) and a
+// packed staging strip (leading dimension W), on the host pool
+template <typename T>
+void pack_strip(const T* src, int64_t ld, T* dst, int64_t W, int64_t rows, int64_t w) {
+  HostPool::get().run(rows, [&](int64_t r0, int64_t r1) {
+    for (int64_t r = r0; r < r1; ++r) std::memcpy(dst + r * W, src + r * ld, sizeof(T) * (size_t)w);
+  });
+}
+template <typename T>
+void unpack_strip(const T* src, int64_t W, T* dst, int64_t ld, int64_t rows, int64_t w) {
+  HostPool::get().run(rows, [&](int64_t r0, int64_t r1) {
+    for (int64_t r = r0; r < r1; ++r) std::memcpy(dst + r * ld, src + r * W, sizeof(T) * (size_t)w);
+  });
 }
 
 cudaStream_t aux_stream(int which) {
@@ -850,15 +968,23 @@ struct PipeTrace {
   }
 };
 
+// dev_a (nullable): A already resident on the device (spdm_gcoo_auto's fused
+// EO -> KC path); the host GCOO arrays are then not read.
 template <typename T>
 void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int32_t cfg_b, int64_t b_rows,
                int64_t nnz, const T* values, const int32_t* row_idx, const int32_t* col_idx, int64_t groups,
                const int64_t* g_idxes, const int64_t* gnnz, const T* B, T* C, gcoo_stats* stats,
-               const int64_t* tile_order, int64_t tile_count, int flavor) {
+               const int64_t* tile_order, int64_t tile_count, int flavor, const DevGcoo<T>* dev_a = nullptr) {
   validate_spdm(m, k, n, a_p, cfg_p, cfg_b, b_rows, nnz, groups, tile_order, tile_count);
   const bool perm = tile_order ? tile_order_is_permutation(tile_order, tile_count) : true;
   cudaStream_t s = thread_stream();
-  const int64_t W = perm ? pipeline_strip(m, k, n, host_pageable(B) || host_pageable(C)) : 0;
+  const bool page_b = host_pageable(B), page_c = host_pageable(C);
+  const bool staged = (page_b || page_c) && g_host_staging.load(std::memory_order_relaxed) != 0;
+  const int64_t W = perm ? pipeline_strip(m, k, n, page_b || page_c, staged) : 0;
+  // pageable B / C: this thread's pinned staging ring (NBUF strips each)
+  thread_local PinnedBuf stage_b, stage_c;
+  T* hB = (W && staged && page_b) ? static_cast<T*>(stage_b.ensure(sizeof(T) * (size_t)(NBUF * k * W))) : nullptr;
+  T* hC = (W && staged && page_c) ? static_cast<T*>(stage_c.ensure(sizeof(T) * (size_t)(NBUF * m * W))) : nullptr;
   // pipelined path: every buffer first; then A crosses PCIe ahead of B strip 0
   // on the H2D stream (the planner and strip 0's multiply need it first), so
   // the D2H direction can start as early as possible
@@ -868,9 +994,10 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
     dBv.emplace_back(k * W, s);
     dCv.emplace_back(m * W, s);
   }
-  DevBuf<T> d_vals(nnz, s);
-  DevBuf<int32_t> d_rows(nnz, s), d_cols(nnz, s);
-  DevBuf<int64_t> d_gidx(groups, s), d_gnnz(groups, s);
+  const int64_t up = dev_a ? 0 : nnz, up_g = dev_a ? 0 : groups;
+  DevBuf<T> d_vals(up, s);
+  DevBuf<int32_t> d_rows(up, s), d_cols(up, s);
+  DevBuf<int64_t> d_gidx(up_g, s), d_gnnz(up_g, s);
   // events: 0 buffers ready, then per ring slot b: in_done 1+b, cmp_done 1+NBUF+b,
   // out_done 1+2*NBUF+b; 1+3*NBUF: A uploaded
   Events ev(W ? 2 + 3 * NBUF : 0);
@@ -892,23 +1019,40 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
   auto h2d_strip = [&](int64_t j) {
     const int b = (int)(j % NBUF);
     const int64_t c0 = strips[j].first, w = strips[j].second;
-    GCOO_CUDA(cudaMemcpy2DAsync(dBv[b].get(), W * sizeof(T), B + c0, n * sizeof(T), w * sizeof(T), k,
-                                cudaMemcpyHostToDevice, s_in));
+    if (hB) {
+      // staging slot b was last read by strip j-NBUF's H2D copy
+      if (j >= NBUF) GCOO_CUDA(cudaEventSynchronize(in_done(b)));
+      T* st = hB + (size_t)b * k * W;
+      pack_strip<T>(B + c0, n, st, W, k, w);
+      GCOO_CUDA(cudaMemcpy2DAsync(dBv[b].get(), W * sizeof(T), st, W * sizeof(T), w * sizeof(T), k,
+                                  cudaMemcpyHostToDevice, s_in));
+    } else {
+      GCOO_CUDA(cudaMemcpy2DAsync(dBv[b].get(), W * sizeof(T), B + c0, n * sizeof(T), w * sizeof(T), k,
+                                  cudaMemcpyHostToDevice, s_in));
+    }
     GCOO_CUDA(cudaEventRecord(in_done(b), s_in));
     if (trace) trace->mark(s_in, 2, j);
   };
+  // C strip j from its staging slot into the caller's pageable C
+  auto unpack_c = [&](int64_t j) {
+    const int b = (int)(j % NBUF);
+    GCOO_CUDA(cudaEventSynchronize(out_done(b)));
+    unpack_strip<T>(hC + (size_t)b * m * W, W, C + strips[j].first, n, m, strips[j].second);
+  };
   cudaStream_t s_a = W ? s_in : s;
-  h2d(d_vals.get(), values, nnz, s_a);
-  h2d(d_rows.get(), row_idx, nnz, s_a);
-  h2d(d_cols.get(), col_idx, nnz, s_a);
-  h2d(d_gidx.get(), g_idxes, groups, s_a);
-  h2d(d_gnnz.get(), gnnz, groups, s_a);
+  h2d(d_vals.get(), values, up, s_a);
+  h2d(d_rows.get(), row_idx, up, s_a);
+  h2d(d_cols.get(), col_idx, up, s_a);
+  h2d(d_gidx.get(), g_idxes, up_g, s_a);
+  h2d(d_gnnz.get(), gnnz, up_g, s_a);
   if (W) {
     GCOO_CUDA(cudaEventRecord(ev[1 + 3 * NBUF], s_in));
     GCOO_CUDA(cudaStreamWaitEvent(s, ev[1 + 3 * NBUF], 0));
     h2d_strip(0);
   }
-  DevGcoo<T> a{m, k, nnz, groups, a_p, d_vals.get(), d_rows.get(), d_cols.get(), d_gidx.get(), d_gnnz.get()};
+  const DevGcoo<T> a = dev_a ? *dev_a
+                             : DevGcoo<T>{m, k, nnz, groups, a_p, d_vals.get(), d_rows.get(), d_cols.get(),
+                                          d_gidx.get(), d_gnnz.get()};
   if (W == 0) {
     DevBuf<T> d_B(k * n, s), d_C(m * n, s);
     h2d(d_B.get(), B, k * n, s);
@@ -916,7 +1060,7 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
     if (!perm) {
       apply_tile_list<T>(a, n, cfg_b, tile_order, tile_count, d_C.get(), n, stats, s);
     } else if (stats) {
-      device_stats(nnz, n, a_p, cfg_b, groups, d_rows.get(), d_cols.get(), d_gidx.get(), stats, s);
+      device_stats(nnz, n, a_p, cfg_b, groups, a.rows, a.cols, a.gidx, stats, s);
     }
     d2h(C, d_C.get(), m * n, s);
     GCOO_CUDA(cudaStreamSynchronize(s));
@@ -941,12 +1085,18 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
     if (trace) trace->mark(s, 4, j);
     GCOO_CUDA(cudaEventRecord(cmp_done(b), s));
     GCOO_CUDA(cudaStreamWaitEvent(s_out, cmp_done(b), 0));
-    GCOO_CUDA(cudaMemcpy2DAsync(C + c0, n * sizeof(T), dCv[b].get(), W * sizeof(T), w * sizeof(T), m,
-                                cudaMemcpyDeviceToHost, s_out));
+    if (hC)  // staging slot b was emptied by unpack_c(j - NBUF) in an earlier iteration
+      GCOO_CUDA(cudaMemcpy2DAsync(hC + (size_t)b * m * W, W * sizeof(T), dCv[b].get(), W * sizeof(T),
+                                  w * sizeof(T), m, cudaMemcpyDeviceToHost, s_out));
+    else
+      GCOO_CUDA(cudaMemcpy2DAsync(C + c0, n * sizeof(T), dCv[b].get(), W * sizeof(T), w * sizeof(T), m,
+                                  cudaMemcpyDeviceToHost, s_out));
     GCOO_CUDA(cudaEventRecord(out_done(b), s_out));
     if (trace) trace->mark(s_out, 5, j);
+    if (hC && j >= 1) unpack_c(j - 1);  // overlaps strip j's copies and multiply
   }
-  if (stats) device_stats(nnz, n, a_p, cfg_b, groups, d_rows.get(), d_cols.get(), d_gidx.get(), stats, s);
+  if (hC && nstrips > 0) unpack_c(nstrips - 1);
+  if (stats) device_stats(nnz, n, a_p, cfg_b, groups, a.rows, a.cols, a.gidx, stats, s);
   if (trace) trace->dump(nstrips);
   // the strip buffers are freed (stream-ordered on s) only after the last copy-outs
   for (int64_t j = std::max<int64_t>(0, nstrips - NBUF); j < nstrips; ++j)
@@ -1429,6 +1579,38 @@ void gemm_dense_host(int64_t m, int64_t k, int64_t n, const T* A, const T* B, T*
   GCOO_CUDA(cudaStreamSynchronize(s));
 }
 
+// spdm_gcoo_auto (kernels.hpp:353-367) with the GCOO kept on the device: EO
+// = A up + count + fill, KC = the host-pointer multiply from the resident
+// GCOO (B up, C down) — the GCOO never crosses PCIe, unlike the reference's
+// two calls through host GcooMatrix arrays.  Host wall-clock phases.
+template <typename T>
+void spdm_auto_host(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, const T* A, const T* B, T* C,
+                    gcoo_stats* stats, double* eo_s, double* kc_s) {
+  if (!is_pow2(p) || !is_pow2(b)) einval("ExecConfig: p and b must be powers of two");
+  using clock = std::chrono::steady_clock;
+  const auto t0 = clock::now();
+  cudaStream_t s = thread_stream();
+  if (m < 1 || k < 1) einval("DenseMatrix: dimensions must be >= 1");
+  const int64_t groups = ceil_div(m, p);
+  DevBuf<T> dA(m * k, s);
+  h2d(dA.get(), A, m * k, s);
+  DevBuf<int64_t> dgi(groups, s), dgn(groups, s);
+  const int64_t nnz = dense_to_gcoo_device<T>(m, k, p, dA.get(), 0, nullptr, nullptr, nullptr, dgi.get(),
+                                              dgn.get(), s);
+  DevBuf<T> dv(nnz, s);
+  DevBuf<int32_t> dr(nnz, s), dc(nnz, s);
+  dense_to_gcoo_device<T>(m, k, p, dA.get(), nnz, dv.get(), dr.get(), dc.get(), dgi.get(), dgn.get(), s);
+  dA.release();
+  GCOO_CUDA(cudaStreamSynchronize(s));
+  const auto t1 = clock::now();
+  const DevGcoo<T> a{m, k, nnz, groups, p, dv.get(), dr.get(), dc.get(), dgi.get(), dgn.get()};
+  spdm_host<T>(m, k, n, p, p, b, k, nnz, nullptr, nullptr, nullptr, groups, nullptr, nullptr, B, C, stats, nullptr,
+               0, GCOO_FLAVOR_FMA, &a);
+  const auto t2 = clock::now();
+  if (eo_s) *eo_s = std::chrono::duration<double>(t1 - t0).count();
+  if (kc_s) *kc_s = std::chrono::duration<double>(t2 - t1).count();
+}
+
 }  // namespace gcoo_b200
 
 // =================================================================== C ABI =
@@ -1505,6 +1687,14 @@ int gcoo_debug_prof(unsigned long long* out, int reset) {
   });
 }
 #endif
+
+// Test hook (not in the public header): 0 sends pageable host buffers through
+// the driver's own staging (the pre-ring behaviour), 1 (default) through the
+// library's pinned staging ring.
+int gcoo_debug_host_staging(int on) {
+  g_host_staging.store(on, std::memory_order_relaxed);
+  return GCOO_OK;
+}
 
 // Tuning hook (not in the public header): column strips of the host pipeline.
 int gcoo_debug_pipeline_strips(int strips) {
@@ -1770,6 +1960,16 @@ int gcoo_dense_to_gcoo_f32_dev(int64_t m, int64_t k, int32_t p, const float* A, 
     *nnz = dense_to_gcoo_device<float>(m, k, p, A, capacity, out_values, out_row_idx, out_col_idx, g_idxes,
                                        nnz_per_group, static_cast<cudaStream_t>(stream));
   });
+}
+
+int gcoo_spdm_auto_f32(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, const float* A, const float* B,
+                       float* C, gcoo_stats* stats, double* eo_seconds, double* kc_seconds) {
+  return guarded([&] { spdm_auto_host<float>(m, k, n, p, b, A, B, C, stats, eo_seconds, kc_seconds); });
+}
+
+int gcoo_spdm_auto_f64(int64_t m, int64_t k, int64_t n, int32_t p, int32_t b, const double* A, const double* B,
+                       double* C, gcoo_stats* stats, double* eo_seconds, double* kc_seconds) {
+  return guarded([&] { spdm_auto_host<double>(m, k, n, p, b, A, B, C, stats, eo_seconds, kc_seconds); });
 }
 
 int gcoo_dense_to_gcoo_f64_dev(int64_t m, int64_t k, int32_t p, const double* A, int64_t capacity,

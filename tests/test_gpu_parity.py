@@ -591,6 +591,35 @@ def test_host_pipeline_strips_bitwise_equal(gcoo, cuda, oracle, n):
     assert st.flops == 2 * g.nnz() * n
 
 
+def test_host_staging_ring_pageable_and_pinned(gcoo, cuda, oracle):
+    """The host-pointer path with pageable buffers packs B strips into and
+    unpacks C strips out of a pinned staging ring on host threads; pinned
+    buffers skip it; the driver-staged path remains as a switch.  All three
+    give the same bits, for a ragged last strip too."""
+    import torch
+    rng = np.random.default_rng(77)
+    m, k, n = 6000, 7000, 3001
+    a = rand_dense(rng, m, k, 0.005)
+    bm = (1.0 - rng.random((k, n))).astype(np.float32)
+    g = gcoo.dense_to_gcoo(a, 4)
+    c_ring = gcoo.spdm_gcoo(g, bm)
+    gcoo.host_staging(False)
+    try:
+        c_driver = gcoo.spdm_gcoo(g, bm)
+    finally:
+        gcoo.host_staging(True)
+    b_pin = torch.empty((k, n), dtype=torch.float32, pin_memory=True)
+    b_pin.numpy()[:] = bm
+    c_pin = torch.empty((m, n), dtype=torch.float32, pin_memory=True)
+    gcoo.spdm_gcoo(g, b_pin.numpy(), out=c_pin.numpy())
+    assert np.array_equal(c_ring, c_driver) and np.array_equal(c_ring, c_pin.numpy())
+    rows = np.random.default_rng(3).choice(m, 24, replace=False)
+    go = oracle.dense_to_gcoo(a, 4)
+    for r0 in rows:
+        want = oracle.spdm_rows(go, bm, int(r0), int(r0) + 1, fma=True)[r0]
+        assert c_ring[r0].tobytes() == want.tobytes()
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("case", ["powerlaw_n16384", "uniform_n32768"])
 def test_large_configs_sampled_rows_bit_exact(gcoo, cuda, oracle, case):
@@ -795,3 +824,24 @@ def test_two_class_split_powerlaw_full_rows(gcoo, cuda, oracle):
     for r0 in rows:
         want = oracle.spdm_rows(go, bm, int(r0), int(r0) + 1, fma=True)[r0]
         assert got[r0].tobytes() == want.tobytes(), r0
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_spdm_gcoo_auto_device_resident(gcoo, cuda, oracle, dtype):
+    """spdm_gcoo_auto keeps the GCOO on the device between EO and KC: C and
+    KernelStats equal the two-call path bit for bit, both phases are timed,
+    and the pipelined size works from the resident GCOO too."""
+    rng = np.random.default_rng(31)
+    for m, k, n in [(300, 257, 129), (5000, 6000, 2304)]:
+        a = rand_dense(rng, m, k, 0.01, dtype)
+        bm = rand_dense(rng, k, n, 1.0, dtype)
+        tb = gcoo.TimingBreakdown()
+        st = gcoo.KernelStats()
+        c = gcoo.spdm_gcoo_auto(a, bm, gcoo.ExecConfig(), tb, st)
+        st2 = gcoo.KernelStats()
+        c2 = gcoo.spdm_gcoo(gcoo.dense_to_gcoo(a, 4), bm, gcoo.ExecConfig(), stats=st2)
+        assert np.array_equal(c, c2), (m, k, n)
+        assert st == st2
+        assert tb.eo_seconds > 0 and tb.kc_seconds > 0
+    with pytest.raises(ValueError):
+        gcoo.spdm_gcoo_auto(a, bm[:-1], gcoo.ExecConfig(), gcoo.TimingBreakdown())
