@@ -486,14 +486,14 @@ __global__ void rank_rows_kernel(int64_t m, const int32_t* __restrict__ row_nnz,
 // One class of a two-class split: rows at heaviest-first positions [lo, hi)
 // are placed into this plan's units as row_balance_kernel does (block i/rpb,
 // dealt over its warps); every other row gets unit -1 (the other plan's).
-// Row block 0 holds the class's heaviest rows and its CTAs launch first
-// (*skew_flag), so they never start late and form a tail.
+// Row block 0 holds the class's heaviest rows; `first` = 1 launches its CTAs
+// first (*skew_flag), so they never start late and form a tail.
 __global__ void place_class_kernel(int64_t m, const int32_t* __restrict__ pos, int64_t lo, int64_t hi,
                                    int32_t rb_rows, int32_t nw, int32_t rw, int32_t rpb,
                                    int32_t* __restrict__ unit_of, int32_t* __restrict__ row_of,
-                                   int32_t* __restrict__ skew_flag) {
+                                   int32_t* __restrict__ skew_flag, int32_t first) {
   griddep_wait();  // PDL: predecessor complete
-  if (blockIdx.x == 0 && threadIdx.x == 0) *skew_flag = 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *skew_flag = first;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = pos[r];
     if (p < lo || p >= hi) {

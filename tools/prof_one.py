@@ -18,7 +18,7 @@ ap.add_argument("--kernel", default="auto")
 ap.add_argument("--launches", type=int, default=2)
 ap.add_argument("--powerlaw", action="store_true")
 args = ap.parse_args()
-n = args.n
+n = args.n if not (args.powerlaw and args.n == 8000) else 16384  # configs[3] is n=16384
 if args.powerlaw:
     v, r, c = G.generate_powerlaw_coo(n, args.s, 1.0, 1)
     d = G.coo_to_gcoo_dev(n, n, torch.from_numpy(v).cuda(), torch.from_numpy(r).cuda(), torch.from_numpy(c).cuda(), 4)

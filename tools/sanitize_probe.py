@@ -42,13 +42,14 @@ def main():
         perm = rng.permutation(r.size)
         G.spdm_coo(m, k, v[perm], r[perm], cc[perm], b)
         G.gemm_dense_blocked(a[:200, :300].copy(), b[:300, :100].copy())
-    # two-class split
-    a = np.where(rng.random((m, k)) < 0.004, 1 - rng.random((m, k)), 0).astype(np.float32)
-    a[::97] = (1 - rng.random((len(a[::97]), k))).astype(np.float32)
-    b = (1 - rng.random((k, 4096))).astype(np.float32)
+    # two-class split (above the small-product gate, so the TMEM kernels run)
+    ms, ks = 2000, 2000
+    a = np.where(rng.random((ms, ks)) < 0.004, 1 - rng.random((ms, ks)), 0).astype(np.float32)
+    a[::97] = (1 - rng.random((len(a[::97]), ks))).astype(np.float32)
+    b = (1 - rng.random((ks, 4096))).astype(np.float32)
     d = G.dense_to_gcoo_dev(torch.from_numpy(a).to(dev), 4)
-    c1 = torch.empty((m, 4096), device=dev)
-    c2 = torch.empty((m, 4096), device=dev)
+    c1 = torch.empty((ms, 4096), device=dev)
+    c2 = torch.empty((ms, 4096), device=dev)
     G.force_split("always")
     G.spdm_gcoo_dev(d, torch.from_numpy(b).to(dev), c1)
     split = G.last_split()

@@ -6,7 +6,7 @@ run() { timeout 300 python tools/kernel_sweep.py --powerlaw --s 0.99 --kernels a
 import sys, json
 for l in sys.stdin:
     d = json.loads(l); print('   ', d['kernel'], d['kernel_ms'], d['ms'])"; }
-for f in ${FACTORS:-2}; do echo "== factor $f"; GCOO_SPLIT_FACTOR=$f run; done
+for f in ${FACTORS:-1}; do echo "== factor $f"; GCOO_SPLIT_FACTOR=$f run; done
 for h in ${ROWS:-}; do for k in ${HK:-auto}; do
   echo "== rows $h heavy kind $k"
   if [ "$k" = auto ]; then GCOO_SPLIT_ROWS=$h run; else GCOO_SPLIT_ROWS=$h GCOO_SPLIT_HEAVY_KIND=$k run; fi
