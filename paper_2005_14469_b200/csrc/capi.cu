@@ -298,9 +298,11 @@ void set_smem_attr() {
 // host pipeline); 0 = full row blocks.
 // `pos` (two-class split): rows at heaviest-first positions [lo, hi) only
 // (rank_rows_kernel ran before); nullptr = every row, placed here.
+// `even` (A's rows known to be even, no pos): identity placement written by
+// plan_init_kernel, without the row count / histogram / placement kernels.
 template <class Cfg, typename T>
 void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ctas = 0, int64_t col_tiles = 1,
-                const int32_t* pos = nullptr, int64_t lo = 0, int64_t hi = 0) {
+                const int32_t* pos = nullptr, int64_t lo = 0, int64_t hi = 0, bool even = false) {
   set_smem_attr<Cfg>();
   const int64_t rows = pos ? hi - lo : a.m;
   P.row_blocks = ceil_div(rows, Cfg::RB);
@@ -319,7 +321,8 @@ void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ct
   const int64_t nseg = P.row_blocks * nchunks;
   // every buffer first: the kernels below form one uninterrupted PDL chain
   DevBuf<uint32_t> cnt(units * nchunks * Cfg::RW, s);
-  DevBuf<int32_t> row_nnz(pos ? 0 : a.m, s), hist(pos ? 0 : 33, s), cursor(33, s);
+  const bool ident = even && !pos;
+  DevBuf<int32_t> row_nnz(pos || ident ? 0 : a.m, s), hist(pos || ident ? 0 : 33, s), cursor(33, s);
   P.unit_of = DevBuf<int32_t>(a.m, s);
   P.row_of = DevBuf<int32_t>(P.row_blocks * Cfg::RB, s);
   P.skewed = DevBuf<int32_t>(1, s);
@@ -332,10 +335,22 @@ void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ct
   DevBuf<uint32_t> woff(nseg * Cfg::NW, s);  // warp segment offsets inside a segment
 
   const int64_t init_n = std::max<int64_t>((int64_t)cnt.count, std::max<int64_t>(a.m, (int64_t)P.row_of.count));
+  IdentPlace ip;
+  if (ident) {
+    ip.unit_of = P.unit_of.get();
+    ip.skew_flag = P.skewed.get();
+    ip.rb_rows = Cfg::RB;
+    ip.nw = Cfg::NW;
+    ip.rw = Cfg::RW;
+    ip.rpb = (int32_t)rpb;
+  }
   GCOO_LAUNCH_PDL(plan_init_kernel, grid_for(init_n, 256), 256, 0, s, cnt.get(), (int64_t)cnt.count,
-                  pos ? (int32_t*)nullptr : row_nnz.get(), a.m, pos ? (int32_t*)nullptr : hist.get(), cursor.get(),
-                  P.row_of.get(), (int64_t)P.row_of.count);
-  if (pos) {
+                  pos || ident ? (int32_t*)nullptr : row_nnz.get(), a.m,
+                  pos || ident ? (int32_t*)nullptr : hist.get(), cursor.get(), P.row_of.get(),
+                  (int64_t)P.row_of.count, ip);
+  if (ident) {
+    // placed by plan_init_kernel
+  } else if (pos) {
     // the heavy class (lo == 0) launches its heaviest row block first; the light class
     // keeps plain order (row blocks fastest: co-resident CTAs share B strips in L2 —
     // configs[3]: same time, 1.63 instead of 2.67 GB of DRAM reads for the light kernel)
@@ -468,12 +483,12 @@ int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const 
 // column strips of the host pipeline) — when that grid is smaller than one
 // wave, TMEM kernels spread A's rows over enough row blocks to fill the GPU.
 template <typename T>
-void make_plan(SpdmPlan& P, const DevGcoo<T>& a, int kind, cudaStream_t s, int64_t strip_n = 0) {
+void make_plan(SpdmPlan& P, const DevGcoo<T>& a, int kind, cudaStream_t s, int64_t strip_n = 0, bool even = false) {
   P.kind = kind;
   const int64_t wave = strip_n ? sm_count() : 0;
   with_cfg<T>(kind, [&](auto c) {
     using Cfg = decltype(c);
-    build_plan<Cfg>(P, a, s, wave, ceil_div(strip_n, Cfg::W));
+    build_plan<Cfg>(P, a, s, wave, ceil_div(strip_n, Cfg::W), nullptr, 0, 0, even);
   });
 }
 
@@ -531,6 +546,7 @@ void run_spdm(const SpdmPlan& P, const DevGcoo<T>& a, int64_t n, const T* B, int
 // positions.
 struct SkewHint {
   bool split = false;
+  bool even = false;  // largest row <= 4x the mean + 16: row_balance_kernel would keep identity placement
   int64_t heavy_rows = 0, heavy_nnz = 0;
   double top_density = 0;  // density of the heaviest 504 rows (the heavy plan's first row block)
 };
@@ -552,6 +568,7 @@ double split_factor() {
 // 8.03 at factors 2 / 4 and 7.95 / 8.87 at 0.5 / 0.25 (tools/split_sweep.sh).
 SkewHint decide_split(int64_t m, int64_t nnz, const unsigned long long* st) {
   SkewHint h;
+  h.even = (double)st[0] <= 4.0 * std::ceil((double)nnz / (double)std::max<int64_t>(m, 1)) + 16.0;
   const int force = g_force_split.load(std::memory_order_relaxed);
   if (force == 0 || m < 2 || nnz <= 0) return h;
   const double mean = (double)nnz / (double)m;
@@ -645,7 +662,7 @@ bool make_split_plan(SpdmPlan& P, const DevGcoo<T>& a, const SkewHint& h, int64_
   if (!fits) return false;
   DevBuf<int32_t> row_nnz(a.m, s), hist(33, s), cursor(33, s), pos(a.m, s);
   GCOO_LAUNCH_PDL(plan_init_kernel, grid_for(a.m, 256), 256, 0, s, (uint32_t*)nullptr, (int64_t)0, row_nnz.get(),
-                  a.m, hist.get(), cursor.get(), (int32_t*)nullptr, (int64_t)0);
+                  a.m, hist.get(), cursor.get(), (int32_t*)nullptr, (int64_t)0, IdentPlace{});
   if (a.nnz > 0) GCOO_LAUNCH_PDL(row_nnz_kernel, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.rows, row_nnz.get());
   GCOO_LAUNCH_PDL(bucket_hist_kernel, grid_for(a.m, 256), 256, 0, s, a.m, (const int32_t*)row_nnz.get(), hist.get());
   GCOO_LAUNCH_PDL(rank_rows_kernel, grid_for(a.m, 256), 256, 0, s, a.m, (const int32_t*)row_nnz.get(),
@@ -670,15 +687,22 @@ bool make_split_plan(SpdmPlan& P, const DevGcoo<T>& a, const SkewHint& h, int64_
 // The plan for one call (or one pipelined strip width): a two-class split for
 // a skewed A, else the density choice.  `cached`: reuse this A's split
 // decision (device path); the plan API and the host path probe afresh.
+// `max_group_nnz` (>= 0 when the caller holds the group sizes on the host): a
+// row cannot outweigh its group, so groups no heavier than 8x the mean row
+// rule the split out without the device probe and its synchronisation.
 template <typename T>
 void plan_for(SpdmPlan& P, const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const T* B, const T* C,
-              int flavor, cudaStream_t s, int64_t strip_n, bool small_gate, bool cached) {
+              int flavor, cudaStream_t s, int64_t strip_n, bool small_gate, bool cached, int64_t max_group_nnz = -1) {
   const int kind = choose_kind<T>(a, n, ldb, ldc, B, C, flavor, small_gate);
-  if (kind != 0 && g_force_kernel.load(std::memory_order_relaxed) < 0) {
+  bool even = false;
+  const bool no_split = max_group_nnz >= 0 && g_force_split.load(std::memory_order_relaxed) < 0 &&
+                        (double)max_group_nnz <= 8.0 * (double)a.nnz / (double)std::max<int64_t>(a.m, 1);
+  if (kind != 0 && !no_split && g_force_kernel.load(std::memory_order_relaxed) < 0) {
     const SkewHint h = skew_hint<T>(a, s, cached);
     if (h.split && make_split_plan<T>(P, a, h, n, ldb, ldc, B, C, flavor, s, strip_n)) return;
+    even = h.even;
   }
-  make_plan<T>(P, a, kind, s, strip_n);
+  make_plan<T>(P, a, kind, s, strip_n, even);
 }
 
 template <typename T>
@@ -986,6 +1010,12 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
   validate_spdm(m, k, n, a_p, cfg_p, cfg_b, b_rows, nnz, groups, tile_order, tile_count);
   const bool perm = tile_order ? tile_order_is_permutation(tile_order, tile_count) : true;
   cudaStream_t s = thread_stream();
+  // the heaviest group bounds every row (plan_for skips the split probe for even A)
+  int64_t max_group = -1;
+  if (!dev_a) {
+    max_group = 0;
+    for (int64_t g = 0; g < groups; ++g) max_group = std::max(max_group, gnnz[g]);
+  }
   const bool page_b = host_pageable(B), page_c = host_pageable(C);
   const bool staged = (page_b || page_c) && g_host_staging.load(std::memory_order_relaxed) != 0;
   const int64_t W = perm ? pipeline_strip(m, k, n, page_b || page_c, staged) : 0;
@@ -1064,7 +1094,9 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
   if (W == 0) {
     DevBuf<T> d_B(k * n, s), d_C(m * n, s);
     h2d(d_B.get(), B, k * n, s);
-    launch_spdm<T>(a, n, d_B.get(), n, d_C.get(), n, flavor, s);
+    SpdmPlan P1;
+    plan_for<T>(P1, a, n, n, n, d_B.get(), d_C.get(), flavor, s, n, /*small_gate=*/true, /*cached=*/false, max_group);
+    run_spdm<T>(P1, a, n, d_B.get(), n, d_C.get(), n, flavor, s);
     if (!perm) {
       apply_tile_list<T>(a, n, cfg_b, tile_order, tile_count, d_C.get(), n, stats, s);
     } else if (stats) {
@@ -1077,7 +1109,12 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
   // ---- pipelined: a ring of NBUF strip buffers (ld = W)
   if (trace) trace->mark(s, 0, -1);  // A uploaded
   SpdmPlan P;
-  plan_for<T>(P, a, W, W, W, dBv[0].get(), dCv[0].get(), flavor, s, W, /*small_gate=*/true, /*cached=*/false);
+  // the small-product gate looks at one strip: a strip's multiply is short, and
+  // the planner would sit on the critical path before the first C strip can
+  // cross PCIe (n=8000, s=0.99, 32 strips: 6.0 ms per call with the row-tile
+  // kernel per strip against 6.6 ms with the TMEM kernel and its planner)
+  plan_for<T>(P, a, W, W, W, dBv[0].get(), dCv[0].get(), flavor, s, W, /*small_gate=*/true, /*cached=*/false,
+              max_group);
   if (trace) trace->mark(s, 1, -1);  // planned
   for (int64_t j = 0; j < nstrips; ++j) {
     const int b = (int)(j % NBUF);

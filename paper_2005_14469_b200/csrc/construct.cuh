@@ -355,17 +355,40 @@ __global__ void row_nnz_kernel(int64_t nnz, const int32_t* __restrict__ rows, in
 
 // Planner scratch initialisation in one launch (replaces five memsets so the
 // planner's kernel chain stays programmatically dependent end to end).
+// `ident` (unit_of != nullptr): the placement row_balance_kernel gives an
+// A whose rows are known to be even (the host's cached degree statistics):
+// row r at position r, block r / rpb, dealt over the block's warps — written
+// here directly, per row and per slot, so the plan skips the row count,
+// histogram and placement kernels.
+struct IdentPlace {
+  int32_t* unit_of = nullptr;
+  int32_t* skew_flag = nullptr;
+  int32_t rb_rows = 0, nw = 0, rw = 0, rpb = 0;
+};
+
 __global__ void plan_init_kernel(uint32_t* __restrict__ cnt, int64_t cnt_n, int32_t* __restrict__ row_nnz,
                                  int64_t m, int32_t* __restrict__ hist, int32_t* __restrict__ cursor,
-                                 int32_t* __restrict__ row_of, int64_t row_of_n) {
+                                 int32_t* __restrict__ row_of, int64_t row_of_n, IdentPlace ident) {
   griddep_wait();  // PDL: predecessor complete
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (int64_t i = t0; i < cnt_n; i += stride) cnt[i] = 0u;
   if (row_nnz)
     for (int64_t i = t0; i < m; i += stride) row_nnz[i] = 0;
-  if (row_of)
+  if (ident.unit_of) {
+    if (t0 == 0) *ident.skew_flag = 0;
+    for (int64_t r = t0; r < m; r += stride) {
+      const int64_t blk = r / ident.rpb, j = r % ident.rpb;
+      ident.unit_of[r] = (int32_t)(blk * ident.rb_rows + (j % ident.nw) * ident.rw + j / ident.nw);
+    }
+    for (int64_t u = t0; u < row_of_n; u += stride) {
+      const int64_t blk = u / ident.rb_rows, q = u % ident.rb_rows;
+      const int64_t j = (q % ident.rw) * ident.nw + q / ident.rw, r = blk * ident.rpb + j;
+      row_of[u] = (j < ident.rpb && r < m) ? (int32_t)r : -1;
+    }
+  } else if (row_of) {
     for (int64_t i = t0; i < row_of_n; i += stride) row_of[i] = -1;
+  }
   if (hist && t0 < 33) {
     hist[t0] = 0;
     cursor[t0] = 0;
@@ -448,13 +471,32 @@ __global__ void skew_probe_kernel(int64_t m, const int32_t* __restrict__ row_nnz
   if (threadIdx.x < 33) cnt[threadIdx.x] = sum[threadIdx.x] = 0;
   if (threadIdx.x == 0) mx = 0;
   __syncthreads();
+  // a thread's rows mostly share one bucket (uniform A: all of them): count
+  // runs locally and flush a run when the bucket changes
+  int cur = -1;
+  unsigned long long c_cnt = 0, c_sum = 0;
+  int32_t my_max = 0;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
     const int32_t c = row_nnz[r];
-    const int b = nnz_bucket(c) + 1;
-    atomicAdd(&cnt[b - 1], 1ull);
-    atomicAdd(&sum[b - 1], (unsigned long long)c);
-    atomicMax(&mx, c);
+    const int b = nnz_bucket(c);
+    if (b != cur) {
+      if (c_cnt) {
+        atomicAdd(&cnt[cur], c_cnt);
+        atomicAdd(&sum[cur], c_sum);
+      }
+      cur = b;
+      c_cnt = c_sum = 0;
+    }
+    ++c_cnt;
+    c_sum += (unsigned long long)c;
+    my_max = max(my_max, c);
   }
+  if (c_cnt) {
+    atomicAdd(&cnt[cur], c_cnt);
+    atomicAdd(&sum[cur], c_sum);
+  }
+  my_max = __reduce_max_sync(0xffffffffu, my_max);
+  if ((threadIdx.x & 31) == 0) atomicMax(&mx, my_max);
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(&out[0], (unsigned long long)mx);
   if (threadIdx.x < 33) {
