@@ -18,8 +18,10 @@
 //     28), warp w owns TMEM lane quadrant w%4 and TCOLS = 512/(NW/4) columns
 //     = RW = TCOLS/V rows x V columns per lane.  V=4, 28 warps: W=128, RB=504
 //     (the default); 16 warps: RB=512; V=2: W=64, RB=1024.
-//   * A warp walks its chunk's records in one flat loop: a record carries up
-//     to two entries of one row slot {v0, v1, off0 | slot << 24, off1}.  The
+//   * A warp walks its chunk's entries in one flat loop: a 16-byte record
+//     carries two consecutive entries of the warp's slot-major stream
+//     {v0, v1, off0 | slot0 << 24, off1 | slot1 << 24} (denser
+//     configurations: three entries of one slot).  The
 //     slot's V accumulators are pulled into registers from TMEM
 //     (tcgen05.ld.32x32b) when the slot changes and pushed back
 //     (tcgen05.st) when it is left: one ld/st pair per visited (slot, chunk),
@@ -67,7 +69,8 @@ struct TaccCfg {
   static constexpr uint32_t STAGE_BYTES = BTILE + CAP_;
   static constexpr int HDR = 16;           // per-warp header: record count
   static constexpr int REC = 16;           // bytes per record
-  // entries per record: 2 = {v0, v1, off0 | slot<<24, off1} (byte offsets, ~0 = absent);
+  // entries per record: 2 = {v0, v1, off0 | slot0<<24, off1 | slot1<<24} (B byte offsets; any two
+  //   consecutive entries of the warp's stream, header = entry count);
   // 3 = {v0, v1, v2, r0 | r1<<8 | r2<<16 | slot<<24} (B row indices in the chunk, 0xFF = absent);
   // 1 (double) = {lo(v), hi(v), off | slot<<24, 0}
   static constexpr int EPR = EPR_;
@@ -131,6 +134,11 @@ __device__ __forceinline__ uint32_t tacc_warp_records(const uint32_t* __restrict
   if (u >= units) return 0u;
   const uint32_t* p = cnt + (u * nchunks + c) * Cfg::RW;
   uint32_t r = 0;
+  if constexpr (Cfg::EPR == 2) {  // dense pairs: any two consecutive entries of the warp's stream
+#pragma unroll 8
+    for (int s = 0; s < Cfg::RW; ++s) r += p[s];
+    return (r + 1) / 2;
+  }
 #pragma unroll 8
   for (int s = 0; s < Cfg::RW; ++s) r += (p[s] + Cfg::EPR - 1) / Cfg::EPR;
   return r;
@@ -162,8 +170,12 @@ __global__ void tacc_size_kernel(const uint32_t* __restrict__ cnt, int64_t units
 }
 
 // P4: one thread per (segment, warp, slot): the stream position of the slot's
-// record run (for the scatter) and its "absent second entry" marks; the
-// slot-0 thread also writes the warp's offset-table entry and record count.
+// entries (for the scatter); the slot-0 thread also writes the warp's
+// offset-table entry and its header.  EPR 2: the warp's entries form one
+// dense stream of pairs (slot-major, column order), `slot_pos` = the entry
+// index of the slot's first entry counted in 8-byte halves of the stream
+// (stream start / 8 + entries before), no absent marks; header {entries}.
+// EPR 1/3: records per slot run, absent entries marked; header {records}.
 template <class Cfg>
 __global__ void tacc_header_kernel(const uint32_t* __restrict__ cnt, int64_t units, int nchunks, int64_t nseg,
                                    const int64_t* __restrict__ seg_off, const uint32_t* __restrict__ woff,
@@ -179,24 +191,40 @@ __global__ void tacc_header_kernel(const uint32_t* __restrict__ cnt, int64_t uni
     const int c = (int)(x % nchunks);
     const int64_t u = rb * Cfg::NW + w;
     const uint32_t* p = cnt + (u * nchunks + c) * Cfg::RW;
-    uint32_t before = 0;
-    if (u < units)
-      for (int q = 0; q < s; ++q) before += (p[q] + Cfg::EPR - 1) / Cfg::EPR;
-    const uint32_t ns = u < units ? (p[s] + Cfg::EPR - 1) / Cfg::EPR : 0u;
     const uint32_t wo = woff[xw];
-    const int64_t pos = seg_off[x] + wo + Cfg::HDR + (int64_t)Cfg::REC * before;
-    slot_pos[t] = pos;
-    uint32_t* rec = reinterpret_cast<uint32_t*>(ent + pos);
-    // absent-entry marks, overwritten by the entries that exist
-    const uint32_t mark = Cfg::EPR == 3 ? 0x00FFFFFFu | ((uint32_t)s << 24) : Cfg::EPR == 1 ? 0u : ~0u;
-    for (uint32_t j = 0; j < ns; ++j) rec[4 * j + 3] = mark;
-    if (s == 0) {
-      uint32_t nrec = 0;
+    const int64_t start = seg_off[x] + wo + Cfg::HDR;  // 16-byte aligned
+    if constexpr (Cfg::EPR == 2) {
+      uint32_t before = 0;
       if (u < units)
-        for (int q = 0; q < Cfg::RW; ++q) nrec += (p[q] + Cfg::EPR - 1) / Cfg::EPR;
-      unsigned char* seg = ent + seg_off[x];
-      reinterpret_cast<uint32_t*>(seg)[w] = wo;
-      *reinterpret_cast<uint4*>(seg + wo) = make_uint4(nrec, 0u, 0u, 0u);
+        for (int q = 0; q < s; ++q) before += p[q];
+      slot_pos[t] = start / 8 + before;
+      if (s == 0) {
+        uint32_t nent = 0;
+        if (u < units)
+          for (int q = 0; q < Cfg::RW; ++q) nent += p[q];
+        unsigned char* seg = ent + seg_off[x];
+        reinterpret_cast<uint32_t*>(seg)[w] = wo;
+        *reinterpret_cast<uint4*>(seg + wo) = make_uint4(nent, 0u, 0u, 0u);
+      }
+    } else {
+      uint32_t before = 0;
+      if (u < units)
+        for (int q = 0; q < s; ++q) before += (p[q] + Cfg::EPR - 1) / Cfg::EPR;
+      const uint32_t ns = u < units ? (p[s] + Cfg::EPR - 1) / Cfg::EPR : 0u;
+      const int64_t pos = start + (int64_t)Cfg::REC * before;
+      slot_pos[t] = pos;
+      uint32_t* rec = reinterpret_cast<uint32_t*>(ent + pos);
+      // absent-entry marks, overwritten by the entries that exist
+      const uint32_t mark = Cfg::EPR == 3 ? 0x00FFFFFFu | ((uint32_t)s << 24) : 0u;
+      for (uint32_t j = 0; j < ns; ++j) rec[4 * j + 3] = mark;
+      if (s == 0) {
+        uint32_t nrec = 0;
+        if (u < units)
+          for (int q = 0; q < Cfg::RW; ++q) nrec += (p[q] + Cfg::EPR - 1) / Cfg::EPR;
+        unsigned char* seg = ent + seg_off[x];
+        reinterpret_cast<uint32_t*>(seg)[w] = wo;
+        *reinterpret_cast<uint4*>(seg + wo) = make_uint4(nrec, 0u, 0u, 0u);
+      }
     }
   }
 }
@@ -238,11 +266,12 @@ __global__ void tacc_fill_kernel(int64_t nnz, int32_t p, const typename Cfg::E* 
       uint32_t* word = reinterpret_cast<uint32_t*>(ent + base + (int64_t)Cfg::REC * (rank / 3));
       word[rank % 3] = __float_as_uint((float)vals[e]);
       reinterpret_cast<unsigned char*>(word + 3)[rank % 3] = (unsigned char)(col - lo_col);  // slot byte: header
-    } else {
-      uint32_t* word = reinterpret_cast<uint32_t*>(ent + base + (int64_t)Cfg::REC * (rank >> 1));
-      const uint32_t off = (uint32_t)(col - lo_col) * Cfg::ROWB;
-      word[rank & 1] = __float_as_uint((float)vals[e]);
-      word[2 + (rank & 1)] = (rank & 1) ? off : (off | (slot << 24));
+    } else {  // dense pairs: entry index base + rank, in 8-byte halves of the stream
+      const int64_t ve = base + rank;
+      uint32_t* word = reinterpret_cast<uint32_t*>(ent + (ve >> 1) * 16);
+      const uint32_t h = (uint32_t)(ve & 1);
+      word[h] = __float_as_uint((float)vals[e]);
+      word[2 + h] = ((uint32_t)(col - lo_col) * Cfg::ROWB) | (slot << 24);
     }
   }
 }
@@ -326,18 +355,14 @@ __device__ __forceinline__ void tacc_fma(float (&acc)[V], float a, const float (
   }
 }
 
-// One record: its (up to) two entries of one row slot.
-template <class Cfg, bool GLOBAL>
-__device__ __forceinline__ void tacc_one(float (&acc)[Cfg::V], uint32_t& cur, uint32_t tacc, const uint4 q,
-                                         uint32_t bbase) {
-  constexpr int V = Cfg::V;
-  float b0[V], b1[V];
-  const bool two = q.w != ~0u;
-  lds_vec<V>(bbase + (q.z & 0xffffffu), b0);
-  if (two) lds_vec<V>(bbase + q.w, b1);
-  tacc_switch<Cfg>(acc, cur, tacc, q.z >> 24);
-  tacc_fma<V, true>(acc, __uint_as_float(q.x), b0);
-  if (two) tacc_fma<V, true>(acc, __uint_as_float(q.y), b1);
+// One entry {v, off | slot << 24}.
+template <class Cfg>
+__device__ __forceinline__ void tacc_entry(float (&acc)[Cfg::V], uint32_t& cur, uint32_t tacc, uint32_t v, uint32_t o,
+                                           uint32_t bbase) {
+  float b[Cfg::V];
+  lds_vec<Cfg::V>(bbase + (o & 0xffffffu), b);
+  tacc_switch<Cfg>(acc, cur, tacc, o >> 24);
+  tacc_fma<Cfg::V, true>(acc, __uint_as_float(v), b);
 }
 
 // Three-entry records (dense regime: long runs fill them): B row r of the
@@ -410,10 +435,11 @@ __device__ __forceinline__ void tacc_consume1(float (&acc)[Cfg::V], uint32_t& cu
   }
 }
 
-// One warp walks its records for one chunk, two records per step (both
-// records and their B rows are in flight before the first FMA), then the odd
-// record if any — the paired loop carries no "second record present" tests.
-// `cur` (the slot whose accumulators are in registers) persists across chunks.
+// One warp walks its entries for one chunk: a dense stream of pairs
+// {v0, v1, off0 | slot0 << 24, off1 | slot1 << 24} in slot-major, column
+// order, two pairs (four entries, their four B rows in flight) per step, then
+// the 0-3 left over — no absent entries, so no predicated FMAs.  `cur` (the
+// slot whose accumulators are in registers) persists across chunks.
 template <class Cfg, bool GLOBAL>
 __device__ __forceinline__ void tacc_consume(float (&acc)[Cfg::V], uint32_t& cur, uint32_t tacc,
                                              typename RecSrc<GLOBAL>::addr_t seg, int warp, uint32_t bbase) {
@@ -424,39 +450,55 @@ __device__ __forceinline__ void tacc_consume(float (&acc)[Cfg::V], uint32_t& cur
   asm volatile("mov.b32 %0, %0;" : "+r"(bbase));
   const uint32_t woff = Src::ld32(seg + 4 * warp);
   const auto wseg = seg + woff;
-  const uint32_t nrec = Src::ld32(wseg);
+  const uint32_t nent = Src::ld32(wseg);
 #if GCOO_PROF
-  if ((threadIdx.x & 31) == 0) g_prof_recs[threadIdx.x >> 5] += nrec;
+  if ((threadIdx.x & 31) == 0) g_prof_recs[threadIdx.x >> 5] += (nent + 1) / 2;
 #endif
   auto rec = wseg + Cfg::HDR;
-  for (uint32_t r = 1; r < nrec; r += 2, rec += 2 * Cfg::REC) {
+  uint32_t r = 0;
+  for (; r + 4 <= nent; r += 4, rec += 2 * Cfg::REC) {
     const uint4 qa = Src::ld(rec);
     const uint4 qb = Src::ld(rec + Cfg::REC);
-    float ba0[V], ba1[V], bb0[V], bb1[V];
-    const bool a2 = qa.w != ~0u;
-    const bool b2 = qb.w != ~0u;
+    float b0[V], b1[V], b2[V], b3[V];
     if constexpr (GCOO_ABL & 2) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        ba0[v] = __uint_as_float(qa.z + v);
-        ba1[v] = __uint_as_float(qa.w + v);
-        bb0[v] = __uint_as_float(qb.z + v);
-        bb1[v] = __uint_as_float(qb.w + v);
+        b0[v] = __uint_as_float(qa.z + v);
+        b1[v] = __uint_as_float(qa.w + v);
+        b2[v] = __uint_as_float(qb.z + v);
+        b3[v] = __uint_as_float(qb.w + v);
       }
     } else {
-      lds_vec<V>(bbase + (qa.z & 0xffffffu), ba0);
-      if (a2) lds_vec<V>(bbase + qa.w, ba1);
-      lds_vec<V>(bbase + (qb.z & 0xffffffu), bb0);
-      if (b2) lds_vec<V>(bbase + qb.w, bb1);
+      lds_vec<V>(bbase + (qa.z & 0xffffffu), b0);
+      lds_vec<V>(bbase + (qa.w & 0xffffffu), b1);
+      lds_vec<V>(bbase + (qb.z & 0xffffffu), b2);
+      lds_vec<V>(bbase + (qb.w & 0xffffffu), b3);
     }
     tacc_switch<Cfg>(acc, cur, tacc, qa.z >> 24);
-    tacc_fma<V, true>(acc, __uint_as_float(qa.x), ba0);
-    if (a2) tacc_fma<V, true>(acc, __uint_as_float(qa.y), ba1);
+    tacc_fma<V, true>(acc, __uint_as_float(qa.x), b0);
+    tacc_switch<Cfg>(acc, cur, tacc, qa.w >> 24);
+    tacc_fma<V, true>(acc, __uint_as_float(qa.y), b1);
     tacc_switch<Cfg>(acc, cur, tacc, qb.z >> 24);
-    tacc_fma<V, true>(acc, __uint_as_float(qb.x), bb0);
-    if (b2) tacc_fma<V, true>(acc, __uint_as_float(qb.y), bb1);
+    tacc_fma<V, true>(acc, __uint_as_float(qb.x), b2);
+    tacc_switch<Cfg>(acc, cur, tacc, qb.w >> 24);
+    tacc_fma<V, true>(acc, __uint_as_float(qb.y), b3);
   }
-  if (nrec & 1u) tacc_one<Cfg, GLOBAL>(acc, cur, tacc, Src::ld(rec), bbase);
+  const uint32_t left = nent - r;  // 0..3
+  if (left >= 2) {
+    const uint4 q = Src::ld(rec);
+    float b0[V], b1[V];
+    lds_vec<V>(bbase + (q.z & 0xffffffu), b0);
+    lds_vec<V>(bbase + (q.w & 0xffffffu), b1);
+    tacc_switch<Cfg>(acc, cur, tacc, q.z >> 24);
+    tacc_fma<V, true>(acc, __uint_as_float(q.x), b0);
+    tacc_switch<Cfg>(acc, cur, tacc, q.w >> 24);
+    tacc_fma<V, true>(acc, __uint_as_float(q.y), b1);
+    rec += Cfg::REC;
+  }
+  if (left & 1u) {
+    const uint4 q = Src::ld(rec);
+    tacc_entry<Cfg>(acc, cur, tacc, q.x, q.z, bbase);
+  }
 }
 
 template <class Cfg>
