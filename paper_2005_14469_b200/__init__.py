@@ -116,6 +116,7 @@ def lib():
     _sig(L, "gcoo_debug_last_kernel", _int, [])
     _sig(L, "gcoo_debug_last_split", _int, [])
     _sig(L, "gcoo_debug_force_split", _int, [_int])
+    _sig(L, "gcoo_debug_seg_planner", _int, [_int])
     _sig(L, "gcoo_plan_create_f32_dev", _int, [_i64, _i64, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _int,
                                                 C.POINTER(_vp), _vp])
     _sig(L, "gcoo_plan_spdm_f32_dev", _int, [_vp, _i64, _vp, _i64, _vp, _i64, _vp])
@@ -192,6 +193,12 @@ def force_split(mode: str = "auto") -> None:
     """Test hook: the two-class split of skewed matrices ("auto", "never",
     "always" = whenever the rows form two degree classes)."""
     lib().gcoo_debug_force_split({"auto": -1, "never": 0, "always": 1}[mode])
+
+
+def seg_planner(on: bool = True) -> None:
+    """Test hook: build even-A plans with the segment planner (default) or the
+    general count / size / header / fill chain."""
+    lib().gcoo_debug_seg_planner(1 if on else 0)
 
 
 def kernel_timing(enable: bool = True) -> None:

@@ -282,6 +282,10 @@ struct SpdmPlan {
   std::unique_ptr<SpdmPlan> heavy;
 };
 
+// The segment planner for even A (seg_plan_kernel); 0 = the general chain
+// for every A (test / measurement hook gcoo_debug_seg_planner).
+std::atomic<int> g_seg_planner{1};
+
 template <class Cfg>
 void set_smem_attr() {
   // cudaFuncSetAttribute is idempotent; the flags only skip repeated calls
@@ -319,9 +323,30 @@ void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ct
   P.nchunks = (int)ceil_div(a.k, Cfg::KC);
   const int nchunks = P.nchunks;
   const int64_t nseg = P.row_blocks * nchunks;
+  const bool ident = even && !pos;
+  if (ident && g_seg_planner.load(std::memory_order_relaxed)) {
+    // even A: the segment planner (count pass, scan, build pass) straight from the GCOO
+    P.unit_of = DevBuf<int32_t>(a.m, s);
+    P.row_of = DevBuf<int32_t>(P.row_blocks * Cfg::RB, s);
+    P.skewed = DevBuf<int32_t>(1, s);
+    DevBuf<int64_t> seg_len(nseg, s), scan_tmp(scan_scratch(nseg), s), tab(a.groups * (nchunks + 1), s);
+    P.seg_off = DevBuf<int64_t>(nseg + 1, s);
+    P.ent = DevBuf<unsigned char>(nseg * (Cfg::TABLE + Cfg::NW * Cfg::HDR) + (int64_t)Cfg::REC * a.nnz + 16, s);
+    const unsigned grid = (unsigned)std::min<int64_t>(std::max<int64_t>(nseg, 1), (int64_t)sm_count() * 8);
+    GCOO_LAUNCH_PDL(chunk_table_kernel, grid_for(std::max(a.nnz, a.groups), 256), 256, 0, s, a.nnz, a.p, a.groups,
+                    a.rows, a.cols, a.gidx, a.gnnz, (int32_t)Cfg::KC, nchunks, tab.get());
+    GCOO_LAUNCH_PDL((seg_plan_kernel<Cfg, 1>), grid, kSegThreads, 0, s, a.m, a.nnz, a.p, a.vals, a.rows, a.cols,
+                    a.gidx, a.gnnz, (const int64_t*)tab.get(), nchunks, nseg, (int32_t)rpb, seg_len.get(),
+                    P.unit_of.get(), P.row_of.get(), P.skewed.get(), (const int64_t*)nullptr, (unsigned char*)nullptr);
+    exclusive_scan(seg_len.get(), P.seg_off.get(), nseg, s, scan_tmp.get());
+    GCOO_LAUNCH_PDL((seg_plan_kernel<Cfg, 2>), grid, kSegThreads, 0, s, a.m, a.nnz, a.p, a.vals, a.rows, a.cols,
+                    a.gidx, a.gnnz, (const int64_t*)tab.get(), nchunks, nseg, (int32_t)rpb, (int64_t*)nullptr,
+                    (int32_t*)nullptr,
+                    (int32_t*)nullptr, (int32_t*)nullptr, (const int64_t*)P.seg_off.get(), P.ent.get());
+    return;
+  }
   // every buffer first: the kernels below form one uninterrupted PDL chain
   DevBuf<uint32_t> cnt(units * nchunks * Cfg::RW, s);
-  const bool ident = even && !pos;
   DevBuf<int32_t> row_nnz(pos || ident ? 0 : a.m, s), hist(pos || ident ? 0 : 33, s), cursor(33, s);
   P.unit_of = DevBuf<int32_t>(a.m, s);
   P.row_of = DevBuf<int32_t>(P.row_blocks * Cfg::RB, s);
@@ -694,12 +719,16 @@ template <typename T>
 void plan_for(SpdmPlan& P, const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const T* B, const T* C,
               int flavor, cudaStream_t s, int64_t strip_n, bool small_gate, bool cached, int64_t max_group_nnz = -1) {
   const int kind = choose_kind<T>(a, n, ldb, ldc, B, C, flavor, small_gate);
-  bool even = false;
   const bool no_split = max_group_nnz >= 0 && g_force_split.load(std::memory_order_relaxed) < 0 &&
                         (double)max_group_nnz <= 8.0 * (double)a.nnz / (double)std::max<int64_t>(a.m, 1);
-  if (kind != 0 && !no_split && g_force_kernel.load(std::memory_order_relaxed) < 0) {
+  // groups no heavier than 8x the mean row: rows stay in place (identity
+  // placement, the segment planner) — balancing would move only a few rows
+  bool even = no_split;
+  if (kind != 0 && !no_split) {
     const SkewHint h = skew_hint<T>(a, s, cached);
-    if (h.split && make_split_plan<T>(P, a, h, n, ldb, ldc, B, C, flavor, s, strip_n)) return;
+    if (g_force_kernel.load(std::memory_order_relaxed) < 0 && h.split &&
+        make_split_plan<T>(P, a, h, n, ldb, ldc, B, C, flavor, s, strip_n))
+      return;
     even = h.even;
   }
   make_plan<T>(P, a, kind, s, strip_n, even);
@@ -1759,6 +1788,11 @@ int gcoo_debug_last_split(void) { return t_last_split ? 1 : 0; }
 // whenever the degree distribution has two classes).
 int gcoo_debug_force_split(int mode) {
   g_force_split.store(mode, std::memory_order_relaxed);
+  return GCOO_OK;
+}
+
+int gcoo_debug_seg_planner(int on) {
+  g_seg_planner.store(on ? 1 : 0, std::memory_order_relaxed);
   return GCOO_OK;
 }
 

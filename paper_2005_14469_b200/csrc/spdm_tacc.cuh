@@ -276,6 +276,245 @@ __global__ void tacc_fill_kernel(int64_t nnz, int32_t p, const typename Cfg::E* 
   }
 }
 
+// ------------------------------------------ segment planner (even A) ------
+// For an A whose rows keep identity placement (row r in row block r / rpb,
+// warp (r % rpb) % NW, slot (r % rpb) / NW) one CTA per segment (row block,
+// chunk) builds its segment straight from the GCOO: the row block's rows are
+// whole group slices (or a row-filtered part of one when p > rpb), and inside
+// a group slice — sorted by (col, row) — a chunk's entries are one contiguous
+// range, found by binary search.  Pass 1 counts per (warp, slot) in shared
+// memory and writes the segment length (c == 0 CTAs also write the row
+// placement); pass 2, after the scan of the lengths, writes the offset table,
+// the warp headers and every entry.  Replaces the count / size / header / fill
+// chain (global atomics, per-slot scratch) for even A.
+constexpr int kSegThreads = 512;
+constexpr int kSegMaxGroups = 512;  // groups per row block (p = 1: rpb <= RB <= 512)
+constexpr int kSegRowCache = 4096;  // a segment's entry rows and columns staged in shared memory (pass 2)
+
+// tab[g * (nchunks + 1) + c] = the first entry of group g's slice with a
+// column >= c * KC, relative to the slice start (c = nchunks: the slice
+// length): every chunk range of every group without a search.  Each entry
+// writes the table cells of the chunks its column opens (from the previous
+// entry's chunk + 1 up to its own); the slice's last entry closes the rest.
+__global__ void chunk_table_kernel(int64_t nnz, int32_t p, int64_t groups, const int32_t* __restrict__ rows,
+                                   const int32_t* __restrict__ cols, const int64_t* __restrict__ gidx,
+                                   const int64_t* __restrict__ gnnz, int32_t kc, int nchunks,
+                                   int64_t* __restrict__ tab) {
+  griddep_wait();  // PDL: predecessor complete
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t e = t0; e < nnz; e += stride) {
+    const int64_t g = rows[e] / p;
+    const int64_t gs = gidx[g], ge = gs + gnnz[g];
+    const int c = cols[e] / kc;
+    const int cp = e == gs ? -1 : cols[e - 1] / kc;
+    int64_t* t = tab + g * (nchunks + 1);
+    for (int q = cp + 1; q <= c; ++q) t[q] = e - gs;
+    if (e == ge - 1)
+      for (int q = c + 1; q <= nchunks; ++q) t[q] = ge - gs;
+  }
+  for (int64_t g = t0; g < groups; g += stride)  // empty slices: every range empty
+    if (gnnz[g] == 0)
+      for (int q = 0; q <= nchunks; ++q) tab[g * (nchunks + 1) + q] = 0;
+}
+
+template <class Cfg>
+struct SegSmem {
+  uint32_t cnt[Cfg::NW * Cfg::RW];   // entries per (warp, slot)
+  uint32_t base[Cfg::NW * Cfg::RW];  // pass 2: the slot's first entry (EPR 2: 8-byte halves) / record byte, in-segment
+  int64_t lo[kSegMaxGroups];         // the chunk's range in each group slice
+  int32_t pre[kSegMaxGroups + 1];    // exclusive prefix of the range lengths
+  int32_t row[kSegRowCache];         // pass 2: the flattened ranges' rows (ranks) and columns, when they fit
+  int32_t col[kSegRowCache];
+};
+
+template <class Cfg, int PASS>
+__global__ void __launch_bounds__(kSegThreads)
+seg_plan_kernel(int64_t m, int64_t nnz, int32_t p, const typename Cfg::E* __restrict__ vals,
+                const int32_t* __restrict__ rows, const int32_t* __restrict__ cols, const int64_t* __restrict__ gidx,
+                const int64_t* __restrict__ gnnz, const int64_t* __restrict__ tab, int nchunks, int64_t nseg,
+                int32_t rpb,
+                int64_t* __restrict__ seg_len, int32_t* __restrict__ unit_of, int32_t* __restrict__ row_of,
+                int32_t* __restrict__ skew_flag, const int64_t* __restrict__ seg_off, unsigned char* __restrict__ ent) {
+  static_assert(Cfg::RB <= kSegMaxGroups, "groups per row block");
+  constexpr int NW = Cfg::NW, RW = Cfg::RW, EPR = Cfg::EPR;
+  __shared__ SegSmem<Cfg> sm;
+  __shared__ int32_t s_total;
+  griddep_wait();  // PDL: predecessor complete
+  const int tid = threadIdx.x;
+  if (PASS == 1 && blockIdx.x == 0 && tid == 0) *skew_flag = 0;
+  for (int64_t x = blockIdx.x; x < nseg; x += gridDim.x) {
+    const int64_t rb = x / nchunks;
+    const int c = (int)(x % nchunks);
+    const int64_t r0 = rb * rpb, r1 = r0 + rpb < m ? r0 + rpb : m;
+    const int32_t lo_col = c * Cfg::KC, hi_col = lo_col + Cfg::KC;
+    if (PASS == 1 && c == 0) {  // identity placement of the row block's rows
+      for (int64_t r = r0 + tid; r < r1; r += kSegThreads) {
+        const int64_t j = r - r0;
+        unit_of[r] = (int32_t)(rb * Cfg::RB + (j % NW) * RW + j / NW);
+      }
+      for (int q = tid; q < Cfg::RB; q += kSegThreads) {
+        const int64_t j = (int64_t)(q % RW) * NW + q / RW, r = r0 + j;
+        row_of[rb * Cfg::RB + q] = (j < rpb && r < r1) ? (int32_t)r : -1;
+      }
+    }
+    const int64_t g0 = r0 / p;
+    const int ng = r1 > r0 ? (int)((r1 - 1) / p - g0 + 1) : 0;
+    for (int i = tid; i < NW * RW; i += kSegThreads) sm.cnt[i] = 0u;
+    // the chunk's range in each group slice (chunk_table_kernel)
+    for (int t = tid; t < ng; t += kSegThreads) {
+      const int64_t* tg = tab + (g0 + t) * (int64_t)(nchunks + 1) + c;
+      const int64_t gs = gidx[g0 + t];
+      sm.lo[t] = gs + tg[0];
+      sm.pre[t + 1] = (int32_t)(tg[1] - tg[0]);
+    }
+    __syncthreads();
+    if (tid < 32) {  // warp 0: exclusive prefix of the range lengths
+      const int per = (ng + 31) / 32, t0 = tid * per, t1 = t0 + per < ng ? t0 + per : ng;
+      int32_t sum = 0;
+      for (int t = t0; t < t1; ++t) sum += sm.pre[t + 1];
+      int32_t incl = sum;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (tid >= d) incl += y;
+      }
+      int32_t run = incl - sum;
+      for (int t = t0; t < t1; ++t) {
+        const int32_t len = sm.pre[t + 1];
+        sm.pre[t] = run;
+        run += len;
+      }
+      if (tid == 31) {
+        sm.pre[ng] = incl;
+        s_total = incl;
+      }
+    }
+    __syncthreads();
+    const int32_t total = s_total;
+    // entry i of the flattened ranges: its group by binary search over pre
+    auto locate = [&](int32_t i, int64_t& e, int& g) {
+      int a = 0, b = ng;  // pre[a] <= i < pre[b]
+      while (b - a > 1) {
+        const int mid = (a + b) >> 1;
+        if (sm.pre[mid] <= i) a = mid; else b = mid;
+      }
+      g = a;
+      e = sm.lo[a] + (i - sm.pre[a]);
+    };
+    const bool cached = PASS == 2 && total <= kSegRowCache;
+    for (int32_t i = tid; i < total; i += kSegThreads) {
+      int64_t e;
+      int g;
+      locate(i, e, g);
+      const int32_t r = rows[e];
+      if (cached) {
+        sm.row[i] = r;
+        sm.col[i] = cols[e];
+      }
+      if (r < r0 || r >= r1) continue;  // another row block's row of a shared group (p > rpb)
+      const int64_t j = r - r0;
+      atomicAdd(&sm.cnt[(j % NW) * RW + j / NW], 1u);
+    }
+    __syncthreads();
+    if constexpr (PASS == 1) {
+      if (tid < 32) {
+        uint32_t sz = 0;
+        for (int w = tid; w < NW; w += 32) {
+          uint32_t recs = 0;
+          if constexpr (EPR == 2) {
+            for (int q = 0; q < RW; ++q) recs += sm.cnt[w * RW + q];
+            recs = (recs + 1) / 2;
+          } else {
+            for (int q = 0; q < RW; ++q) recs += (sm.cnt[w * RW + q] + EPR - 1) / EPR;
+          }
+          sz += Cfg::HDR + Cfg::REC * recs;
+        }
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) sz += __shfl_xor_sync(0xffffffffu, sz, d);
+        if (tid == 0) seg_len[x] = Cfg::TABLE + sz;
+      }
+    } else {
+      const int64_t so = seg_off[x];
+      unsigned char* seg = ent + so;
+      if (tid < 32) {  // warp 0: warp segment offsets (one lane per warp), then per-slot bases
+        uint32_t recs = 0, nent = 0;
+        if (tid < NW) {
+          for (int q = 0; q < RW; ++q) {
+            nent += sm.cnt[tid * RW + q];
+            recs += (sm.cnt[tid * RW + q] + EPR - 1) / EPR;
+          }
+          if (EPR == 2) recs = (nent + 1) / 2;
+        }
+        const uint32_t sz = tid < NW ? Cfg::HDR + Cfg::REC * recs : 0u;
+        uint32_t incl = sz;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+          if (tid >= d) incl += y;
+        }
+        if (tid < NW) {
+          const uint32_t wo = Cfg::TABLE + incl - sz;
+          reinterpret_cast<uint32_t*>(seg)[tid] = wo;
+          *reinterpret_cast<uint4*>(seg + wo) = make_uint4(EPR == 2 ? nent : recs, 0u, 0u, 0u);
+          uint32_t before = 0;
+          for (int q = 0; q < RW; ++q) {
+            const uint32_t cq = sm.cnt[tid * RW + q];
+            if constexpr (EPR == 2) {
+              sm.base[tid * RW + q] = (wo + Cfg::HDR) / 8 + before;
+              before += cq;
+            } else {
+              const uint32_t pos = wo + Cfg::HDR + Cfg::REC * before, ns = (cq + EPR - 1) / EPR;
+              sm.base[tid * RW + q] = pos;
+              // absent-entry marks, overwritten by the entries that exist
+              const uint32_t mark = EPR == 3 ? 0x00FFFFFFu | ((uint32_t)q << 24) : 0u;
+              for (uint32_t jj = 0; jj < ns; ++jj) reinterpret_cast<uint32_t*>(seg + pos)[4 * jj + 3] = mark;
+              before += ns;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      for (int32_t i = tid; i < total; i += kSegThreads) {
+        int64_t e;
+        int g;
+        locate(i, e, g);
+        const int32_t r = cached ? sm.row[i] : rows[e];
+        if (r < r0 || r >= r1) continue;
+        // rank among the row's entries of this chunk: same-row entries earlier in the range
+        uint32_t rank = 0;
+        if (cached) {
+          for (int32_t jx = sm.pre[g]; jx < i; ++jx) rank += sm.row[jx] == r;
+        } else {
+          for (int64_t jx = sm.lo[g]; jx < e; ++jx) rank += rows[jx] == r;
+        }
+        const int64_t j = r - r0;
+        const uint32_t slot = (uint32_t)(j / NW);
+        const uint32_t bse = sm.base[(j % NW) * RW + slot];
+        const int32_t col = cached ? sm.col[i] : cols[e];
+        if constexpr (EPR == 1) {
+          uint32_t* word = reinterpret_cast<uint32_t*>(seg + bse + (int64_t)Cfg::REC * rank);
+          const double v = (double)vals[e];
+          word[0] = (uint32_t)__double2loint(v);
+          word[1] = (uint32_t)__double2hiint(v);
+          word[2] = ((uint32_t)(col - lo_col) * Cfg::ROWB) | (slot << 24);
+        } else if constexpr (EPR == 3) {
+          uint32_t* word = reinterpret_cast<uint32_t*>(seg + bse + (int64_t)Cfg::REC * (rank / 3));
+          word[rank % 3] = __float_as_uint((float)vals[e]);
+          reinterpret_cast<unsigned char*>(word + 3)[rank % 3] = (unsigned char)(col - lo_col);
+        } else {
+          const int64_t ve = so / 8 + bse + rank;
+          uint32_t* word = reinterpret_cast<uint32_t*>(ent + (ve >> 1) * 16);
+          const uint32_t h = (uint32_t)(ve & 1);
+          word[h] = __float_as_uint((float)vals[e]);
+          word[2 + h] = ((uint32_t)(col - lo_col) * Cfg::ROWB) | (slot << 24);
+        }
+      }
+    }
+    __syncthreads();  // shared state is reused by the next segment
+  }
+}
+
 // ---------------------------------------------------------- main kernel --
 template <bool GLOBAL>
 struct RecSrc;

@@ -98,14 +98,20 @@ def test_random_shapes_bit_exact(gcoo, cuda, oracle, seed):
         assert max_rel(c, c_mad) <= 1e-5
 
 
+@pytest.mark.parametrize("planner", ["segment", "general"])
 @pytest.mark.parametrize("kernel", ["rowtile", "tacc_v4", "tacc28_k192", "tacc28_k160",
                                     "tacc28_k128", "tacc28_k96", "tacc28_k64", "tacc28_k200", "tacc_v4_k216", "tacc28_k176", "auto"])
-def test_each_fp32_kernel_bit_exact(gcoo, cuda, oracle, kernel):
+def test_each_fp32_kernel_bit_exact(gcoo, cuda, oracle, kernel, planner):
     """Every fp32 kernel variant, on shapes that hit its edges (m not a multiple
     of the row block, k not a multiple of the chunk, n not a multiple of the
-    strip, empty rows/tiles, every p the variant supports)."""
+    strip, empty rows/tiles, every p the variant supports), with its record
+    stream built by the segment planner (even A, the default) and by the
+    general count / header / fill chain."""
+    if kernel == "rowtile" and planner == "general":
+        pytest.skip("the row-tile kernel has no planner")
     rng = np.random.default_rng(sorted(gcoo.KERNELS).index(kernel))
     gcoo.force_kernel(kernel)
+    gcoo.seg_planner(planner == "segment")
     try:
         for m, k, n, p, dens in [(1, 1, 4, 1, 1.0), (300, 200, 132, 4, 0.02), (777, 1000, 256, 1, 0.01),
                                  (513, 129, 68, 16, 0.2), (1030, 333, 200, 8, 0.05), (64, 4000, 512, 2, 0.003),
@@ -118,6 +124,42 @@ def test_each_fp32_kernel_bit_exact(gcoo, cuda, oracle, kernel):
             assert np.array_equal(c, c_ref), (kernel, m, k, n, p)
     finally:
         gcoo.force_kernel("auto")
+        gcoo.seg_planner(True)
+
+
+def test_segment_planner_group_sizes_and_row_spread(gcoo, cuda, oracle):
+    """The segment planner across group sizes p = 1 .. 4096 (groups spanning
+    several row blocks when p > RB), three-entry and fp64 records, and the
+    narrow-strip row spreading (rows per block < RB): bit-exact against the
+    oracle and equal to the general planner's C."""
+    import torch
+    rng = np.random.default_rng(91)
+    cases = [("tacc28_k200", np.float32, 0.01), ("tacc28_k128", np.float32, 0.08), ("tacc_v4_k216", np.float32, 0.002),
+             ("tacc28_f64_k160", np.float64, 0.01)]
+    try:
+        for kernel, dt, dens in cases:
+            gcoo.force_kernel(kernel)
+            m, k, n = 2100, 1700, 260 if dt == np.float32 else 130
+            a = rand_dense(rng, m, k, dens, dt)
+            bm = rand_dense(rng, k, n, 1.0, dt)
+            for p in (1, 2, 8, 64, 512, 4096):
+                go = oracle.dense_to_gcoo(a, p)
+                c_ref, _ = oracle.spdm(go, bm, 64, fma=True)
+                for seg in (True, False):
+                    gcoo.seg_planner(seg)
+                    c = gcoo.spdm_gcoo(to_prod(gcoo, go), bm, gcoo.ExecConfig(p=p))
+                    assert np.array_equal(c, c_ref), (kernel, p, seg)
+            # device path on a narrow strip: one column tile, rows spread over more row blocks
+            go = oracle.dense_to_gcoo(a, 4)
+            d = gcoo.dense_to_gcoo_dev(torch.from_numpy(a).cuda(), 4)
+            bn = bm[:, :64].copy()
+            c_ref, _ = oracle.spdm(go, bn, 64, fma=True)
+            cd = torch.empty((m, 64), dtype=torch.from_numpy(bn).dtype, device="cuda")
+            gcoo.spdm_gcoo_dev(d, torch.from_numpy(bn).cuda(), cd)
+            assert np.array_equal(cd.cpu().numpy(), c_ref), kernel
+    finally:
+        gcoo.force_kernel("auto")
+        gcoo.seg_planner(True)
 
 
 def test_f64(gcoo, cuda, oracle):
