@@ -282,6 +282,8 @@ struct SpdmPlan {
   std::unique_ptr<SpdmPlan> heavy;
 };
 
+int split_heavy_deal();
+
 // The segment planner for even A (seg_plan_kernel); 0 = the general chain
 // for every A (test / measurement hook gcoo_debug_seg_planner).
 std::atomic<int> g_seg_planner{1};
@@ -383,9 +385,14 @@ void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ct
       const char* e = std::getenv("GCOO_SPLIT_LIGHT_FIRST");  // measurement hook
       return e ? std::atoi(e) : 0;
     }();
+    static const int heavy_first = [] {
+      const char* e = std::getenv("GCOO_SPLIT_HEAVY_FIRST");  // measurement hook
+      return e ? std::atoi(e) : 1;
+    }();
+    const int deal = lo == 0 ? split_heavy_deal() : 0;
     GCOO_LAUNCH_PDL(place_class_kernel, grid_for(a.m, 256), 256, 0, s, a.m, pos, lo, hi, (int32_t)Cfg::RB,
                     (int32_t)Cfg::NW, (int32_t)Cfg::RW, (int32_t)rpb, P.unit_of.get(), P.row_of.get(), P.skewed.get(),
-                    (int32_t)(lo == 0 ? 1 : light_first));
+                    (int32_t)(lo == 0 ? (deal ? 0 : heavy_first) : light_first), (int32_t)deal);
   } else {
     // load-balanced row placement: heaviest rows first, dealt over a block's warps
     if (a.nnz > 0)
@@ -578,6 +585,20 @@ struct SkewHint {
 
 std::atomic<int> g_force_split{-1};  // test hook: -1 auto, 0 never, 1 whenever A has two classes
 
+// Heavy class placement: 0 = heaviest rows packed into row block 0, whose
+// CTAs launch first (the default); 1 = the ranked rows dealt round-robin over
+// the row blocks (equal blocks, plain CTA order).  Dealing reads B about once
+// from DRAM (configs[3]: heavy kernel 1.10 instead of 2.75 GB) but the step
+// is 8 % slower (8.15 vs 7.56 ms; tools/split_deal.sh): HBM is ~10 % busy
+// here, the long dense-row CTAs starting first is what shortens the tail.
+int split_heavy_deal() {
+  static const int d = [] {
+    const char* e = std::getenv("GCOO_SPLIT_HEAVY_DEAL");  // measurement hook
+    return e ? std::atoi(e) : 0;
+  }();
+  return d;
+}
+
 double split_factor() {
   static const double f = [] {
     const char* e = std::getenv("GCOO_SPLIT_FACTOR");  // measurement hook
@@ -678,7 +699,10 @@ bool make_split_plan(SpdmPlan& P, const DevGcoo<T>& a, const SkewHint& h, int64_
                      const T* B, const T* C, int flavor, cudaStream_t s, int64_t strip_n) {
   if (flavor == GCOO_FLAVOR_MUL_ADD) return false;
   const bool f64 = sizeof(T) == 8;
-  int kh = pick_by_density(h.top_density / (double)a.k, f64);
+  // the heavy plan's chunk depth: its densest row block's segments must fit the record stage
+  const double heavy_dens = split_heavy_deal() ? (double)h.heavy_nnz / ((double)h.heavy_rows * (double)a.k)
+                                               : h.top_density / (double)a.k;
+  int kh = pick_by_density(heavy_dens, f64);
   if (const char* e = std::getenv("GCOO_SPLIT_HEAVY_KIND")) kh = std::atoi(e);  // measurement hook
   const int kl = pick_by_density((double)(a.nnz - h.heavy_nnz) / ((double)(a.m - h.heavy_rows) * (double)a.k), f64);
   bool fits = true;

@@ -533,16 +533,19 @@ __global__ void rank_rows_kernel(int64_t m, const int32_t* __restrict__ row_nnz,
 __global__ void place_class_kernel(int64_t m, const int32_t* __restrict__ pos, int64_t lo, int64_t hi,
                                    int32_t rb_rows, int32_t nw, int32_t rw, int32_t rpb,
                                    int32_t* __restrict__ unit_of, int32_t* __restrict__ row_of,
-                                   int32_t* __restrict__ skew_flag, int32_t first) {
+                                   int32_t* __restrict__ skew_flag, int32_t first, int32_t deal) {
   griddep_wait();  // PDL: predecessor complete
   if (blockIdx.x == 0 && threadIdx.x == 0) *skew_flag = first;
+  const int64_t nblk = (hi - lo + rpb - 1) / rpb;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = pos[r];
     if (p < lo || p >= hi) {
       unit_of[r] = -1;
       continue;
     }
-    const int64_t i = p - lo, blk = i / rpb, j = i % rpb;
+    // deal: ranked rows round-robin over the row blocks (every block as heavy
+    // as the next); else consecutive ranks fill a block (the heaviest first)
+    const int64_t i = p - lo, blk = deal ? i % nblk : i / rpb, j = deal ? i / nblk : i % rpb;
     const int64_t u = blk * rb_rows + (j % nw) * rw + j / nw;
     unit_of[r] = (int32_t)u;
     row_of[u] = (int32_t)r;

@@ -795,6 +795,10 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
     if (lane == 0) {
       const int32_t x = (int32_t)(ct * W);
       int64_t lo = so[0], hi = so[1];
+      // every column tile re-reads the row block's records: keep them in L2
+      // while the B strips stream through (configs[3]: DRAM reads per launch
+      // would otherwise carry the record stream once per column tile)
+      const uint64_t keep = l2_policy_evict_last();
 #if GCOO_PROF
       const long long p0 = clock64();
       long long pw = 0;
@@ -824,7 +828,7 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
         stage_len[s] = len;
         mbar_arrive_expect_tx(&full[s], (any ? Cfg::BTILE : 0u) + bytes);
         if (any) tma_load_2d(stage, &tmap_b, x, c * Cfg::KC, &full[s]);
-        if (bytes) bulk_g2s(smem_u32(stage + Cfg::BTILE), ent + lo, bytes, &full[s]);
+        if (bytes) bulk_g2s_hint(smem_u32(stage + Cfg::BTILE), ent + lo, bytes, &full[s], keep);
         lo = hi;
         hi = hi_next;
       }
