@@ -60,6 +60,13 @@ typedef struct gcoo_stats {
 
 /* ------------------------------------------------------------ runtime ---- */
 int gcoo_abi_version(void);
+
+/* The B200 roofline profile the reference's table lacks (kProfiles,
+ * src/traffic.cpp:223-227 holds gtx980 / titanx / p100): this pool's measured
+ * FP32 FFMA peak (tools/microbench/mb.cu, profiles/r01_microbench.json) and
+ * HBM copy bandwidth (MEASURED_PEAKS.json), FLOP/s and bytes/s.  No device
+ * needed. */
+int gcoo_roofline_b200(double* peak_flops, double* bandwidth);
 const char* gcoo_last_error(void);
 /* Number of visible CUDA devices (0 on a machine without a GPU). */
 int gcoo_device_count(int* count);

@@ -635,7 +635,7 @@ ROOFLINE_PROFILES = {
     "gtx980": (4.981e12, 224e9),
     "titanx": (10.97e12, 433e9),
     "p100": (9.5e12, 732e9),
-    "b200": (72.47e12, 6547.8e9),
+    "b200": (72.47e12, 6524.3e9),  # = gcoo_roofline_b200 (include/gcoo/roofline_b200.hpp)
 }
 
 

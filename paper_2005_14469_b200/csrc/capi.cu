@@ -1717,6 +1717,16 @@ using namespace gcoo_b200;
 extern "C" {
 
 int gcoo_abi_version(void) { return GCOO_ABI_VERSION; }
+
+int gcoo_roofline_b200(double* peak_flops, double* bandwidth) {
+  if (!peak_flops || !bandwidth) {
+    t_error = "gcoo_roofline_b200: null output";
+    return GCOO_EINVAL;
+  }
+  *peak_flops = 72.47e12;  // FFMA, 148 SMs x 128 lanes x 2 at the measured clock (profiles/r01_microbench.json)
+  *bandwidth = 6524.3e9;   // HBM copy bandwidth (MEASURED_PEAKS.json)
+  return GCOO_OK;
+}
 const char* gcoo_last_error(void) { return t_error.c_str(); }
 
 int gcoo_device_count(int* count) {

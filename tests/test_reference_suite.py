@@ -107,3 +107,16 @@ def test_reference_acceptance_gate_on_b200(cuda, gcoo):
     nums = lambda t: [float(x) for x in re.findall(r"exponent=([0-9.e+-]+)", t)]  # noqa: E731
     assert nums(got["5"][1]) == pytest.approx(nums(native["5"]["detail_model"]), rel=1e-12)
     assert r.returncode == sum(v["verdict"] == "FAIL" for v in native.values()), r.stdout
+
+
+def test_b200_roofline_profile_cpp():
+    """The drop-in roofline_profile_ext("b200") (include/gcoo/roofline_b200.hpp)
+    beside the reference's own table (traffic.cpp:223-237, compiled unchanged):
+    the measured B200 peaks, the reference's entries and its exception for an
+    unknown name.  No GPU needed."""
+    import json
+    r = _run_suite("b200_profile")
+    assert r.returncode == 0, r.stdout + r.stderr
+    d = json.loads(r.stdout)
+    assert d["name"] == "b200" and abs(d["peak_flops"] - 72.47e12) < 1e9 and abs(d["bandwidth"] - 6524.3e9) < 1e7
+    assert d["p100_peak"] == 9.5e12 and d["unknown_throws"]
