@@ -98,20 +98,21 @@ def test_random_shapes_bit_exact(gcoo, cuda, oracle, seed):
         assert max_rel(c, c_mad) <= 1e-5
 
 
-@pytest.mark.parametrize("planner", ["segment", "general"])
-@pytest.mark.parametrize("kernel", ["rowtile", "tacc_v4", "tacc28_k192", "tacc28_k160",
-                                    "tacc28_k128", "tacc28_k96", "tacc28_k64", "tacc28_k200", "tacc_v4_k216", "tacc28_k176", "auto"])
+_TACC_FP32 = ["tacc_v4", "tacc28_k192", "tacc28_k160", "tacc28_k128", "tacc28_k96", "tacc28_k64", "tacc28_k200",
+              "tacc_v4_k216", "tacc28_k176", "auto"]
+
+
+@pytest.mark.parametrize("kernel,planner", [("rowtile", "none")] +
+                         [(k, pl) for pl in ("segment", "general") for k in _TACC_FP32])
 def test_each_fp32_kernel_bit_exact(gcoo, cuda, oracle, kernel, planner):
     """Every fp32 kernel variant, on shapes that hit its edges (m not a multiple
     of the row block, k not a multiple of the chunk, n not a multiple of the
     strip, empty rows/tiles, every p the variant supports), with its record
     stream built by the segment planner (even A, the default) and by the
     general count / header / fill chain."""
-    if kernel == "rowtile" and planner == "general":
-        pytest.skip("the row-tile kernel has no planner")
     rng = np.random.default_rng(sorted(gcoo.KERNELS).index(kernel))
     gcoo.force_kernel(kernel)
-    gcoo.seg_planner(planner == "segment")
+    gcoo.seg_planner(planner != "general")  # the row-tile kernel has no planner
     try:
         for m, k, n, p, dens in [(1, 1, 4, 1, 1.0), (300, 200, 132, 4, 0.02), (777, 1000, 256, 1, 0.01),
                                  (513, 129, 68, 16, 0.2), (1030, 333, 200, 8, 0.05), (64, 4000, 512, 2, 0.003),
