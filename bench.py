@@ -205,18 +205,19 @@ def make_inputs(G, n, s, seed, dev, b_seed):
 
 def time_kernel(G, dg, dB, dC, steps, warmup, stream, flush):
     """(mean ms per step, min ms, library launches in the timed region, mean ms
-    of the multiply kernel itself) — CUDA events on `stream`, L2 flushed first."""
+    of the multiply kernel itself) — CUDA events on `stream`, L2 flushed first.
+    The step times come from a pass without the library's kernel-timing events
+    (an event recorded between the planner and the multiply would sit inside
+    their programmatic-dependent-launch chain and add ~9 us to a step); the
+    multiply kernel's own time from a second pass with them."""
     import torch
     cfg = G.ExecConfig(p=dg.p, b=BW)
-    with torch.cuda.stream(stream):
-        for _ in range(warmup):
-            flush.zero_()
-            G.spdm_gcoo_dev(dg, dB, dC, cfg, stream=stream)
-        torch.cuda.synchronize()
+
+    def run(kernel_events):
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         l0 = G.launch_count()
-        G.kernel_timing(True)  # CUDA events around each multiply-kernel launch, same stream
+        G.kernel_timing(kernel_events)
         # the device sleeps ~5 ms first so the host queues the timed steps ahead of it:
         # per-step device times then never include host enqueue latency
         torch.cuda._sleep(int(1e7))
@@ -229,8 +230,16 @@ def time_kernel(G, dg, dB, dC, steps, warmup, stream, flush):
         launches = G.launch_count() - l0
         k_ms, k_n = G.kernel_time()
         G.kernel_timing(False)
-    times = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    return sum(times) / len(times), min(times), launches, k_ms / max(k_n, 1)
+        return [s.elapsed_time(e) for s, e in zip(starts, ends)], launches, k_ms / max(k_n, 1)
+
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            flush.zero_()
+            G.spdm_gcoo_dev(dg, dB, dC, cfg, stream=stream)
+        torch.cuda.synchronize()
+        times, launches, _ = run(False)
+        _, _, kernel_ms = run(True)
+    return sum(times) / len(times), min(times), launches, kernel_ms
 
 
 class Dist:
