@@ -117,6 +117,7 @@ def lib():
     _sig(L, "gcoo_debug_last_split", _int, [])
     _sig(L, "gcoo_debug_force_split", _int, [_int])
     _sig(L, "gcoo_debug_seg_planner", _int, [_int])
+    _sig(L, "gcoo_debug_persistent", _int, [_int])
     _sig(L, "gcoo_plan_create_f32_dev", _int, [_i64, _i64, _i32, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _int,
                                                 C.POINTER(_vp), _vp])
     _sig(L, "gcoo_plan_spdm_f32_dev", _int, [_vp, _i64, _vp, _i64, _vp, _i64, _vp])
@@ -193,6 +194,12 @@ def force_split(mode: str = "auto") -> None:
     """Test hook: the two-class split of skewed matrices ("auto", "never",
     "always" = whenever the rows form two degree classes)."""
     lib().gcoo_debug_force_split({"auto": -1, "never": 0, "always": 1}[mode])
+
+
+def persistent(on: bool = True) -> None:
+    """Test / measurement hook: the TMEM multiply as one persistent CTA per SM
+    walking the tiles, or one CTA per tile."""
+    lib().gcoo_debug_persistent(1 if on else 0)
 
 
 def seg_planner(on: bool = True) -> None:

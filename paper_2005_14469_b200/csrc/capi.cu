@@ -287,6 +287,9 @@ int split_heavy_deal();
 // The segment planner for even A (seg_plan_kernel); 0 = the general chain
 // for every A (test / measurement hook gcoo_debug_seg_planner).
 std::atomic<int> g_seg_planner{1};
+// The multiply kernel as one CTA per tile (0) or one persistent CTA per SM
+// walking the tiles (1; hook gcoo_debug_persistent).
+std::atomic<int> g_persistent{0};
 
 template <class Cfg>
 void set_smem_attr() {
@@ -422,7 +425,10 @@ template <class Cfg, typename T>
 void run_plan(const SpdmPlan& P, const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C,
               int64_t ldc, cudaStream_t s, bool timed = true) {
   const CUtensorMap map = make_b_map(B, a.k, n, ldb, Cfg::W, Cfg::KC);
-  const int64_t grid = P.row_blocks * ceil_div(n, Cfg::W);
+  const int64_t tiles = P.row_blocks * ceil_div(n, Cfg::W);
+  // persistent: one CTA per SM walks the tiles (the next tile's first stages
+  // load while the previous tile is written back)
+  const int64_t grid = g_persistent.load(std::memory_order_relaxed) ? std::min<int64_t>(tiles, sm_count()) : tiles;
   if (grid > INT32_MAX) fail(GCOO_EINVAL, "spdm_gcoo: problem too large for one launch");
   const cudaEvent_t kt0 = timed ? kt_start(s) : nullptr;
   GCOO_LAUNCH_PDL(spdm_tacc_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n,
@@ -1822,6 +1828,11 @@ int gcoo_debug_last_split(void) { return t_last_split ? 1 : 0; }
 // whenever the degree distribution has two classes).
 int gcoo_debug_force_split(int mode) {
   g_force_split.store(mode, std::memory_order_relaxed);
+  return GCOO_OK;
+}
+
+int gcoo_debug_persistent(int on) {
+  g_persistent.store(on ? 1 : 0, std::memory_order_relaxed);
   return GCOO_OK;
 }
 

@@ -772,29 +772,33 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
   tmem_fence_after();
   const uint32_t tbase = *tmem_slot;
   griddep_wait();  // PDL: the planner's record stream is complete
-  // CTA order.  Row blocks vary fastest, so the CTAs co-resident on the GPU
-  // share a few B strips and every B tile crosses HBM once.  A skewed matrix
-  // (*skewed, row_balance_kernel) has its heaviest rows in row block 0: those
-  // CTAs go first so they overlap everything else instead of forming a tail.
-  int64_t rb, ct;
-  if (*skewed && row_blocks > 1 && (int64_t)blockIdx.x < col_tiles) {
-    rb = 0;
-    ct = blockIdx.x;
-  } else if (*skewed && row_blocks > 1) {
-    const int64_t x = (int64_t)blockIdx.x - col_tiles;
-    rb = 1 + x % (row_blocks - 1);
-    ct = x / (row_blocks - 1);
-  } else {
-    rb = (int64_t)blockIdx.x % row_blocks;
-    ct = (int64_t)blockIdx.x / row_blocks;
-  }
-  const int64_t* so = seg_off + rb * nchunks;
+  // Tiles (row block, column tile) in launch order; CTA i takes tiles i,
+  // i + gridDim.x, ... (one each when the grid covers every tile; persistent
+  // otherwise: the producer then streams the next tile's first chunks while
+  // the consumers write the previous tile back).  Row blocks vary fastest, so
+  // the tiles in flight share a few B strips and every B tile crosses HBM
+  // once.  A skewed matrix (*skewed, row_balance_kernel) has its heaviest rows
+  // in row block 0: those tiles go first so they overlap everything else
+  // instead of forming a tail.
+  const int64_t tiles = row_blocks * col_tiles;
+  const bool skew = *skewed && row_blocks > 1;
+  auto tile_of = [&](int64_t t, int64_t& rb, int64_t& ct) {
+    if (skew && t < col_tiles) {
+      rb = 0;
+      ct = t;
+    } else if (skew) {
+      const int64_t x = t - col_tiles;
+      rb = 1 + x % (row_blocks - 1);
+      ct = x / (row_blocks - 1);
+    } else {
+      rb = t % row_blocks;
+      ct = t / row_blocks;
+    }
+  };
 
   if (warp == NW) {
     // ------------- producer: B tile (TMA 2-D) + record segment (bulk 1-D)
     if (lane == 0) {
-      const int32_t x = (int32_t)(ct * W);
-      int64_t lo = so[0], hi = so[1];
       // every column tile re-reads the row block's records: keep them in L2
       // while the B strips stream through (configs[3]: DRAM reads per launch
       // would otherwise carry the record stream once per column tile)
@@ -803,34 +807,42 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
       const long long p0 = clock64();
       long long pw = 0;
 #endif
-      for (int c = 0; c < nchunks; ++c) {
-        const int s = c % S;
-        const int64_t hi_next = so[c + 2 <= nchunks ? c + 2 : nchunks];  // prefetch
-        const uint32_t len = (uint32_t)(hi - lo);
-        const uint32_t bytes = len <= Cfg::CAP ? len : 0u;  // oversize: consumers read global memory
-        // a segment of empty warp headers only: no consumer reads this chunk's B tile
-        const bool any = len > (uint32_t)(Cfg::TABLE + Cfg::NW * Cfg::HDR);
+      uint32_t q = 0;  // chunks issued by this CTA so far: stage q % S, ring round q / S
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int64_t rb, ct;
+        tile_of(t, rb, ct);
+        const int64_t* so = seg_off + rb * nchunks;
+        const int32_t x = (int32_t)(ct * W);
+        int64_t lo = so[0], hi = so[1];
+        for (int c = 0; c < nchunks; ++c, ++q) {
+          const int s = (int)(q % S);
+          const int64_t hi_next = so[c + 2 <= nchunks ? c + 2 : nchunks];  // prefetch
+          const uint32_t len = (uint32_t)(hi - lo);
+          const uint32_t bytes = len <= Cfg::CAP ? len : 0u;  // oversize: consumers read global memory
+          // a segment of empty warp headers only: no consumer reads this chunk's B tile
+          const bool any = len > (uint32_t)(Cfg::TABLE + Cfg::NW * Cfg::HDR);
 #if GCOO_PROF
-        const long long w0 = clock64();
+          const long long w0 = clock64();
 #endif
-        if (c >= S) {
+          if (q >= S) {
 #if GCOO_PRODUCER_HINT_NS
-          mbar_wait_sleep(&empty[s], (uint32_t)((c / S) - 1) & 1u, GCOO_PRODUCER_HINT_NS);
+            mbar_wait_sleep(&empty[s], (q / S - 1) & 1u, GCOO_PRODUCER_HINT_NS);
 #else
-          mbar_wait(&empty[s], (uint32_t)((c / S) - 1) & 1u);
+            mbar_wait(&empty[s], (q / S - 1) & 1u);
 #endif
-        }
+          }
 #if GCOO_PROF
-        pw += clock64() - w0;
+          pw += clock64() - w0;
 #endif
-        unsigned char* stage = smem_raw + (size_t)s * Cfg::STAGE_BYTES;
-        stage_lo[s] = lo;
-        stage_len[s] = len;
-        mbar_arrive_expect_tx(&full[s], (any ? Cfg::BTILE : 0u) + bytes);
-        if (any) tma_load_2d(stage, &tmap_b, x, c * Cfg::KC, &full[s]);
-        if (bytes) bulk_g2s_hint(smem_u32(stage + Cfg::BTILE), ent + lo, bytes, &full[s], keep);
-        lo = hi;
-        hi = hi_next;
+          unsigned char* stage = smem_raw + (size_t)s * Cfg::STAGE_BYTES;
+          stage_lo[s] = lo;
+          stage_len[s] = len;
+          mbar_arrive_expect_tx(&full[s], (any ? Cfg::BTILE : 0u) + bytes);
+          if (any) tma_load_2d(stage, &tmap_b, x, c * Cfg::KC, &full[s]);
+          if (bytes) bulk_g2s_hint(smem_u32(stage + Cfg::BTILE), ent + lo, bytes, &full[s], keep);
+          lo = hi;
+          hi = hi_next;
+        }
       }
 #if GCOO_PROF
       GCOO_PROF_ADD(3, pw);
@@ -843,97 +855,107 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
   // ------------------------------------------------------------ consumers
   // my accumulators: TMEM lanes 32*(warp%4).., columns (warp/4)*TCOLS + slot*V + v
   const uint32_t tacc = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * Cfg::TCOLS);
-#pragma unroll
-  for (int c0 = 0; c0 < Cfg::TCOLS; c0 += 8) tmem_st8_zero(tacc + c0);
-  tmem_wait_st();
-
-  float acc[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) acc[v] = 0.f;
-  uint32_t cur = 0;  // slot 0, zero accumulators (see tacc_switch)
+  uint32_t q = 0;  // chunks consumed by this CTA so far (the producer's count)
 #if GCOO_PROF
   if (lane == 0) g_prof_swaps[warp] = g_prof_recs[warp] = 0;
   __syncwarp();
-  const long long q0 = clock64();
-  long long qw = 0;
+  long long qw = 0, qloop = 0, qepi = 0;
 #endif
-
-  for (int c = 0; c < nchunks; ++c) {
-    const int s_idx = c % S;
-#if GCOO_PROF
-    const long long w0 = clock64();
-    mbar_wait(&full[s_idx], (uint32_t)(c / S) & 1u);
-    qw += clock64() - w0;
-#else
-    mbar_wait(&full[s_idx], (uint32_t)(c / S) & 1u);
-#endif
-    tmem_wait_st();  // slots pushed during earlier chunks are complete before they are pulled again
-    const uint32_t stage = smem0 + (uint32_t)s_idx * Cfg::STAGE_BYTES;
-    const uint32_t bbase = stage + (uint32_t)(lane * V * 4);
-    const int64_t lo = stage_lo[s_idx];
-    if (stage_len[s_idx] <= Cfg::CAP) {
-      if constexpr (Cfg::EPR == 1)
-        tacc_consume1<Cfg, false>(acc, cur, tacc, stage + Cfg::BTILE, warp, bbase);
-      else if constexpr (Cfg::EPR == 3)
-        tacc_consume3<Cfg, false>(acc, cur, tacc, stage + Cfg::BTILE, warp, bbase);
-      else
-        tacc_consume<Cfg, false>(acc, cur, tacc, stage + Cfg::BTILE, warp, bbase);
-    } else {
-      if constexpr (Cfg::EPR == 1)
-        tacc_consume1<Cfg, true>(acc, cur, tacc, ent + lo, warp, bbase);
-      else if constexpr (Cfg::EPR == 3)
-        tacc_consume3<Cfg, true>(acc, cur, tacc, ent + lo, warp, bbase);
-      else
-        tacc_consume<Cfg, true>(acc, cur, tacc, ent + lo, warp, bbase);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s_idx]);
-  }
-  tmem_st<V>(tacc + cur * V, acc);
-  tmem_wait_st();
-#if GCOO_PROF
-  const long long q1 = clock64();
-#endif
-
-  // read back and single write of the tile: slot s, value v at column s*V + v
-  const int64_t row0 = (rb * NW + warp) * (int64_t)RW;
-  const int64_t j = ct * W + lane * Cfg::VE;  // first element (column) of this lane
-#pragma unroll 1
-  for (int c0 = 0; c0 < Cfg::TCOLS; c0 += 8) {
-    float r[8];
-    tmem_ld8(tacc + c0, r);
-    tmem_wait_ld();
-    if (j < n) {
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    int64_t rb, ct;
+    tile_of(t, rb, ct);
+    // this tile's accumulators start at zero (the previous tile's were read back)
 #pragma unroll
-      for (int k = 0; k < 8 / V; ++k) {
-        const int64_t row = row_of[row0 + c0 / V + k];  // -1: padding slot
-        if (row >= 0) {
-          typename Cfg::E* dst = C + row * ldc + j;
-          if constexpr (V == 4) {  // 16 bytes: four floats or two doubles
-            __stcs(reinterpret_cast<float4*>(dst), make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]));
-          } else if constexpr (V == 2) {
-            __stcs(reinterpret_cast<float2*>(dst), make_float2(r[2 * k], r[2 * k + 1]));
-          } else {
-            __stcs(dst, r[k]);
+    for (int c0 = 0; c0 < Cfg::TCOLS; c0 += 8) tmem_st8_zero(tacc + c0);
+    tmem_wait_st();
+    float acc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = 0.f;
+    uint32_t cur = 0;  // slot 0, zero accumulators (see tacc_switch)
+#if GCOO_PROF
+    const long long q0 = clock64();
+#endif
+    for (int c = 0; c < nchunks; ++c, ++q) {
+      const int s_idx = (int)(q % S);
+#if GCOO_PROF
+      const long long w0 = clock64();
+      mbar_wait(&full[s_idx], (q / S) & 1u);
+      qw += clock64() - w0;
+#else
+      mbar_wait(&full[s_idx], (q / S) & 1u);
+#endif
+      tmem_wait_st();  // slots pushed during earlier chunks are complete before they are pulled again
+      const uint32_t stage = smem0 + (uint32_t)s_idx * Cfg::STAGE_BYTES;
+      const uint32_t bbase = stage + (uint32_t)(lane * V * 4);
+      const int64_t lo = stage_lo[s_idx];
+      if (stage_len[s_idx] <= Cfg::CAP) {
+        if constexpr (Cfg::EPR == 1)
+          tacc_consume1<Cfg, false>(acc, cur, tacc, stage + Cfg::BTILE, warp, bbase);
+        else if constexpr (Cfg::EPR == 3)
+          tacc_consume3<Cfg, false>(acc, cur, tacc, stage + Cfg::BTILE, warp, bbase);
+        else
+          tacc_consume<Cfg, false>(acc, cur, tacc, stage + Cfg::BTILE, warp, bbase);
+      } else {
+        if constexpr (Cfg::EPR == 1)
+          tacc_consume1<Cfg, true>(acc, cur, tacc, ent + lo, warp, bbase);
+        else if constexpr (Cfg::EPR == 3)
+          tacc_consume3<Cfg, true>(acc, cur, tacc, ent + lo, warp, bbase);
+        else
+          tacc_consume<Cfg, true>(acc, cur, tacc, ent + lo, warp, bbase);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s_idx]);
+    }
+    tmem_st<V>(tacc + cur * V, acc);
+    tmem_wait_st();
+#if GCOO_PROF
+    const long long q1 = clock64();
+    qloop += q1 - q0;
+    if (lane == 0 && *skewed && rb == 0) {
+      GCOO_PROF_ADD(8, q1 - q0);
+      GCOO_PROF_ADD(9, 1);
+    }
+    if (lane == 0) atomicMax(&g_prof[10], (unsigned long long)(q1 - q0));
+#endif
+
+    // read back and single write of the tile: slot s, value v at column s*V + v
+    const int64_t row0 = (rb * NW + warp) * (int64_t)RW;
+    const int64_t j = ct * W + lane * Cfg::VE;  // first element (column) of this lane
+#pragma unroll 1
+    for (int c0 = 0; c0 < Cfg::TCOLS; c0 += 8) {
+      float r[8];
+      tmem_ld8(tacc + c0, r);
+      tmem_wait_ld();
+      if (j < n) {
+#pragma unroll
+        for (int k = 0; k < 8 / V; ++k) {
+          const int64_t row = row_of[row0 + c0 / V + k];  // -1: padding slot
+          if (row >= 0) {
+            typename Cfg::E* dst = C + row * ldc + j;
+            if constexpr (V == 4) {  // 16 bytes: four floats or two doubles
+              __stcs(reinterpret_cast<float4*>(dst), make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]));
+            } else if constexpr (V == 2) {
+              __stcs(reinterpret_cast<float2*>(dst), make_float2(r[2 * k], r[2 * k + 1]));
+            } else {
+              __stcs(dst, r[k]);
+            }
           }
         }
       }
     }
+#if GCOO_PROF
+    qepi += clock64() - q1;
+#endif
   }
 
 #if GCOO_PROF
   if (lane == 0) {
     GCOO_PROF_ADD(0, qw);
-    GCOO_PROF_ADD(1, q1 - q0);
-    GCOO_PROF_ADD(2, clock64() - q1);
+    GCOO_PROF_ADD(1, qloop);
+    GCOO_PROF_ADD(2, qepi);
     GCOO_PROF_ADD(5, 1);
     GCOO_PROF_ADD(6, g_prof_recs[warp]);
     GCOO_PROF_ADD(7, g_prof_swaps[warp]);
-    if (*skewed && rb == 0) {
-      GCOO_PROF_ADD(8, q1 - q0);
-      GCOO_PROF_ADD(9, 1);
-    }
-    atomicMax(&g_prof[10], (unsigned long long)(q1 - q0));
   }
 #endif
   // free TMEM once every consumer warp is done with it
