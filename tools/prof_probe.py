@@ -13,7 +13,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-VARIANT = os.path.join(ROOT, "tools", "_abl", "libgcoo_prof.so")
+VARIANT = os.environ.get("GCOO_PROF_LIB", os.path.join(ROOT, "tools", "_abl", "libgcoo_prof.so"))
 
 
 def main():
@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--kernel", nargs="+", default=["auto"])
     ap.add_argument("--powerlaw", action="store_true")
     ap.add_argument("--build", action="store_true")
+    ap.add_argument("--persistent", action="store_true", help="one persistent CTA per SM (even A)")
     args = ap.parse_args()
     if args.build:
         from paper_2005_14469_b200 import build
@@ -33,6 +34,8 @@ def main():
     import torch
     import paper_2005_14469_b200 as G
     L = G.lib()
+    if args.persistent:
+        G.persistent(True)
     L.gcoo_debug_prof.restype = C.c_int
     L.gcoo_debug_prof.argtypes = [C.c_void_p, C.c_int]
     buf = (C.c_ulonglong * 12)()
