@@ -54,6 +54,10 @@ _lib = None
 
 
 def _sig(L, name, res, args):
+    # test / measurement hooks may be absent from a measurement variant's
+    # library (GCOO_LIB); every other entry point is required
+    if name.startswith("gcoo_debug_") and os.environ.get("GCOO_LIB") and not hasattr(L, name):
+        return
     f = getattr(L, name)
     f.restype = res
     f.argtypes = args

@@ -276,6 +276,7 @@ struct SpdmPlan {
   // TMEM kernels: row placement (original row -> unit row, and back; -1 = padding)
   DevBuf<int32_t> unit_of, row_of;
   DevBuf<int32_t> skewed;  // 1: heaviest rows in row block 0 (launched first)
+  bool even = false;       // identity placement: tiles of about equal work (persistent launch)
   // two-class split of a skewed A (split_plan): this plan holds the light rows,
   // `heavy` the heaviest rows with a configuration chosen for their density;
   // the two multiply kernels write disjoint rows of C and run concurrently
@@ -287,9 +288,11 @@ int split_heavy_deal();
 // The segment planner for even A (seg_plan_kernel); 0 = the general chain
 // for every A (test / measurement hook gcoo_debug_seg_planner).
 std::atomic<int> g_seg_planner{1};
-// The multiply kernel as one CTA per tile (0) or one persistent CTA per SM
-// walking the tiles (1; hook gcoo_debug_persistent).
-std::atomic<int> g_persistent{0};
+// The multiply kernel for even A as one persistent CTA per SM walking the
+// tiles (1, default: n=8000 steps s=0.99 0.875 -> 0.862 ms, 0.995 0.524 ->
+// 0.513, 0.998 0.353 -> 0.341) or one CTA per tile (0; hook
+// gcoo_debug_persistent).  Skewed A always runs one CTA per tile.
+std::atomic<int> g_persistent{1};
 
 template <class Cfg>
 void set_smem_attr() {
@@ -329,6 +332,7 @@ void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ct
   const int nchunks = P.nchunks;
   const int64_t nseg = P.row_blocks * nchunks;
   const bool ident = even && !pos;
+  P.even = ident;
   if (ident && g_seg_planner.load(std::memory_order_relaxed)) {
     // even A: the segment planner (count pass, scan, build pass) straight from the GCOO
     P.unit_of = DevBuf<int32_t>(a.m, s);
@@ -426,9 +430,12 @@ void run_plan(const SpdmPlan& P, const DevGcoo<T>& a, int64_t n, const T* B, int
               int64_t ldc, cudaStream_t s, bool timed = true) {
   const CUtensorMap map = make_b_map(B, a.k, n, ldb, Cfg::W, Cfg::KC);
   const int64_t tiles = P.row_blocks * ceil_div(n, Cfg::W);
-  // persistent: one CTA per SM walks the tiles (the next tile's first stages
-  // load while the previous tile is written back)
-  const int64_t grid = g_persistent.load(std::memory_order_relaxed) ? std::min<int64_t>(tiles, sm_count()) : tiles;
+  // persistent for even A: one CTA per SM walks the tiles in launch order (the
+  // next tile's first stages load while the previous tile is written back);
+  // tiles of unequal work (skewed placement, the split's classes) keep one CTA
+  // per tile so the hardware scheduler balances them
+  const int64_t grid =
+      P.even && g_persistent.load(std::memory_order_relaxed) ? std::min<int64_t>(tiles, sm_count()) : tiles;
   if (grid > INT32_MAX) fail(GCOO_EINVAL, "spdm_gcoo: problem too large for one launch");
   const cudaEvent_t kt0 = timed ? kt_start(s) : nullptr;
   GCOO_LAUNCH_PDL(spdm_tacc_kernel<Cfg>, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, map, a.m, n,

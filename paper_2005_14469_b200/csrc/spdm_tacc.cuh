@@ -856,6 +856,10 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
   // my accumulators: TMEM lanes 32*(warp%4).., columns (warp/4)*TCOLS + slot*V + v
   const uint32_t tacc = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * Cfg::TCOLS);
   uint32_t q = 0;  // chunks consumed by this CTA so far (the producer's count)
+  // the shared-memory window base and this lane's offset stay in registers
+  // (ptxas otherwise rematerialises them from special registers every chunk)
+  uint32_t sbase = smem0 + (uint32_t)(lane * V * 4);
+  asm volatile("mov.b32 %0, %0;" : "+r"(sbase));
 #if GCOO_PROF
   if (lane == 0) g_prof_swaps[warp] = g_prof_recs[warp] = 0;
   __syncwarp();
@@ -885,8 +889,8 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
       mbar_wait(&full[s_idx], (q / S) & 1u);
 #endif
       tmem_wait_st();  // slots pushed during earlier chunks are complete before they are pulled again
-      const uint32_t stage = smem0 + (uint32_t)s_idx * Cfg::STAGE_BYTES;
-      const uint32_t bbase = stage + (uint32_t)(lane * V * 4);
+      const uint32_t bbase = sbase + (uint32_t)s_idx * Cfg::STAGE_BYTES;
+      const uint32_t stage = bbase - (uint32_t)(lane * V * 4);
       const int64_t lo = stage_lo[s_idx];
       if (stage_len[s_idx] <= Cfg::CAP) {
         if constexpr (Cfg::EPR == 1)

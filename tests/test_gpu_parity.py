@@ -113,7 +113,7 @@ def test_each_fp32_kernel_bit_exact(gcoo, cuda, oracle, kernel, planner):
     rng = np.random.default_rng(sorted(gcoo.KERNELS).index(kernel))
     gcoo.force_kernel(kernel)
     gcoo.seg_planner(planner != "general")  # the row-tile kernel has no planner
-    gcoo.persistent(planner == "persistent")  # one persistent CTA per SM walking the tiles
+    gcoo.persistent(planner == "persistent")  # one persistent CTA per SM walking the tiles (default) or one per tile
     try:
         for m, k, n, p, dens in [(1, 1, 4, 1, 1.0), (300, 200, 132, 4, 0.02), (777, 1000, 256, 1, 0.01),
                                  (513, 129, 68, 16, 0.2), (1030, 333, 200, 8, 0.05), (64, 4000, 512, 2, 0.003),
@@ -127,7 +127,7 @@ def test_each_fp32_kernel_bit_exact(gcoo, cuda, oracle, kernel, planner):
     finally:
         gcoo.force_kernel("auto")
         gcoo.seg_planner(True)
-        gcoo.persistent(False)
+        gcoo.persistent(True)
 
 
 def test_segment_planner_group_sizes_and_row_spread(gcoo, cuda, oracle):
