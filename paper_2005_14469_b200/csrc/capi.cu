@@ -739,8 +739,10 @@ bool make_split_plan(SpdmPlan& P, const DevGcoo<T>& a, const SkewHint& h, int64_
   P.heavy->kind = kh;
   with_cfg<T>(kh, [&](auto c) {
     using Cfg = decltype(c);
-    // the heavy class is small: spread it over at least one wave of CTAs
-    build_plan<Cfg>(*P.heavy, a, s, sm_count(), ceil_div(strip_n ? strip_n : n, Cfg::W), pos.get(), 0,
+    // the heavy class is small: spread it over at least one wave of CTAs for
+    // the width it will serve (strip_n = 0: a reusable plan, width unknown —
+    // full row blocks)
+    build_plan<Cfg>(*P.heavy, a, s, strip_n ? sm_count() : 0, ceil_div(strip_n, Cfg::W), pos.get(), 0,
                     h.heavy_rows);
   });
   return true;

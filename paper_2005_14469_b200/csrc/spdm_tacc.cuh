@@ -474,24 +474,12 @@ seg_plan_kernel(int64_t m, int64_t nnz, int32_t p, const typename Cfg::E* __rest
           }
         }
       }
-      __syncthreads();
-      for (int32_t i = tid; i < total; i += kSegThreads) {
-        int64_t e;
-        int g;
-        locate(i, e, g);
-        const int32_t r = cached ? sm.row[i] : rows[e];
-        if (r < r0 || r >= r1) continue;
-        // rank among the row's entries of this chunk: same-row entries earlier in the range
-        uint32_t rank = 0;
-        if (cached) {
-          for (int32_t jx = sm.pre[g]; jx < i; ++jx) rank += sm.row[jx] == r;
-        } else {
-          for (int64_t jx = sm.lo[g]; jx < e; ++jx) rank += rows[jx] == r;
-        }
+      // entry e (row r of this block, column col) at its rank among row r's
+      // entries of this chunk
+      auto emit = [&](int64_t e, int32_t r, uint32_t rank, int32_t col) {
         const int64_t j = r - r0;
         const uint32_t slot = (uint32_t)(j / NW);
         const uint32_t bse = sm.base[(j % NW) * RW + slot];
-        const int32_t col = cached ? sm.col[i] : cols[e];
         if constexpr (EPR == 1) {
           uint32_t* word = reinterpret_cast<uint32_t*>(seg + bse + (int64_t)Cfg::REC * rank);
           const double v = (double)vals[e];
@@ -508,6 +496,52 @@ seg_plan_kernel(int64_t m, int64_t nnz, int32_t p, const typename Cfg::E* __rest
           const uint32_t h = (uint32_t)(ve & 1);
           word[h] = __float_as_uint((float)vals[e]);
           word[2 + h] = ((uint32_t)(col - lo_col) * Cfg::ROWB) | (slot << 24);
+        }
+      };
+      if (total <= 32 * ng) {
+        // short group ranges (small p): one thread per entry, its rank by
+        // counting same-row entries earlier in its group's range
+        __syncthreads();
+        for (int32_t i = tid; i < total; i += kSegThreads) {
+          int64_t e;
+          int g;
+          locate(i, e, g);
+          const int32_t r = cached ? sm.row[i] : rows[e];
+          if (r < r0 || r >= r1) continue;
+          uint32_t rank = 0;
+          if (cached) {
+            for (int32_t jx = sm.pre[g]; jx < i; ++jx) rank += sm.row[jx] == r;
+          } else {
+            for (int64_t jx = sm.lo[g]; jx < e; ++jx) rank += rows[jx] == r;
+          }
+          emit(e, r, rank, cached ? sm.col[i] : cols[e]);
+        }
+      } else {
+        // long group ranges (large p): one warp per group range, 32 entries
+        // at a time — a row's entries in the batch rank by lane order
+        // (match_any) after its running count, which the row's last lane
+        // advances; rows belong to one group, so no other warp touches them
+        __syncthreads();  // the bases are read; cnt becomes the running counts
+        for (int q2 = tid; q2 < NW * RW; q2 += kSegThreads) sm.cnt[q2] = 0u;
+        __syncthreads();
+        const int wid = tid >> 5, ln = tid & 31;
+        for (int g = wid; g < ng; g += kSegThreads / 32) {
+          const int32_t i0 = sm.pre[g], i1 = sm.pre[g + 1];
+          for (int32_t b0 = i0; b0 < i1; b0 += 32) {
+            const int32_t i = b0 + ln;
+            const int64_t e = sm.lo[g] + (i - i0);
+            int32_t r = -1;
+            if (i < i1) r = cached ? sm.row[i] : rows[e];
+            const bool mine = r >= r0 && r < r1;
+            const unsigned same = __match_any_sync(0xffffffffu, mine ? r : -1 - ln);
+            const int64_t j = r - r0;
+            const int sidx = mine ? (int)((j % NW) * RW + j / NW) : 0;
+            const uint32_t rank = mine ? sm.cnt[sidx] + (uint32_t)__popc(same & ((1u << ln) - 1u)) : 0u;
+            __syncwarp();
+            if (mine && (same >> ln) == 1u) sm.cnt[sidx] += (uint32_t)__popc(same);
+            __syncwarp();
+            if (mine) emit(e, r, rank, cached ? sm.col[i] : cols[e]);
+          }
         }
       }
     }

@@ -292,6 +292,23 @@ def test_concurrent_host_calls_are_independent(gcoo, cuda, oracle):
         assert np.array_equal(c, c_ref)
 
 
+@pytest.mark.parametrize("p", [128, 1024])
+def test_large_group_size_bit_exact(gcoo, cuda, oracle, p):
+    """Large p: a group spans several row blocks and a chunk's range inside a
+    group slice holds hundreds of entries (the planner ranks them one warp per
+    range); C bit-exact against the oracle, the multiply on a TMEM kernel."""
+    rng = np.random.default_rng(p)
+    m, k, n = 2600, 3000, 4096  # above the small-product gate: the TMEM kernel runs
+    a = rand_dense(rng, m, k, 0.01)
+    bm = rand_dense(rng, k, n, 1.0)
+    go = oracle.dense_to_gcoo(a, p)
+    c_ref, st_ref = oracle.spdm(go, bm, 64, fma=True)
+    st = gcoo.KernelStats()
+    c = gcoo.spdm_gcoo(to_prod(gcoo, go), bm, gcoo.ExecConfig(p=p), stats=st)
+    assert np.array_equal(c, c_ref)
+    assert (st.flops, st.b_loads_total, st.b_loads_reused, st.staging_fills) == st_ref
+    assert gcoo.last_kernel().startswith("tacc")
+
 def test_plan_execute_split_bit_exact(gcoo, cuda, oracle):
     """gcoo_plan_*: one plan, many multiplies (different B widths, a strided
     column shard, an unaligned shard that needs another kernel class) — every
