@@ -166,7 +166,7 @@ def set_device(device: int) -> None:
     _check(lib().gcoo_set_device(device))
 
 
-KERNELS = {"auto": -1, "rowtile": 0, "tacc_v4": 8, "tacc28_k192": 11, "tacc28_k160": 12,
+KERNELS = {"auto": -1, "rowtile": 0, "tacc28_k192": 11, "tacc28_k160": 12,
            "tacc28_k128": 13, "tacc28_k96": 14, "tacc28_k64": 15, "tacc28_k200": 16, "tacc_v4_k216": 17, "tacc28_k176": 18,
            "tacc28_f64_k160": 20, "tacc28_f64_k96": 21, "tacc28_f64_k64": 22}
 

@@ -450,7 +450,6 @@ template <typename T, typename Fn>
 bool with_cfg(int kind, Fn&& fn) {
   if constexpr (std::is_same<T, float>::value) {
     switch (kind) {
-      case 8: fn(TaccV4{}); return true;
       case 11: fn(Tacc28K192{}); return true;
       case 12: fn(Tacc28K160{}); return true;
       case 13: fn(Tacc28K128{}); return true;
@@ -475,12 +474,12 @@ bool with_cfg(int kind, Fn&& fn) {
 // by density), the row-tile kernel for everything else.
 std::atomic<int> g_force_kernel{-1};  // test hook: -1 auto, 0 row-tile, else a configuration id
 
-// measured crossovers at n=8000 (profiles/r01_kernel_sweep_28w.jsonl): TMEM accumulators
-// with 28 warps everywhere, the chunk depth shrinking as the density grows (the record
-// stage must hold a chunk's records); 16 warps at the sparse end
-// (profiles/r01_kernel_sweep_kc.jsonl: a deeper chunk with a smaller record stage where
-// the stage still holds a chunk's records — KC 200 / 12 KB at 0.35-1.1 %, 16 warps with
-// KC 216 / 4 KB up to 0.22 %)
+// measured crossovers at n=8000 (profiles/r01_kernel_sweep_28w.jsonl; round 2 with the
+// persistent launch: profiles/r02_kernel_sweep_persistent.jsonl, auto within 0.3 % of
+// the best configuration from s=0.9 to 0.999): TMEM accumulators with 28 warps, the chunk
+// depth shrinking as the density grows (the record stage must hold a chunk's records);
+// a deeper chunk with a smaller record stage where the stage still holds a chunk's
+// records (KC 200 / 12 KB at 0.27-1.1 %); 16 warps with KC 216 / 4 KB below 0.27 %
 int pick_by_density(double density, bool f64) {
   if (f64) return density >= 0.07 ? 22 : density >= 0.025 ? 21 : 20;
   return density >= 0.3      ? 15
@@ -489,8 +488,7 @@ int pick_by_density(double density, bool f64) {
          : density >= 0.035  ? 12
          : density >= 0.017  ? 18
          : density >= 0.011  ? 11
-         : density >= 0.0035 ? 16
-         : density >= 0.0022 ? 8
+         : density >= 0.0027 ? 16
                              : 17;
 }
 

@@ -87,7 +87,6 @@ struct TaccCfg {
 };
 
 //                      V  KC   S  CAP
-using TaccV4 = TaccCfg<4, 192, 2, 16384>;   // W=128, RB=512, 16 warps: density 0.22 % .. 0.35 %
 // 28 consumer warps (RB=504): the chunk depth KC trades run length (swaps per
 // entry) against the record-stage capacity, which must hold a row block's
 // records for one chunk (an oversize segment is read from global memory):

@@ -98,7 +98,7 @@ def test_random_shapes_bit_exact(gcoo, cuda, oracle, seed):
         assert max_rel(c, c_mad) <= 1e-5
 
 
-_TACC_FP32 = ["tacc_v4", "tacc28_k192", "tacc28_k160", "tacc28_k128", "tacc28_k96", "tacc28_k64", "tacc28_k200",
+_TACC_FP32 = ["tacc28_k192", "tacc28_k160", "tacc28_k128", "tacc28_k96", "tacc28_k64", "tacc28_k200",
               "tacc_v4_k216", "tacc28_k176", "auto"]
 
 

@@ -23,7 +23,7 @@ def main():
     ap.add_argument("--n", type=int, default=8000)
     ap.add_argument("--s", type=float, nargs="+", default=[0.9, 0.99, 0.995])
     ap.add_argument("--kernels", nargs="+", default=["auto", "tacc28_k200", "tacc28_k192", "tacc28_k160", "tacc28_k128",
-                                                       "tacc28_k96", "tacc28_k64", "tacc_v4", "tacc_v4_k216", "rowtile"])
+                                                       "tacc28_k96", "tacc28_k64", "tacc_v4_k216", "rowtile"])
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--powerlaw", action="store_true", help="BASELINE configs[3]: power-law A (n=16384 default)")
     args = ap.parse_args()

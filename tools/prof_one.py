@@ -1,6 +1,6 @@
 """Run one spdm launch configuration for ncu (no timing printed: profiler runs are not bench numbers).
 
-    python tools/prof_one.py --s 0.99 --kernel tacc_v4 --launches 2 [--powerlaw] [--n 8000]
+    python tools/prof_one.py --s 0.99 --kernel tacc28_k200 --launches 2 [--powerlaw] [--n 8000]
 """
 import argparse
 import os
