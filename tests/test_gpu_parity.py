@@ -758,7 +758,7 @@ def test_output_beyond_2g_elements_bit_exact(gcoo, cuda, oracle):
     del dC
 
 
-@pytest.mark.parametrize("kernel", ["tacc_v4", "tacc28_k192", "tacc28_k64", "tacc28_k200", "tacc_v4_k216", "tacc28_k176"])
+@pytest.mark.parametrize("kernel", ["tacc28_k192", "tacc28_k64", "tacc28_k200", "tacc_v4_k216", "tacc28_k176"])
 def test_heavy_rows_balanced_placement(gcoo, cuda, oracle, kernel):
     """The TMEM kernels place rows heaviest-first across warps (a permutation
     of rows into accumulator slots): with very uneven rows C must still be
