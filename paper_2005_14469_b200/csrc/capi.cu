@@ -367,6 +367,8 @@ void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ct
   P.ent = DevBuf<unsigned char>(bound, s);
   DevBuf<int64_t> slot_pos(nseg * Cfg::NW * Cfg::RW, s);
   DevBuf<uint32_t> woff(nseg * Cfg::NW, s);  // warp segment offsets inside a segment
+  // every group slice's chunk boundaries (fill by chunk range, p <= kFillRangeMaxP)
+  DevBuf<int64_t> tab(a.p <= kFillRangeMaxP && a.nnz > 0 ? a.groups * (nchunks + 1) : 0, s);
 
   const int64_t init_n = std::max<int64_t>((int64_t)cnt.count, std::max<int64_t>(a.m, (int64_t)P.row_of.count));
   IdentPlace ip;
@@ -420,9 +422,20 @@ void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ct
   GCOO_LAUNCH_PDL(tacc_header_kernel<Cfg>, grid_for(nseg * Cfg::NW * Cfg::RW, 256), 256, 0, s,
                   (const uint32_t*)cnt.get(), units, nchunks, nseg, (const int64_t*)P.seg_off.get(),
                   (const uint32_t*)woff.get(), P.ent.get(), slot_pos.get());
-  if (a.nnz > 0)
-    GCOO_LAUNCH_PDL(tacc_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols,
-                    a.gidx, nchunks, (const int64_t*)slot_pos.get(), P.ent.get(), (const int32_t*)P.unit_of.get());
+  if (a.nnz > 0) {
+    if (a.p <= kFillRangeMaxP) {
+      // ranks by (group, chunk) range: linear in the range (the per-entry scan is quadratic in it)
+      GCOO_LAUNCH_PDL(chunk_table_kernel, grid_for(std::max(a.nnz, a.groups), 256), 256, 0, s, a.nnz, a.p,
+                      a.groups, a.rows, a.cols, a.gidx, a.gnnz, (int32_t)Cfg::KC, nchunks, tab.get());
+      GCOO_LAUNCH_PDL(tacc_fill_range_kernel<Cfg>, grid_for(a.groups * nchunks * 32, kFillRangeWarps * 32),
+                      kFillRangeWarps * 32, 0, s, a.m, a.p, a.groups, a.vals, a.rows, a.cols, a.gidx,
+                      (const int64_t*)tab.get(), nchunks, (const int64_t*)slot_pos.get(), P.ent.get(),
+                      (const int32_t*)P.unit_of.get());
+    } else {
+      GCOO_LAUNCH_PDL(tacc_fill_kernel<Cfg>, grid_for(a.nnz, 256), 256, 0, s, a.nnz, a.p, a.vals, a.rows, a.cols,
+                      a.gidx, nchunks, (const int64_t*)slot_pos.get(), P.ent.get(), (const int32_t*)P.unit_of.get());
+    }
+  }
 }
 
 template <class Cfg, typename T>

@@ -275,6 +275,85 @@ __global__ void tacc_fill_kernel(int64_t nnz, int32_t p, const typename Cfg::E* 
   }
 }
 
+// P5 by chunk range (general chain, p <= kFillRangeMaxP): one warp per
+// (group, chunk) — the chunk's entries of a group slice are one contiguous
+// (col,row)-sorted range (chunk_table_kernel) — 32 entries at a time, a row's
+// entries ranked by lane order (match_any) after its running count in the
+// range, kept in shared memory per warp (a tag per row names the range the
+// count belongs to, so nothing is cleared).  Linear in the range, where the
+// per-entry scan of tacc_fill_kernel is quadratic in it.
+constexpr int kFillRangeMaxP = 256;
+constexpr int kFillRangeWarps = 8;
+
+template <class Cfg>
+__global__ void __launch_bounds__(kFillRangeWarps * 32)
+tacc_fill_range_kernel(int64_t m, int32_t p, int64_t groups, const typename Cfg::E* __restrict__ vals,
+                       const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
+                       const int64_t* __restrict__ gidx, const int64_t* __restrict__ tab, int nchunks,
+                       const int64_t* __restrict__ slot_pos, unsigned char* __restrict__ ent,
+                       const int32_t* __restrict__ unit_of) {
+  __shared__ int64_t s_tag[kFillRangeWarps][kFillRangeMaxP];
+  __shared__ uint32_t s_cnt[kFillRangeWarps][kFillRangeMaxP];
+  griddep_wait();  // PDL: predecessor complete
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int q = lane; q < p; q += 32) s_tag[wl][q] = -1;
+  __syncwarp();
+  const int64_t pairs = groups * (int64_t)nchunks;
+  const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t x = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < pairs; x += wstride) {
+    const int64_t g = x / nchunks;
+    const int c = (int)(x % nchunks);
+    const int64_t* tg = tab + g * (nchunks + 1) + c;
+    const int64_t gs = gidx[g];
+    const int64_t e0 = gs + tg[0], e1 = gs + tg[1];
+    if (e0 >= e1) continue;
+    const int32_t lo_col = c * Cfg::KC;
+    for (int64_t b0 = e0; b0 < e1; b0 += 32) {
+      const int64_t e = b0 + lane;
+      int32_t r = -1, ur = -1;
+      if (e < e1) {
+        r = rows[e];
+        ur = unit_of[r];
+      }
+      const bool mine = ur >= 0;  // a row of this plan (two-class split: the other class is skipped)
+      const unsigned same = __match_any_sync(0xffffffffu, mine ? r : -1 - lane);
+      const int rl = mine ? (int)(r - g * p) : 0;
+      const uint32_t before = mine && s_tag[wl][rl] == x ? s_cnt[wl][rl] : 0u;
+      const uint32_t rank = before + (uint32_t)__popc(same & ((1u << lane) - 1u));
+      __syncwarp();
+      if (mine && (same >> lane) == 1u) {  // the row's last entry in this batch
+        s_tag[wl][rl] = x;
+        s_cnt[wl][rl] = rank + 1;
+      }
+      __syncwarp();
+      if (!mine) continue;
+      const int32_t col = cols[e];
+      const int64_t u = ur / Cfg::RW;
+      const int64_t rb = u / Cfg::NW;
+      const int w = (int)(u % Cfg::NW);
+      const uint32_t slot = (uint32_t)(ur % Cfg::RW);
+      const int64_t base = slot_pos[((rb * nchunks + c) * Cfg::NW + w) * Cfg::RW + slot];
+      if constexpr (Cfg::EPR == 1) {
+        uint32_t* word = reinterpret_cast<uint32_t*>(ent + base + (int64_t)Cfg::REC * rank);
+        const double v = (double)vals[e];
+        word[0] = (uint32_t)__double2loint(v);
+        word[1] = (uint32_t)__double2hiint(v);
+        word[2] = ((uint32_t)(col - lo_col) * Cfg::ROWB) | (slot << 24);
+      } else if constexpr (Cfg::EPR == 3) {
+        uint32_t* word = reinterpret_cast<uint32_t*>(ent + base + (int64_t)Cfg::REC * (rank / 3));
+        word[rank % 3] = __float_as_uint((float)vals[e]);
+        reinterpret_cast<unsigned char*>(word + 3)[rank % 3] = (unsigned char)(col - lo_col);
+      } else {
+        const int64_t ve = base + rank;
+        uint32_t* word = reinterpret_cast<uint32_t*>(ent + (ve >> 1) * 16);
+        const uint32_t h = (uint32_t)(ve & 1);
+        word[h] = __float_as_uint((float)vals[e]);
+        word[2 + h] = ((uint32_t)(col - lo_col) * Cfg::ROWB) | (slot << 24);
+      }
+    }
+  }
+}
+
 // ------------------------------------------ segment planner (even A) ------
 // For an A whose rows keep identity placement (row r in row block r / rpb,
 // warp (r % rpb) % NW, slot (r % rpb) / NW) one CTA per segment (row block,
