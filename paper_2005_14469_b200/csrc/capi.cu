@@ -367,8 +367,8 @@ void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ct
   P.ent = DevBuf<unsigned char>(bound, s);
   DevBuf<int64_t> slot_pos(nseg * Cfg::NW * Cfg::RW, s);
   DevBuf<uint32_t> woff(nseg * Cfg::NW, s);  // warp segment offsets inside a segment
-  // every group slice's chunk boundaries (fill by chunk range, p <= kFillRangeMaxP)
-  DevBuf<int64_t> tab(a.p <= kFillRangeMaxP && a.nnz > 0 ? a.groups * (nchunks + 1) : 0, s);
+  // every group slice's chunk boundaries (fill by chunk range)
+  DevBuf<int64_t> tab(a.p >= kFillRangeMinP && a.p <= kFillRangeMaxP && a.nnz > 0 ? a.groups * (nchunks + 1) : 0, s);
 
   const int64_t init_n = std::max<int64_t>((int64_t)cnt.count, std::max<int64_t>(a.m, (int64_t)P.row_of.count));
   IdentPlace ip;
@@ -423,8 +423,11 @@ void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ct
                   (const uint32_t*)cnt.get(), units, nchunks, nseg, (const int64_t*)P.seg_off.get(),
                   (const uint32_t*)woff.get(), P.ent.get(), slot_pos.get());
   if (a.nnz > 0) {
-    if (a.p <= kFillRangeMaxP) {
-      // ranks by (group, chunk) range: linear in the range (the per-entry scan is quadratic in it)
+    if (a.p >= kFillRangeMinP && a.p <= kFillRangeMaxP) {
+      // ranks by (group, chunk) range: linear in the range, where the per-entry scan is quadratic
+      // in it; small groups keep the per-entry scan (short ranges, and a (group, chunk) walk
+      // would visit mostly empty ranges: configs[3] planner p=4 0.28 ms against 0.43, p=64
+      // 0.56 against 0.21; tools/planner_cost.py)
       GCOO_LAUNCH_PDL(chunk_table_kernel, grid_for(std::max(a.nnz, a.groups), 256), 256, 0, s, a.nnz, a.p,
                       a.groups, a.rows, a.cols, a.gidx, a.gnnz, (int32_t)Cfg::KC, nchunks, tab.get());
       GCOO_LAUNCH_PDL(tacc_fill_range_kernel<Cfg>, grid_for(a.groups * nchunks * 32, kFillRangeWarps * 32),

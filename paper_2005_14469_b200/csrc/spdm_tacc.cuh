@@ -275,13 +275,14 @@ __global__ void tacc_fill_kernel(int64_t nnz, int32_t p, const typename Cfg::E* 
   }
 }
 
-// P5 by chunk range (general chain, p <= kFillRangeMaxP): one warp per
+// P5 by chunk range (general chain, 16 <= p <= kFillRangeMaxP): one warp per
 // (group, chunk) — the chunk's entries of a group slice are one contiguous
 // (col,row)-sorted range (chunk_table_kernel) — 32 entries at a time, a row's
 // entries ranked by lane order (match_any) after its running count in the
 // range, kept in shared memory per warp (a tag per row names the range the
 // count belongs to, so nothing is cleared).  Linear in the range, where the
 // per-entry scan of tacc_fill_kernel is quadratic in it.
+constexpr int kFillRangeMinP = 16;
 constexpr int kFillRangeMaxP = 256;
 constexpr int kFillRangeWarps = 8;
 

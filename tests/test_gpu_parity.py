@@ -772,7 +772,7 @@ def test_heavy_rows_balanced_placement(gcoo, cuda, oracle, kernel):
     bm = (1.0 - rng.random((k, n))).astype(np.float32)
     gcoo.force_kernel(kernel)
     try:
-        # p <= 256: the fill ranks by (group, chunk) range; 512: the per-entry scan
+        # 16 <= p <= 256: the fill ranks by (group, chunk) range; others: the per-entry scan
         for p in (1, 4, 16, 32, 256, 512):
             go = oracle.dense_to_gcoo(a, p)
             c_ref, _ = oracle.spdm(go, bm, 64, fma=True)
