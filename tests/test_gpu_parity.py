@@ -309,6 +309,31 @@ def test_large_group_size_bit_exact(gcoo, cuda, oracle, p):
     assert (st.flops, st.b_loads_total, st.b_loads_reused, st.staging_fills) == st_ref
     assert gcoo.last_kernel().startswith("tacc")
 
+@pytest.mark.parametrize("n,s", [(2000, 0.8), (2000, 0.999), (4000, 0.95), (14000, 0.99), (14000, 0.9)])
+def test_configs2_sweep_points_vs_oracle(gcoo, cuda, oracle, n, s):
+    """BASELINE configs[2] (the sparsity sweep at n = 2000..14000, inputs from
+    the reference's sweep seeds as tools/sweep_crossover.py makes them): the
+    GPU's dense -> GCOO (K3) and multiply on device tensors, against the
+    oracle — GCOO arrays bit-exact, C bit-exact on sampled row blocks (the
+    oracle's row-range multiply keeps each row's chain)."""
+    import torch
+    dens = round(n * n * (1.0 - s)) / (n * n)  # the reference's realised sparsity (bench.cpp:67-74)
+    a_seed = gcoo.derive_seed(1, n, int(round(dens * n * n)))
+    a = gcoo.generate_uniform_sparse(n, s, a_seed)
+    b = gcoo.generate_uniform_sparse(n, 0.0, gcoo.derive_seed(a_seed, n, 0xB))
+    d = gcoo.dense_to_gcoo_dev(torch.from_numpy(a).cuda(), 4)
+    c = torch.empty((n, n), dtype=torch.float32, device="cuda")
+    gcoo.spdm_gcoo_dev(d, torch.from_numpy(b).cuda(), c)
+    torch.cuda.synchronize()
+    go = oracle.dense_to_gcoo(a, 4)
+    g = d.to_host()
+    for f in ("values", "row_idx", "col_idx", "g_idxes", "nnz_per_group"):
+        assert np.array_equal(getattr(g, f), getattr(go, f)), f
+    rows = 16 if n > 4000 else 64
+    for r0 in (0, n // 2 - rows // 2, n - rows):
+        c_ref = oracle.spdm_rows(go, b, r0, r0 + rows)
+        assert np.array_equal(c[r0:r0 + rows].cpu().numpy(), c_ref[r0:r0 + rows]), (n, s, r0)
+
 def test_plan_execute_split_bit_exact(gcoo, cuda, oracle):
     """gcoo_plan_*: one plan, many multiplies (different B widths, a strided
     column shard, an unaligned shard that needs another kernel class) — every
