@@ -1461,20 +1461,31 @@ int64_t dense_to_gcoo_device(int64_t m, int64_t k, int32_t p, const T* A, int64_
   if (!is_pow2(p)) einval("dense_to_gcoo: p must be a power of two");
   if (m < 1 || k < 1) einval("DenseMatrix: dimensions must be >= 1");
   const int64_t groups = ceil_div(m, p);
-  const int64_t n_ct = ceil_div(k, kDenseTileCols);
+  // 16-byte loads when every row starts 16-byte aligned
+  constexpr int VEC = 16 / (int)sizeof(T);
+  const bool vec = k % VEC == 0 && (reinterpret_cast<uintptr_t>(A) % 16) == 0;
+  const int64_t n_ct = ceil_div(k, (int64_t)kDenseTileCols * (vec ? VEC : 1));
   const int64_t tiles = groups * n_ct;
   DevBuf<int64_t> counts(tiles, s), off(tiles + 1, s);
   const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * 16);
-  GCOO_LAUNCH(dense_count_kernel<T>, grid, kDenseTileCols, 0, s, m, k, p, A, n_ct, tiles, counts.get());
+  if (vec)
+    GCOO_LAUNCH((dense_count_kernel<T, VEC>), grid, kDenseTileCols, 0, s, m, k, p, A, n_ct, tiles, counts.get());
+  else
+    GCOO_LAUNCH((dense_count_kernel<T, 1>), grid, kDenseTileCols, 0, s, m, k, p, A, n_ct, tiles, counts.get());
   exclusive_scan(counts.get(), off.get(), tiles, s);
   GCOO_LAUNCH(dense_groups_kernel, (unsigned)ceil_div(groups, 256), 256, 0, s, groups, n_ct, off.get(), gidx,
               gnnz);
   int64_t nnz = 0;
   d2h(&nnz, off.get() + tiles, 1, s);
   GCOO_CUDA(cudaStreamSynchronize(s));
-  if (nnz > 0 && capacity >= nnz && ovals)
-    GCOO_LAUNCH(dense_fill_kernel<T>, grid, kDenseTileCols, 0, s, m, k, p, A, n_ct, tiles, off.get(), ovals,
-                orows, ocols);
+  if (nnz > 0 && capacity >= nnz && ovals) {
+    if (vec)
+      GCOO_LAUNCH((dense_fill_kernel<T, VEC>), grid, kDenseTileCols, 0, s, m, k, p, A, n_ct, tiles, off.get(),
+                  ovals, orows, ocols);
+    else
+      GCOO_LAUNCH((dense_fill_kernel<T, 1>), grid, kDenseTileCols, 0, s, m, k, p, A, n_ct, tiles, off.get(),
+                  ovals, orows, ocols);
+  }
   return nnz;
 }
 

@@ -207,18 +207,57 @@ __global__ void expand_rows_kernel(int64_t nnz, int64_t m, const int64_t* __rest
 constexpr int kDenseTileCols = 256;
 
 // counts[g * n_ct + ct] = nonzeros of band g in columns [ct*256, ct*256+256)
+// A thread owns VEC consecutive columns of a p-row band (one 16-byte load per
+// row when the rows allow it, else VEC = 1): a tile is kDenseTileCols * VEC
+// columns of one group's band.
+template <typename T, int VEC>
+struct DenseVec;
 template <typename T>
+struct DenseVec<T, 1> {
+  static __device__ __forceinline__ void load(const T* p, T (&v)[1]) { v[0] = __ldg(p); }
+};
+template <>
+struct DenseVec<float, 4> {
+  static __device__ __forceinline__ void load(const float* p, float (&v)[4]) {
+    const float4 x = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  }
+};
+template <>
+struct DenseVec<double, 2> {
+  static __device__ __forceinline__ void load(const double* p, double (&v)[2]) {
+    const double2 x = __ldg(reinterpret_cast<const double2*>(p));
+    v[0] = x.x; v[1] = x.y;
+  }
+};
+
+// nonzeros of this thread's VEC columns over the band's rows (k % VEC == 0 when VEC > 1)
+template <typename T, int VEC>
+__device__ __forceinline__ int64_t dense_band_count(const T* __restrict__ A, int64_t k, int64_t lo, int64_t hi,
+                                                    int64_t c) {
+  int64_t cnt = 0;
+  if (c < k) {
+#pragma unroll 4
+    for (int64_t r = lo; r < hi; ++r) {
+      T v[VEC];
+      DenseVec<T, VEC>::load(A + r * k + c, v);
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) cnt += v[q] != T(0);
+    }
+  }
+  return cnt;
+}
+
+template <typename T, int VEC>
 __global__ void __launch_bounds__(kDenseTileCols)
 dense_count_kernel(int64_t m, int64_t k, int32_t p, const T* __restrict__ A, int64_t n_ct,
                    int64_t tiles, int64_t* __restrict__ counts) {
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int64_t g = tile / n_ct, ct = tile % n_ct;
-    const int64_t c = ct * kDenseTileCols + threadIdx.x;
+    const int64_t c = (ct * kDenseTileCols + threadIdx.x) * VEC;
     const int64_t lo = g * p;
     const int64_t hi = lo + p < m ? lo + p : m;
-    int64_t cnt = 0;
-    if (c < k)
-      for (int64_t r = lo; r < hi; ++r) cnt += A[r * k + c] != T(0);
+    int64_t cnt = dense_band_count<T, VEC>(A, k, lo, hi, c);
     // block reduction
 #pragma unroll
     for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
@@ -234,31 +273,33 @@ dense_count_kernel(int64_t m, int64_t k, int32_t p, const T* __restrict__ A, int
   }
 }
 
-template <typename T>
+// Entries in (col, row) order inside the band: a thread writes its columns one
+// after the other, each down the band's rows, at its exclusive-scan offset.
+template <typename T, int VEC>
 __global__ void __launch_bounds__(kDenseTileCols)
 dense_fill_kernel(int64_t m, int64_t k, int32_t p, const T* __restrict__ A, int64_t n_ct, int64_t tiles,
                   const int64_t* __restrict__ tile_off, T* __restrict__ vals, int32_t* __restrict__ rows,
                   int32_t* __restrict__ cols) {
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int64_t g = tile / n_ct, ct = tile % n_ct;
-    const int64_t c = ct * kDenseTileCols + threadIdx.x;
+    const int64_t c = (ct * kDenseTileCols + threadIdx.x) * VEC;
     const int64_t lo = g * p;
     const int64_t hi = lo + p < m ? lo + p : m;
-    int64_t cnt = 0;
-    if (c < k)
-      for (int64_t r = lo; r < hi; ++r) cnt += A[r * k + c] != T(0);
+    const int64_t cnt = dense_band_count<T, VEC>(A, k, lo, hi, c);
     int64_t total;
     int64_t w = tile_off[tile] + block_exclusive_scan<kDenseTileCols>(cnt, total);
-    if (c < k)
-      for (int64_t r = lo; r < hi; ++r) {
-        const T a = A[r * k + c];
-        if (a != T(0)) {
-          vals[w] = a;
-          rows[w] = (int32_t)r;
-          cols[w] = (int32_t)c;
-          ++w;
+    if (c < k && cnt > 0)
+#pragma unroll
+      for (int q = 0; q < VEC; ++q)
+        for (int64_t r = lo; r < hi; ++r) {
+          const T a = A[r * k + c + q];
+          if (a != T(0)) {
+            vals[w] = a;
+            rows[w] = (int32_t)r;
+            cols[w] = (int32_t)(c + q);
+            ++w;
+          }
         }
-      }
   }
 }
 
