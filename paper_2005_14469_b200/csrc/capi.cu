@@ -514,16 +514,22 @@ int pick_by_density(double density, bool f64) {
                              : 17;
 }
 
-// `small_gate`: products below 0.4 GFLOP take the planner-free row-tile kernel
-// (the planner, ~35 us, costs more than it saves; profiles/r01_small_n.jsonl).
-// A caller that reuses a plan (gcoo_plan_*) pays the planner once, so plans
-// are chosen without it.
+// `small_gate` (flops): smaller products take the planner-free row-tile kernel
+// (the planner, ~35 us, costs more than it saves).  Direct calls: 0.25 GFLOP
+// (n=2000-4000 sweep with 4-row tiles: TMEM wins from ~0.3 GFLOP, e.g. n=2000
+// s=0.98 0.085 vs 0.098 ms, n=3000 s=0.995 0.086 vs 0.094; the row-tile kernel
+// below, e.g. n=2000 s=0.99 0.061 vs 0.064).  The host pipeline's column
+// strips: 0.4 GFLOP (a strip's planner would sit on the PCIe critical path;
+// profiles/r01_small_n.jsonl).  A caller that reuses a plan (gcoo_plan_*) pays
+// the planner once, so plans are chosen without a gate (0).
+constexpr double kSmallGateDirect = 2.5e8;
+constexpr double kSmallGateStrip = 4e8;
 template <typename T>
 int choose_kind(const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const T* B, const T* C, int flavor,
-                bool small_gate = true) {
+                double small_gate = kSmallGateDirect) {
   const int force = g_force_kernel.load(std::memory_order_relaxed);
   if (flavor == GCOO_FLAVOR_MUL_ADD || force == 0 || a.m == 0) return 0;
-  if (force < 0 && small_gate && 2.0 * (double)a.nnz * (double)n < 4e8) return 0;
+  if (force < 0 && 2.0 * (double)a.nnz * (double)n < small_gate) return 0;
   const double density = (double)a.nnz / ((double)a.m * (double)a.k);
   const int pick = force > 0 ? force : pick_by_density(density, sizeof(T) == 8);
   int kind = 0;
@@ -776,7 +782,7 @@ bool make_split_plan(SpdmPlan& P, const DevGcoo<T>& a, const SkewHint& h, int64_
 // rule the split out without the device probe and its synchronisation.
 template <typename T>
 void plan_for(SpdmPlan& P, const DevGcoo<T>& a, int64_t n, int64_t ldb, int64_t ldc, const T* B, const T* C,
-              int flavor, cudaStream_t s, int64_t strip_n, bool small_gate, bool cached, int64_t max_group_nnz = -1) {
+              int flavor, cudaStream_t s, int64_t strip_n, double small_gate, bool cached, int64_t max_group_nnz = -1) {
   const int kind = choose_kind<T>(a, n, ldb, ldc, B, C, flavor, small_gate);
   const bool no_split = max_group_nnz >= 0 && g_force_split.load(std::memory_order_relaxed) < 0 &&
                         (double)max_group_nnz <= 8.0 * (double)a.nnz / (double)std::max<int64_t>(a.m, 1);
@@ -799,7 +805,7 @@ void launch_spdm(const DevGcoo<T>& a, int64_t n, const T* B, int64_t ldb, T* C, 
   if (a.m == 0 || n == 0) return;
   SpdmPlan P;
   // strip_n = n: a grid smaller than one wave spreads A's rows over more row blocks
-  plan_for<T>(P, a, n, ldb, ldc, B, C, flavor, s, n, true, true);
+  plan_for<T>(P, a, n, ldb, ldc, B, C, flavor, s, n, kSmallGateDirect, true);
   run_spdm<T>(P, a, n, B, ldb, C, ldc, flavor, s);
 }
 
@@ -1183,7 +1189,7 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
     DevBuf<T> d_B(k * n, s), d_C(m * n, s);
     h2d(d_B.get(), B, k * n, s);
     SpdmPlan P1;
-    plan_for<T>(P1, a, n, n, n, d_B.get(), d_C.get(), flavor, s, n, /*small_gate=*/true, /*cached=*/false, max_group);
+    plan_for<T>(P1, a, n, n, n, d_B.get(), d_C.get(), flavor, s, n, kSmallGateDirect, /*cached=*/false, max_group);
     run_spdm<T>(P1, a, n, d_B.get(), n, d_C.get(), n, flavor, s);
     if (!perm) {
       apply_tile_list<T>(a, n, cfg_b, tile_order, tile_count, d_C.get(), n, stats, s);
@@ -1201,7 +1207,7 @@ void spdm_host(int64_t m, int64_t k, int64_t n, int32_t a_p, int32_t cfg_p, int3
   // the planner would sit on the critical path before the first C strip can
   // cross PCIe (n=8000, s=0.99, 32 strips: 6.0 ms per call with the row-tile
   // kernel per strip against 6.6 ms with the TMEM kernel and its planner)
-  plan_for<T>(P, a, W, W, W, dBv[0].get(), dCv[0].get(), flavor, s, W, /*small_gate=*/true, /*cached=*/false,
+  plan_for<T>(P, a, W, W, W, dBv[0].get(), dCv[0].get(), flavor, s, W, kSmallGateStrip, /*cached=*/false,
               max_group);
   if (trace) trace->mark(s, 1, -1);  // planned
   for (int64_t j = 0; j < nstrips; ++j) {
@@ -1291,7 +1297,7 @@ void plan_create(int64_t m, int64_t k, int32_t p, int64_t nnz, const T* values, 
     // multiply); no small-product gate: the planner runs once here, not per call
     static const double aligned[2] __attribute__((aligned(16))) = {};
     const T* al = reinterpret_cast<const T*>(aligned);
-    plan_for<T>(h->plan, plan_a<T>(h.get()), 4, 4, 4, al, al, flavor, s, 0, /*small_gate=*/false, /*cached=*/false);
+    plan_for<T>(h->plan, plan_a<T>(h.get()), 4, 4, 4, al, al, flavor, s, 0, /*small_gate=*/0.0, /*cached=*/false);
   }
   *plan = h.release();
 }
@@ -1308,7 +1314,7 @@ void plan_spdm(const gcoo_plan* plan, int64_t n, const T* B, int64_t ldb, T* C, 
   const SpdmPlan& P = plan->plan;
   bool usable;
   if (P.kind == 0) {
-    usable = choose_kind<T>(a, n, ldb, ldc, B, C, plan->flavor, /*small_gate=*/false) == 0;
+    usable = choose_kind<T>(a, n, ldb, ldc, B, C, plan->flavor, /*small_gate=*/0.0) == 0;
   } else {
     usable = true;
     for (const SpdmPlan* q = &P; q; q = q->heavy.get())
