@@ -32,6 +32,11 @@
 //     complete_tx); consumers release a stage with one arrive per warp.  The
 //     chunk depth KC is matched to the density so that a chunk's records fit
 //     the stage (choose_kind in capi.cu).
+//   * Tiles (row block x column strip) are walked in launch order by
+//     persistent CTAs (one per SM) for even A: the ring runs across tile
+//     boundaries, so the next tile's first stages load while the consumers
+//     write the previous tile back from TMEM; skewed A launches one CTA per
+//     tile and lets the hardware balance them.
 //
 // Per C element the FMAs run over the row's nonzeros in ascending column
 // order (chunks in order, a (row, chunk)'s entries in column order), one
