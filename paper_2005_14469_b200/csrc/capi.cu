@@ -310,6 +310,14 @@ void set_smem_attr() {
   attr_set[d].store(true, std::memory_order_release);
 }
 
+// Bytes of a record stream: every segment's table and headers (plus a
+// linear extent's slack) and at most one 16-byte record per entry.
+template <class Cfg>
+int64_t ent_bound(int64_t nseg, int64_t nnz) {
+  const int64_t per_seg = (int64_t)Cfg::TABLE + (int64_t)Cfg::NW * Cfg::HDR + 8 * Cfg::NW;
+  return nseg * per_seg + (int64_t)Cfg::REC * nnz + 16;
+}
+
 // Planner: counts -> segment sizes -> scan -> headers -> scatter, on stream s.
 // `min_ctas`: spread rows over enough row blocks that a launch over
 // `col_tiles` column tiles has at least that many CTAs (narrow strips of the
@@ -346,18 +354,37 @@ void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ct
     P.skewed = DevBuf<int32_t>(1, s);
     DevBuf<int64_t> seg_len(nseg, s), scan_tmp(scan_scratch(nseg), s), tab(a.groups * (nchunks + 1), s);
     P.seg_off = DevBuf<int64_t>(nseg + 1, s);
-    P.ent = DevBuf<unsigned char>(nseg * (Cfg::TABLE + Cfg::NW * Cfg::HDR) + (int64_t)Cfg::REC * a.nnz + 16, s);
+    P.ent = DevBuf<unsigned char>(ent_bound<Cfg>(nseg, a.nnz), s);
     const unsigned grid = (unsigned)std::min<int64_t>(std::max<int64_t>(nseg, 1), (int64_t)sm_count() * 8);
+    if constexpr (Cfg::LINEAR_EXTENT) {
+      // extents from entry counts: the chunk table also counts each segment's
+      // entries, a scan of their extents gives every offset, and one build
+      // pass writes the segments (no separate counting pass)
+      GCOO_CUDA(cudaMemsetAsync(seg_len.get(), 0, seg_len.bytes(), s));
+      GCOO_LAUNCH_PDL(chunk_table_kernel, grid_for(std::max(a.nnz, a.groups), 256), 256, 0, s, a.nnz, a.p,
+                      a.groups, a.rows, a.cols, a.gidx, a.gnnz, (int32_t)Cfg::KC, nchunks, tab.get(), (int32_t)rpb,
+                      reinterpret_cast<unsigned long long*>(seg_len.get()));
+      GCOO_LAUNCH_PDL(seg_extent_kernel<Cfg>, grid_for(nseg, 256), 256, 0, s, nseg, seg_len.get());
+      DevBuf<int64_t> nscan(nseg + 1, s);
+      exclusive_scan(seg_len.get(), nscan.get(), nseg, s, scan_tmp.get());
+      GCOO_LAUNCH_PDL((seg_plan_kernel<Cfg, 3>), grid, kSegThreads, 0, s, a.m, a.nnz, a.p, a.vals, a.rows, a.cols,
+                      a.gidx, a.gnnz, (const int64_t*)tab.get(), nchunks, nseg, (int32_t)rpb, (int64_t*)nullptr,
+                      P.unit_of.get(), P.row_of.get(), P.skewed.get(), P.seg_off.get(), P.ent.get(),
+                      (const int64_t*)nscan.get());
+      return;
+    }
     GCOO_LAUNCH_PDL(chunk_table_kernel, grid_for(std::max(a.nnz, a.groups), 256), 256, 0, s, a.nnz, a.p, a.groups,
-                    a.rows, a.cols, a.gidx, a.gnnz, (int32_t)Cfg::KC, nchunks, tab.get());
+                    a.rows, a.cols, a.gidx, a.gnnz, (int32_t)Cfg::KC, nchunks, tab.get(), (int32_t)rpb,
+                    (unsigned long long*)nullptr);
     GCOO_LAUNCH_PDL((seg_plan_kernel<Cfg, 1>), grid, kSegThreads, 0, s, a.m, a.nnz, a.p, a.vals, a.rows, a.cols,
                     a.gidx, a.gnnz, (const int64_t*)tab.get(), nchunks, nseg, (int32_t)rpb, seg_len.get(),
-                    P.unit_of.get(), P.row_of.get(), P.skewed.get(), (const int64_t*)nullptr, (unsigned char*)nullptr);
+                    P.unit_of.get(), P.row_of.get(), P.skewed.get(), (int64_t*)nullptr, (unsigned char*)nullptr,
+                    (const int64_t*)nullptr);
     exclusive_scan(seg_len.get(), P.seg_off.get(), nseg, s, scan_tmp.get());
     GCOO_LAUNCH_PDL((seg_plan_kernel<Cfg, 2>), grid, kSegThreads, 0, s, a.m, a.nnz, a.p, a.vals, a.rows, a.cols,
                     a.gidx, a.gnnz, (const int64_t*)tab.get(), nchunks, nseg, (int32_t)rpb, (int64_t*)nullptr,
-                    (int32_t*)nullptr,
-                    (int32_t*)nullptr, (int32_t*)nullptr, (const int64_t*)P.seg_off.get(), P.ent.get());
+                    (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr, P.seg_off.get(), P.ent.get(),
+                    (const int64_t*)nullptr);
     return;
   }
   // every buffer first: the kernels below form one uninterrupted PDL chain
@@ -369,8 +396,7 @@ void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ct
   DevBuf<int64_t> seg_len(nseg, s), scan_tmp(scan_scratch(nseg), s);
   P.seg_off = DevBuf<int64_t>(nseg + 1, s);
   // upper bound of the stream: headers + one record (16 B) per entry
-  const int64_t bound = nseg * (Cfg::TABLE + Cfg::NW * Cfg::HDR) + (int64_t)Cfg::REC * a.nnz + 16;
-  P.ent = DevBuf<unsigned char>(bound, s);
+  P.ent = DevBuf<unsigned char>(ent_bound<Cfg>(nseg, a.nnz), s);
   DevBuf<int64_t> slot_pos(nseg * Cfg::NW * Cfg::RW, s);
   DevBuf<uint32_t> woff(nseg * Cfg::NW, s);  // warp segment offsets inside a segment
   // every group slice's chunk boundaries (fill by chunk range)
@@ -435,7 +461,8 @@ void build_plan(SpdmPlan& P, const DevGcoo<T>& a, cudaStream_t s, int64_t min_ct
       // would visit mostly empty ranges: configs[3] planner p=4 0.28 ms against 0.43, p=64
       // 0.56 against 0.21; tools/planner_cost.py)
       GCOO_LAUNCH_PDL(chunk_table_kernel, grid_for(std::max(a.nnz, a.groups), 256), 256, 0, s, a.nnz, a.p,
-                      a.groups, a.rows, a.cols, a.gidx, a.gnnz, (int32_t)Cfg::KC, nchunks, tab.get());
+                      a.groups, a.rows, a.cols, a.gidx, a.gnnz, (int32_t)Cfg::KC, nchunks, tab.get(), (int32_t)1,
+                      (unsigned long long*)nullptr);
       GCOO_LAUNCH_PDL(tacc_fill_range_kernel<Cfg>, grid_for(a.groups * nchunks * 32, kFillRangeWarps * 32),
                       kFillRangeWarps * 32, 0, s, a.m, a.p, a.groups, a.vals, a.rows, a.cols, a.gidx,
                       (const int64_t*)tab.get(), nchunks, (const int64_t*)slot_pos.get(), P.ent.get(),

@@ -82,6 +82,16 @@ struct TaccCfg {
   static_assert((sizeof(E_) == 4 && (EPR_ == 2 || (EPR_ == 3 && KC_ < 255))) || (sizeof(E_) == 8 && EPR_ == 1),
                 "record format");
   static constexpr int TABLE = (4 * NW_ + 15) & ~15;  // per-segment warp offset table (NW x u32)
+  // Segment extents from the entry count n alone (two-entry and fp64
+  // records): extent(n) bounds table + headers + records (a warp's dense pair
+  // stream wastes at most half a record) and keeps 16-byte alignment, so the
+  // offsets are a scan of per-segment counts; a segment holds entries iff its
+  // extent exceeds EXT_BASE.  Three-entry records keep exact lengths.
+  static constexpr bool LINEAR_EXTENT = EPR_ != 3;
+  static constexpr uint32_t EXT_BASE = (uint32_t)TABLE + (uint32_t)NW_ * HDR + (EPR_ == 2 ? 8u * NW_ : 0u);
+  static __host__ __device__ constexpr int64_t extent(int64_t n) {
+    return (int64_t)EXT_BASE + (EPR_ == 2 ? 16 * ((n + 1) / 2) : 16 * n);
+  }
   // stages + full/empty barriers + TMEM address slot + per-stage segment offsets (int64) and lengths
   static constexpr size_t SMEM = (size_t)STAGES_ * STAGE_BYTES + 2 * STAGES_ * 8 + 16 + STAGES_ * 16;
   static_assert(KC_ <= 256, "TMA box rows");
@@ -169,7 +179,18 @@ __global__ void tacc_size_kernel(const uint32_t* __restrict__ cnt, int64_t units
       if (lane >= d) incl += y;
     }
     if (lane < Cfg::NW) woff[x * Cfg::NW + lane] = Cfg::TABLE + incl - sz;
-    if (lane == 31) seg_len[x] = Cfg::TABLE + incl;
+    if constexpr (Cfg::LINEAR_EXTENT) {  // the extent from the segment's entry count
+      uint32_t ne = 0;
+      if (lane < Cfg::NW && rb * Cfg::NW + lane < units) {
+        const uint32_t* pc = cnt + ((rb * Cfg::NW + lane) * nchunks + c) * Cfg::RW;
+        for (int q = 0; q < Cfg::RW; ++q) ne += pc[q];
+      }
+#pragma unroll
+      for (int d = 16; d >= 1; d >>= 1) ne += __shfl_xor_sync(0xffffffffu, ne, d);
+      if (lane == 31) seg_len[x] = Cfg::extent(ne);
+    } else {
+      if (lane == 31) seg_len[x] = Cfg::TABLE + incl;
+    }
   }
 }
 
@@ -383,23 +404,42 @@ constexpr int kSegRowCache = 4096;  // a segment's entry rows and columns staged
 __global__ void chunk_table_kernel(int64_t nnz, int32_t p, int64_t groups, const int32_t* __restrict__ rows,
                                    const int32_t* __restrict__ cols, const int64_t* __restrict__ gidx,
                                    const int64_t* __restrict__ gnnz, int32_t kc, int nchunks,
-                                   int64_t* __restrict__ tab) {
+                                   int64_t* __restrict__ tab, int32_t rpb, unsigned long long* __restrict__ n_seg) {
   griddep_wait();  // PDL: predecessor complete
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (int64_t e = t0; e < nnz; e += stride) {
-    const int64_t g = rows[e] / p;
-    const int64_t gs = gidx[g], ge = gs + gnnz[g];
-    const int c = cols[e] / kc;
-    const int cp = e == gs ? -1 : cols[e - 1] / kc;
-    int64_t* t = tab + g * (nchunks + 1);
-    for (int q = cp + 1; q <= c; ++q) t[q] = e - gs;
-    if (e == ge - 1)
-      for (int q = c + 1; q <= nchunks; ++q) t[q] = ge - gs;
+  for (int64_t e0 = t0 - (threadIdx.x & 31); e0 < nnz; e0 += stride) {  // warp-uniform trip count
+    const int64_t e = e0 + (threadIdx.x & 31);
+    const bool in = e < nnz;
+    int64_t x = -1;
+    if (in) {
+      const int32_t r = rows[e];
+      const int64_t g = r / p;
+      const int64_t gs = gidx[g], ge = gs + gnnz[g];
+      const int c = cols[e] / kc;
+      const int cp = e == gs ? -1 : cols[e - 1] / kc;
+      int64_t* t = tab + g * (nchunks + 1);
+      for (int q = cp + 1; q <= c; ++q) t[q] = e - gs;
+      if (e == ge - 1)
+        for (int q = c + 1; q <= nchunks; ++q) t[q] = ge - gs;
+      x = (int64_t)(r / rpb) * nchunks + c;  // segment (row block, chunk), identity placement
+    }
+    if (n_seg) {  // entries per segment: one atomic per run of equal segments in the warp
+      const unsigned same = __match_any_sync(0xffffffffu, (unsigned long long)x);
+      if (in && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&n_seg[x], (unsigned long long)__popc(same));
+    }
   }
   for (int64_t g = t0; g < groups; g += stride)  // empty slices: every range empty
     if (gnnz[g] == 0)
       for (int q = 0; q <= nchunks; ++q) tab[g * (nchunks + 1) + q] = 0;
+}
+
+// n -> Cfg::extent(n) in place (the chunk table's per-segment entry counts).
+template <class Cfg>
+__global__ void seg_extent_kernel(int64_t nseg, int64_t* __restrict__ len) {
+  griddep_wait();  // PDL: predecessor complete
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nseg; x += (int64_t)gridDim.x * blockDim.x)
+    len[x] = Cfg::extent(len[x]);
 }
 
 template <class Cfg>
@@ -419,20 +459,26 @@ seg_plan_kernel(int64_t m, int64_t nnz, int32_t p, const typename Cfg::E* __rest
                 const int64_t* __restrict__ gnnz, const int64_t* __restrict__ tab, int nchunks, int64_t nseg,
                 int32_t rpb,
                 int64_t* __restrict__ seg_len, int32_t* __restrict__ unit_of, int32_t* __restrict__ row_of,
-                int32_t* __restrict__ skew_flag, const int64_t* __restrict__ seg_off, unsigned char* __restrict__ ent) {
+                int32_t* __restrict__ skew_flag, int64_t* __restrict__ seg_off, unsigned char* __restrict__ ent,
+                const int64_t* __restrict__ nscan) {
+  // PASS 1: lengths; PASS 2: build at the scanned offsets; PASS 3 (count
+  // extents): placement + build at the scan of the extents of the entry
+  // counts (chunk_table_kernel, seg_extent_kernel), copied to seg_off
+  static_assert(PASS != 3 || Cfg::LINEAR_EXTENT, "single build pass: linear extents only");
   static_assert(Cfg::RB <= kSegMaxGroups, "groups per row block");
   constexpr int NW = Cfg::NW, RW = Cfg::RW, EPR = Cfg::EPR;
   __shared__ SegSmem<Cfg> sm;
   __shared__ int32_t s_total;
   griddep_wait();  // PDL: predecessor complete
   const int tid = threadIdx.x;
-  if (PASS == 1 && blockIdx.x == 0 && tid == 0) *skew_flag = 0;
+  if (PASS != 2 && blockIdx.x == 0 && tid == 0) *skew_flag = 0;
+  if (PASS == 3 && blockIdx.x == 0 && tid == 0) seg_off[nseg] = nscan[nseg];
   for (int64_t x = blockIdx.x; x < nseg; x += gridDim.x) {
     const int64_t rb = x / nchunks;
     const int c = (int)(x % nchunks);
     const int64_t r0 = rb * rpb, r1 = r0 + rpb < m ? r0 + rpb : m;
     const int32_t lo_col = c * Cfg::KC, hi_col = lo_col + Cfg::KC;
-    if (PASS == 1 && c == 0) {  // identity placement of the row block's rows
+    if (PASS != 2 && c == 0) {  // identity placement of the row block's rows
       for (int64_t r = r0 + tid; r < r1; r += kSegThreads) {
         const int64_t j = r - r0;
         unit_of[r] = (int32_t)(rb * Cfg::RB + (j % NW) * RW + j / NW);
@@ -486,7 +532,7 @@ seg_plan_kernel(int64_t m, int64_t nnz, int32_t p, const typename Cfg::E* __rest
       g = a;
       e = sm.lo[a] + (i - sm.pre[a]);
     };
-    const bool cached = PASS == 2 && total <= kSegRowCache;
+    const bool cached = PASS != 1 && total <= kSegRowCache;
     for (int32_t i = tid; i < total; i += kSegThreads) {
       int64_t e;
       int g;
@@ -503,23 +549,27 @@ seg_plan_kernel(int64_t m, int64_t nnz, int32_t p, const typename Cfg::E* __rest
     __syncthreads();
     if constexpr (PASS == 1) {
       if (tid < 32) {
-        uint32_t sz = 0;
+        uint32_t sz = 0, ne = 0;
         for (int w = tid; w < NW; w += 32) {
-          uint32_t recs = 0;
-          if constexpr (EPR == 2) {
-            for (int q = 0; q < RW; ++q) recs += sm.cnt[w * RW + q];
-            recs = (recs + 1) / 2;
-          } else {
-            for (int q = 0; q < RW; ++q) recs += (sm.cnt[w * RW + q] + EPR - 1) / EPR;
+          uint32_t recs = 0, nw = 0;
+          for (int q = 0; q < RW; ++q) {
+            nw += sm.cnt[w * RW + q];
+            recs += (sm.cnt[w * RW + q] + EPR - 1) / EPR;
           }
+          if constexpr (EPR == 2) recs = (nw + 1) / 2;
           sz += Cfg::HDR + Cfg::REC * recs;
+          ne += nw;
         }
 #pragma unroll
-        for (int d = 16; d >= 1; d >>= 1) sz += __shfl_xor_sync(0xffffffffu, sz, d);
-        if (tid == 0) seg_len[x] = Cfg::TABLE + sz;
+        for (int d = 16; d >= 1; d >>= 1) {
+          sz += __shfl_xor_sync(0xffffffffu, sz, d);
+          ne += __shfl_xor_sync(0xffffffffu, ne, d);
+        }
+        if (tid == 0) seg_len[x] = Cfg::LINEAR_EXTENT ? Cfg::extent(ne) : Cfg::TABLE + sz;
       }
     } else {
-      const int64_t so = seg_off[x];
+      const int64_t so = PASS == 3 ? nscan[x] : seg_off[x];
+      if (PASS == 3 && tid == 0) seg_off[x] = so;
       unsigned char* seg = ent + so;
       if (tid < 32) {  // warp 0: warp segment offsets (one lane per warp), then per-slot bases
         uint32_t recs = 0, nent = 0;
@@ -938,7 +988,7 @@ spdm_tacc_kernel(const __grid_constant__ CUtensorMap tmap_b, int64_t m, int64_t 
           const uint32_t len = (uint32_t)(hi - lo);
           const uint32_t bytes = len <= Cfg::CAP ? len : 0u;  // oversize: consumers read global memory
           // a segment of empty warp headers only: no consumer reads this chunk's B tile
-          const bool any = len > (uint32_t)(Cfg::TABLE + Cfg::NW * Cfg::HDR);
+          const bool any = len > (Cfg::LINEAR_EXTENT ? Cfg::EXT_BASE : (uint32_t)(Cfg::TABLE + Cfg::NW * Cfg::HDR));
 #if GCOO_PROF
           const long long w0 = clock64();
 #endif
