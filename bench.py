@@ -156,19 +156,40 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def pcie_roofline(nbytes, seconds):
+def pcie_duplex_probe(dev, nbytes=256 << 20, reps=5):
+    """Concurrent pinned H2D + D2H bandwidth of this box's host link, measured
+    in the same run (GB/s, best of `reps`): the host-pointer path's roofline.
+    Boxes of this pool differ (80-99 GB/s measured), so a fixed figure would
+    misstate the fraction."""
+    import torch
+    n = nbytes // 4
+    hx = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    hy = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    dx = torch.empty(n, dtype=torch.float32, device=dev)
+    dy = torch.empty(n, dtype=torch.float32, device=dev)
+    s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    best = 0.0
+    for _ in range(reps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(s1):
+            dx.copy_(hx, non_blocking=True)
+        with torch.cuda.stream(s2):
+            hy.copy_(dy, non_blocking=True)
+        torch.cuda.synchronize()
+        best = max(best, 2 * nbytes / (time.perf_counter() - t0) / 1e9)
+    del hx, hy, dx, dy
+    return best
+
+
+def pcie_roofline(nbytes, seconds, peak):
     """The host-pointer path is PCIe-bound: its bytes per second against the
-    measured concurrent H2D+D2H bandwidth of this pool's B200 host link
-    (tools/pcie_probe.py -> profiles/r01_pcie_probe.jsonl)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_pcie_probe.jsonl")) as f:
-            rows = [json.loads(x) for x in f if x.strip()]
-        peak = max(r["gb_s"] for r in rows if r["probe"].startswith("h2d+d2h"))
-    except Exception:  # noqa: BLE001
+    concurrent H2D+D2H bandwidth measured on this box (pcie_duplex_probe)."""
+    if not peak:
         return {}
     ach = nbytes / seconds / 1e9
-    return {"pcie_gb_s": round(ach, 1), "pcie_peak_gb_s": peak, "pcie_frac": round(ach / peak, 3),
-            "pcie_peak_source": "measured concurrent H2D+D2H (profiles/r01_pcie_probe.jsonl)"}
+    return {"pcie_gb_s": round(ach, 1), "pcie_peak_gb_s": round(peak, 1), "pcie_frac": round(ach / peak, 3),
+            "pcie_peak_source": "measured in this run: concurrent pinned H2D + D2H of 256 MiB each, best of 5"}
 
 
 def synth_b_block(k, lo, hi, dev):
@@ -483,6 +504,10 @@ def run_ours(args):
                          pin(g_host.col_idx), pin(g_host.g_idxes), pin(g_host.nnz_per_group))
     e2e_s, e2e_times = e2e_leg(g_pin, pin(b_host), pin(np.empty((m, n), np.float32)), max(5, min(args.steps, 20)))
     e2e_value = world * flops_rank / e2e_s / 1e9
+    try:
+        pcie_peak = pcie_duplex_probe(dev)
+    except Exception:  # noqa: BLE001
+        pcie_peak = None
     # pageable buffers (the C++ drop-in's std::vector path)
     c_page = np.empty((m, n), np.float32)
     pg_s, pg_times = e2e_leg(g_host, b_host, c_page, 5)
@@ -601,7 +626,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_s * 1e3, 3),
                 "ms_per_step_mean": round(statistics.mean(e2e_times) * 1e3, 3), "calls": len(e2e_times),
                 "path": "paper_2005_14469_b200.spdm_gcoo -> gcoo_spdm_f32 (pinned host buffers)",
-                **pcie_roofline(h2d + d2h, e2e_s)},
+                **pcie_roofline(h2d + d2h, e2e_s, pcie_peak)},
         "construction": construction,
         "e2e_pageable": {"value": round(world * flops_rank / pg_s / 1e9, 2), "unit": "GFLOPS",
                          "ms_per_step": round(pg_s * 1e3, 3), "calls": len(pg_times),
