@@ -271,11 +271,24 @@ __global__ void tacc_fill_kernel(int64_t nnz, int32_t p, const typename Cfg::E* 
     const int c = col / Cfg::KC;
     const int32_t lo_col = c * Cfg::KC;
     const int64_t glo = gidx[r / p];
-    uint32_t rank = 0;
-    for (int64_t j = e - 1; j >= glo; --j) {
-      if (cols[j] < lo_col) break;
-      rank += rows[j] == r;
+    // the chunk's range in the group slice starts at the first column >= lo_col
+    // (columns ascend along the slice): binary search, then count the row's
+    // entries before e, four at a time where rows is 16-byte aligned
+    int64_t a = glo, b = e;
+    while (a < b) {
+      const int64_t mid = (a + b) >> 1;
+      if (cols[mid] < lo_col) a = mid + 1; else b = mid;
     }
+    uint32_t rank = 0;
+    int64_t j = a;
+    if ((reinterpret_cast<uintptr_t>(rows) & 15) == 0) {
+      for (; j < e && (j & 3); ++j) rank += rows[j] == r;
+      for (; j + 4 <= e; j += 4) {
+        const int4 q = __ldg(reinterpret_cast<const int4*>(rows + j));
+        rank += (q.x == r) + (q.y == r) + (q.z == r) + (q.w == r);
+      }
+    }
+    for (; j < e; ++j) rank += rows[j] == r;
     const int64_t u = ur / Cfg::RW;
     const int64_t rb = u / Cfg::NW;
     const int w = (int)(u % Cfg::NW);
