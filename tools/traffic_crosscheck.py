@@ -16,7 +16,7 @@ JSON line per sparsity with three predictions and the ncu measurement:
   = B tiles (CTAs x k x W x 4) + the record stream once per column tile;
   shared-memory wavefronts = B reads (4 per entry and column tile) + record
   loads (1 per record) + TMA tile writes (bytes / 128).
-* measured — ncu (profiles/r01_ncu_*.json, `--set full` of the same launch).
+* measured — ncu (profiles/r0X_ncu_*.json, `--set full` of the same launch).
 
     python tools/traffic_crosscheck.py profiles/r01_ncu_tacc28_s0.9.json \
         profiles/r01_ncu_tacc28_s0.99.json profiles/r01_ncu_tacc28_s0.995.json
@@ -41,10 +41,10 @@ def tiling(kernel_name):
     if m:
         v, kc, nw, epr = int(m.group(1)), int(m.group(2)), int(m.group(3) or 16), int(m.group(4) or 2)
         tcols = (512 // (nw // 4)) & ~7
-        return dict(RB=nw * (tcols // v), W=32 * v, KC=kc, EPR=epr)
+        return dict(RB=nw * (tcols // v), W=32 * v, KC=kc, EPR=epr, NW=nw)
     m = re.search(r"TileCfg<(\d+), (\d+),", kernel_name)
     v, kc = int(m.group(1)), int(m.group(2))
-    return dict(RB=15 * (64 // v), W=32 * v, KC=kc, EPR=2)
+    return dict(RB=15 * (64 // v), W=32 * v, KC=kc, EPR=3, NW=15)
 
 
 def pow2_at_least(x):
@@ -71,10 +71,18 @@ def main():
         dp = G.dense_to_gcoo_dev(a, pow2_at_least(t["RB"]))
         tmodel = G.model_traffic_dev(dp, N, G.ExecConfig(p=dp.p, b=t["W"]), infinite_l2=True)
         del a, dp
-        # this kernel: records hold up to EPR entries of one row per chunk (count them exactly)
+        # this kernel's records, counted exactly: three-entry records hold up to
+        # three entries of one row per chunk; two-entry records hold any two
+        # consecutive entries of a warp's stream (identity placement: row j of a
+        # row block belongs to warp j % NW), i.e. ceil(entries / 2) per warp and chunk
         rows = d.row_idx.long()
         cols = d.col_idx.long()
-        key = rows * ((N + t["KC"] - 1) // t["KC"]) + cols // t["KC"]
+        nch = (N + t["KC"] - 1) // t["KC"]
+        if t["EPR"] == 2:
+            unit = (rows // t["RB"]) * t["NW"] + (rows % t["RB"]) % t["NW"]
+            key = unit * nch + cols // t["KC"]
+        else:
+            key = rows * nch + cols // t["KC"]
         per_run = torch.bincount(key)
         records = int(((per_run + t["EPR"] - 1) // t["EPR"]).sum())
         col_tiles = (N + t["W"] - 1) // t["W"]
