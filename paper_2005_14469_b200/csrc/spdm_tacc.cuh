@@ -152,10 +152,11 @@ __device__ __forceinline__ uint32_t tacc_warp_records(const uint32_t* __restrict
 #pragma unroll 8
     for (int s = 0; s < Cfg::RW; ++s) r += p[s];
     return (r + 1) / 2;
-  }
+  } else {
 #pragma unroll 8
-  for (int s = 0; s < Cfg::RW; ++s) r += (p[s] + Cfg::EPR - 1) / Cfg::EPR;
-  return r;
+    for (int s = 0; s < Cfg::RW; ++s) r += (p[s] + Cfg::EPR - 1) / Cfg::EPR;
+    return r;
+  }
 }
 
 // P2: one warp per (rb, c): segment length (table + warp segments) and each
