@@ -1494,6 +1494,21 @@ void csr_to_gcoo_host(int64_t m, int64_t k, int32_t p, int64_t nnz, const T* val
 }
 
 // dense_to_gcoo on a device A: returns nnz; fills when capacity allows.
+// The count pass of a two-call protocol (nnz first, then the fill) kept for
+// the fill call on the same A, shape, p and stream: the second call then runs
+// only the fill (the host path's DenseStash does the same on the host side).
+struct DenseDevStash {
+  const void* A = nullptr;
+  int64_t m = 0, k = 0;
+  int32_t p = 0;
+  int elem = 0;
+  cudaStream_t s = nullptr;
+  int64_t nnz = -1, n_ct = 0, tiles = 0;
+  bool vec = false;
+  DevBuf<int64_t> off;
+};
+thread_local DenseDevStash t_dev_stash;
+
 template <typename T>
 int64_t dense_to_gcoo_device(int64_t m, int64_t k, int32_t p, const T* A, int64_t capacity, T* ovals,
                              int32_t* orows, int32_t* ocols, int64_t* gidx, int64_t* gnnz, cudaStream_t s) {
@@ -1502,28 +1517,50 @@ int64_t dense_to_gcoo_device(int64_t m, int64_t k, int32_t p, const T* A, int64_
   const int64_t groups = ceil_div(m, p);
   // 16-byte loads when every row starts 16-byte aligned
   constexpr int VEC = 16 / (int)sizeof(T);
-  const bool vec = k % VEC == 0 && (reinterpret_cast<uintptr_t>(A) % 16) == 0;
-  const int64_t n_ct = ceil_div(k, (int64_t)kDenseTileCols * (vec ? VEC : 1));
-  const int64_t tiles = groups * n_ct;
-  DevBuf<int64_t> counts(tiles, s), off(tiles + 1, s);
-  const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * 16);
-  if (vec)
-    GCOO_LAUNCH((dense_count_kernel<T, VEC>), grid, kDenseTileCols, 0, s, m, k, p, A, n_ct, tiles, counts.get());
-  else
-    GCOO_LAUNCH((dense_count_kernel<T, 1>), grid, kDenseTileCols, 0, s, m, k, p, A, n_ct, tiles, counts.get());
-  exclusive_scan(counts.get(), off.get(), tiles, s);
-  GCOO_LAUNCH(dense_groups_kernel, (unsigned)ceil_div(groups, 256), 256, 0, s, groups, n_ct, off.get(), gidx,
-              gnnz);
-  int64_t nnz = 0;
-  d2h(&nnz, off.get() + tiles, 1, s);
-  GCOO_CUDA(cudaStreamSynchronize(s));
-  if (nnz > 0 && capacity >= nnz && ovals) {
-    if (vec)
-      GCOO_LAUNCH((dense_fill_kernel<T, VEC>), grid, kDenseTileCols, 0, s, m, k, p, A, n_ct, tiles, off.get(),
-                  ovals, orows, ocols);
+  DenseDevStash& st = t_dev_stash;
+  const bool hit = st.nnz >= 0 && st.A == A && st.m == m && st.k == k && st.p == p && st.elem == (int)sizeof(T) &&
+                   st.s == s;
+  if (!(hit && ovals && capacity >= st.nnz)) {
+    st.nnz = -1;
+    st.vec = k % VEC == 0 && (reinterpret_cast<uintptr_t>(A) % 16) == 0;
+    st.n_ct = ceil_div(k, (int64_t)kDenseTileCols * (st.vec ? VEC : 1));
+    st.tiles = groups * st.n_ct;
+    DevBuf<int64_t> counts(st.tiles, s);
+    st.off = DevBuf<int64_t>(st.tiles + 1, s);
+    const int grid = (int)std::min<int64_t>(st.tiles, (int64_t)sm_count() * 16);
+    if (st.vec)
+      GCOO_LAUNCH((dense_count_kernel<T, VEC>), grid, kDenseTileCols, 0, s, m, k, p, A, st.n_ct, st.tiles,
+                  counts.get());
     else
-      GCOO_LAUNCH((dense_fill_kernel<T, 1>), grid, kDenseTileCols, 0, s, m, k, p, A, n_ct, tiles, off.get(),
-                  ovals, orows, ocols);
+      GCOO_LAUNCH((dense_count_kernel<T, 1>), grid, kDenseTileCols, 0, s, m, k, p, A, st.n_ct, st.tiles,
+                  counts.get());
+    exclusive_scan(counts.get(), st.off.get(), st.tiles, s);
+    int64_t nnz = 0;
+    d2h(&nnz, st.off.get() + st.tiles, 1, s);
+    GCOO_CUDA(cudaStreamSynchronize(s));
+    st.A = A;
+    st.m = m;
+    st.k = k;
+    st.p = p;
+    st.elem = (int)sizeof(T);
+    st.s = s;
+    st.nnz = nnz;
+  }
+  const int64_t nnz = st.nnz;
+  GCOO_LAUNCH(dense_groups_kernel, (unsigned)ceil_div(groups, 256), 256, 0, s, groups, st.n_ct, st.off.get(), gidx,
+              gnnz);
+  if (nnz > 0 && capacity >= nnz && ovals) {
+    const int grid = (int)std::min<int64_t>(st.tiles, (int64_t)sm_count() * 16);
+    if (st.vec)
+      GCOO_LAUNCH((dense_fill_kernel<T, VEC>), grid, kDenseTileCols, 0, s, m, k, p, A, st.n_ct, st.tiles,
+                  st.off.get(), ovals, orows, ocols);
+    else
+      GCOO_LAUNCH((dense_fill_kernel<T, 1>), grid, kDenseTileCols, 0, s, m, k, p, A, st.n_ct, st.tiles,
+                  st.off.get(), ovals, orows, ocols);
+  }
+  if (ovals && capacity >= nnz) {  // the protocol's second call: the stash is used up
+    st.nnz = -1;
+    st.off.release();
   }
   return nnz;
 }
