@@ -711,11 +711,18 @@ def cpu_baseline(g_host, b_host, n):
         # every host core, explicitly (torchrun exports OMP_NUM_THREADS=1)
         r = R.time_spdm(g, b_host, b=BW, workers=cores, warmup=1, reps=3)
         kc = r["kc_s"]
-        return {"value": round(2.0 * g.nnz * n / kc / 1e9, 3), "unit": "GFLOPS", "cores": int(r["workers"]),
-                "kind": "reference",
-                "sample": f"full workload (n={n}, nnz={g.nnz}): reference spdm_gcoo, median of 3 after 1 warmup, "
-                          f"OpenMP {r['workers']} threads, default-ISA build (as shipped, mul+add)",
-                "kc_seconds": kc, **cpu_description()}
+        out = {"value": round(2.0 * g.nnz * n / kc / 1e9, 3), "unit": "GFLOPS", "cores": int(r["workers"]),
+               "kind": "reference",
+               "sample": f"full workload (n={n}, nnz={g.nnz}): reference spdm_gcoo, median of 3 after 1 warmup, "
+                         f"OpenMP {r['workers']} threads, default-ISA build (as shipped, mul+add)",
+               "kc_seconds": kc, **cpu_description()}
+        try:  # BASELINE.md §3's optional second row: the FMA-contracted build (the GPU's exact bits)
+            rf = Reference(True).time_spdm(g, b_host, b=BW, workers=cores, warmup=1, reps=3)
+            out["fma_build"] = {"value": round(2.0 * g.nnz * n / rf["kc_s"] / 1e9, 3), "unit": "GFLOPS",
+                                "kc_seconds": rf["kc_s"], "build": "-mfma (FMA contraction), same sources"}
+        except Exception as e:  # noqa: BLE001
+            out["fma_build"] = {"error": str(e)[:120]}
+        return out
     return {"error": "oracle/_ref not built"}
 
 
