@@ -224,6 +224,13 @@ def make_inputs(G, n, s, seed, dev, b_seed):
     return a, b, dg, dB
 
 
+def head_start_cycles(steps):
+    """Device spin before a timed loop: ~2 ms per step at 1.965 GHz (a planned
+    call costs the host ~60-70 us to enqueue; a slow or shared host has been
+    seen to take ~1 ms, which would otherwise leak into the step times)."""
+    return int(4e6 * max(steps, 3))
+
+
 def time_kernel(G, dg, dB, dC, steps, warmup, stream, flush):
     """(mean ms per step, min ms, library launches in the timed region, mean ms
     of the multiply kernel itself) — CUDA events on `stream`, L2 flushed first.
@@ -239,14 +246,17 @@ def time_kernel(G, dg, dB, dC, steps, warmup, stream, flush):
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         l0 = G.launch_count()
         G.kernel_timing(kernel_events)
-        # the device sleeps ~5 ms first so the host queues the timed steps ahead of it:
-        # per-step device times then never include host enqueue latency
-        torch.cuda._sleep(int(1e7))
+        # the device sleeps first (~2 ms per timed step) so the host queues every
+        # timed step ahead of it: per-step device times then never include host
+        # enqueue latency, even on a slow or busy host
+        torch.cuda._sleep(head_start_cycles(steps))
+        h0 = time.perf_counter()
         for i in range(steps):
             flush.zero_()  # > L2 (126 MB): every timed launch starts cold
             starts[i].record(stream)
             G.spdm_gcoo_dev(dg, dB, dC, cfg, stream=stream)
             ends[i].record(stream)
+        time_kernel.host_enqueue_us = (time.perf_counter() - h0) / steps * 1e6
         torch.cuda.synchronize()
         launches = G.launch_count() - l0
         k_ms, k_n = G.kernel_time()
@@ -430,6 +440,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     with Clocks(local) as clk:
         ms_mean, ms_min, launches, kernel_ms = time_kernel(G, dg, dB, dC, args.steps, args.warmup, stream, flush)
+        host_enqueue_us = getattr(time_kernel, "host_enqueue_us", None)
     torch.cuda.synchronize()
     D.barrier()
     ms_mean, ms_min, kernel_ms = D.max(ms_mean, ms_min, kernel_ms)
@@ -463,7 +474,7 @@ def run_ours(args):
             torch.cuda.synchronize()
             evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                    for _ in range(args.steps)]
-            torch.cuda._sleep(int(1e7))
+            torch.cuda._sleep(head_start_cycles(args.steps))
             for e0, e1 in evs:
                 flush.zero_()
                 e0.record(stream)
@@ -633,6 +644,7 @@ def run_ours(args):
                          "path": "spdm_gcoo -> gcoo_spdm_f32 with pageable numpy buffers "
                                  "(what a C++ std::vector caller of the drop-in headers passes)"},
         "gpu_launches": int(launches),
+        "host_enqueue_us_per_step": None if host_enqueue_us is None else round(host_enqueue_us, 1),
         "plan_reuse": plan_reuse,
         "roofline": roofline,
         "roofline_hbm": roofline_hbm,
