@@ -943,7 +943,7 @@ bool host_pageable(const void* p) {
 // (staged = true): host threads pack B strips into page-locked buffers and
 // unpack C strips out of them while the DMA engines and the multiply work on
 // neighbouring strips.
-std::atomic<int> g_host_staging{1};  // test hook: 0 = let the driver stage pageable copies
+std::atomic<int> g_host_staging{std::getenv("GCOO_HOST_STAGING") ? std::atoi(std::getenv("GCOO_HOST_STAGING")) : 1};  // test hook: 0 = let the driver stage pageable copies
 
 int64_t pipeline_strip(int64_t m, int64_t k, int64_t n, bool pageable, bool staged) {
   const int want = g_pipeline_strips.load(std::memory_order_relaxed);
@@ -998,7 +998,8 @@ class HostPool {
  private:
   HostPool() {
     const unsigned hc = std::thread::hardware_concurrency();
-    const int nt = (int)std::max(1u, std::min(hc ? hc : 4u, 32u)) - 1;
+    int nt = (int)std::max(1u, std::min(hc ? hc : 4u, 32u)) - 1;
+    if (const char* e = std::getenv("GCOO_HOST_THREADS")) nt = std::max(0, std::atoi(e) - 1);  // measurement hook
     for (int i = 0; i < nt; ++i) workers_.emplace_back([this] { loop(); });
   }
   ~HostPool() {
