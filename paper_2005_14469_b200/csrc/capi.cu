@@ -967,8 +967,11 @@ std::vector<std::pair<int64_t, int64_t>> pipeline_strips(int64_t n, int64_t W) {
 
 // ------------------------------------------------ host staging (pageable) --
 // A process-wide pool of host threads for the strip pack/unpack copies (one
-// caller at a time; a pageable memcpy runs at ~1.5 GB/s per thread here, so
-// the copies need many threads to keep up with PCIe).
+// caller at a time; the strip copies move 2 KB pieces of 32 KB rows and run far
+// below the host's contiguous memcpy rate (~15 GB/s for one thread, ~75 GB/s
+// for eight, tools/host_memcpy_probe.py), so they need many threads to keep
+// up with PCIe; packing B and unpacking C as one pool job per strip was
+// measured and is no faster, profiles/r02_pageable_probe.log).
 class HostPool {
  public:
   static HostPool& get() {
